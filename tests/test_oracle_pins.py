@@ -1,0 +1,302 @@
+"""Pins the CPU oracle (oracle/phfem_oracle.c) before it is trusted:
+
+1. against the golden vectors of the reference's own tests
+   (tests/golden/reference_goldens.json, each entry citing its source), and
+2. against the reference library itself (oracle/_ref, compiled from
+   /root/reference/proj/src by oracle/Makefile): bit for bit on connectivity,
+   refinement, element blocks, C, the Schur matrix and the CG iterates.
+
+CPU only.  The coefficient extension is pinned against the reference with its
+element blocks patched identically (oracle/ref_driver.cpp).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle_bind import CheckerError, MeshArrays, RefCtx, cube5, ref_available
+
+needs_ref = pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+
+
+def refine_n(oracle, m, n):
+    for _ in range(n):
+        m = oracle.refine(m)[0]
+    return m
+
+
+# --------------------------------------------------------------------------
+# 1. golden vectors of the reference tests
+
+
+def test_edge_matrix_golden(oracle, goldens):
+    en, eos = oracle.edges(cube5())
+    assert len(en) == 18
+    lookup = np.zeros((8, 8), dtype=int)
+    for e, (a, b) in enumerate(en):
+        lookup[a, b] = lookup[b, a] = e + 1
+    assert lookup.tolist() == goldens["edge_matrix_8x8"]["value"]
+
+
+def test_single_tet_edges_golden(oracle, goldens):
+    m = MeshArrays(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float),
+                   np.array([[0, 1, 2, 3]], np.int32), np.zeros((0, 3), np.int32),
+                   np.array([[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]], np.int32))
+    en, _ = oracle.edges(m)
+    assert en.tolist() == goldens["single_tet_edges"]["value"]
+    ft = oracle.faces(m)
+    assert ft["nf"] == 4
+    own = m.tets[0][[[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]]
+    assert np.array_equal(ft["faces"], own)
+
+
+def test_cube_face_table_golden(oracle, goldens):
+    m = cube5()
+    ft = oracle.faces(m)
+    g = goldens["cube_face_table"]
+    assert (ft["nf"], ft["n_interior"], ft["n_dirichlet"], ft["n_neumann"], ft["l"]) == (
+        g["n_faces"], g["n_interior"], g["n_dirichlet"], g["n_neumann"], g["n_multipliers"])
+    assert ft["face_of_slot"][16] == g["slot16_face"] and ft["sigma"][16] == g["slot16_sigma"]
+    own = m.tets[0][[[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]]
+    assert np.array_equal(ft["faces"][:4], own)
+    interior = m.tets[4][[[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]]
+    for k, row in enumerate(goldens["cube_faces_up_interior_rows"]["value"]):
+        assert set(ft["faces"][row]) == set(interior[k])
+    fs = ft["face_slots"]
+    inter = fs[:, 1] >= 0
+    assert np.all(ft["sigma"][fs[inter, 0]] + ft["sigma"][fs[inter, 1]] == 0)
+    assert np.all(ft["sigma"][fs[~inter, 0]] == 1)
+
+
+def test_refine_counts_golden(oracle, goldens):
+    m = cube5()
+    table = goldens["refine_counts_ne_nc_ned_nf"]["value"]
+    dims = goldens["system_dims_n_l"]["value"]
+    lcounts = goldens["level_counts_ned_nf_l"]["value"]
+    for lv in range(4):
+        en, _ = oracle.edges(m)
+        ft = oracle.faces(m)
+        assert [m.ne, m.nc, len(en), ft["nf"]] == table[lv]
+        if lv >= 1:
+            assert [4 * m.ne, ft["l"]] == dims[lv - 1]
+            assert [len(en), ft["nf"], ft["l"]] == lcounts[lv - 1]
+        m = oracle.refine(m)[0]
+
+
+def test_single_tet_refine_golden(oracle, goldens):
+    g = goldens["single_tet_refine"]
+    m = MeshArrays(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float),
+                   np.array([[0, 2, 1, 3]], np.int32), np.zeros((0, 3), np.int32), np.zeros((0, 3), np.int32))
+    fine, mid, cen = oracle.refine(m)
+    assert fine.coords.tolist() == g["coords"]
+    assert (fine.tets + 1).tolist() == g["children"]
+    assert cen[0] == g["centroid_node"]
+
+
+def test_boundary_refine_golden(oracle, goldens):
+    fine = oracle.refine(cube5())[0]
+    g = goldens["boundary_refine_level1"]
+    assert (len(fine.db), len(fine.nb)) == (g["n_dirichlet"], g["n_neumann"])
+    rows = [0, 2, 3, 4]  # first Dirichlet parent's children (test_refine.cpp:80-86)
+    nodes = set(fine.db[rows].ravel())
+    assert len(nodes) == 6 and all(fine.coords[n][2] == 1.0 for n in nodes)
+
+
+def test_reference_tet_matrices_golden(oracle, goldens):
+    m = MeshArrays(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float),
+                   np.array([[0, 1, 2, 3]], np.int32), np.zeros((0, 3), np.int32),
+                   np.array([[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]], np.int32))
+    ft = oracle.faces(m)
+    sys_ = oracle.assemble(m, ft, kind=2, schur=False)
+    g = goldens["reference_tet_KM"]
+    expect = np.array(g["k_times_6"]) / 6.0 + np.array(g["m_times_120"]) / 120.0
+    np.testing.assert_allclose(sys_["a_blocks"][0], expect, rtol=1e-14, atol=1e-16)
+
+
+def test_cube_assembly_golden(oracle, goldens):
+    m = cube5()
+    ft = oracle.faces(m)
+    s = oracle.assemble(m, ft, kind=0, schur=False)
+    np.testing.assert_allclose(np.abs(s["slot_coef"][0, 0]), goldens["cube_slot0_C_row"]["value"][0], rtol=1e-14)
+    bd = s["bd"][ft["mrow"][ft["face_class"] == 1]]
+    np.testing.assert_allclose(bd, goldens["cube_dirichlet_bd"]["value"], rtol=1e-14)
+    # level 1: C rows carry 3 (Dirichlet) or 6 (interior) entries
+    m1 = oracle.refine(m)[0]
+    ft1 = oracle.faces(m1)
+    s1 = oracle.assemble(m1, ft1, kind=0)
+    nnz = np.diff(s1["c_rowptr"])
+    g = goldens["level1_C_rows"]
+    assert (np.sum(nnz == 3), np.sum(nnz == 6), len(nnz)) == (g["three"], g["six"], 104)
+
+
+def test_level1_errors_golden(oracle, goldens):
+    m = oracle.refine(cube5())[0]
+    ft = oracle.faces(m)
+    s = oracle.assemble(m, ft, kind=0)
+    u, lam, st = oracle.solve(m, s, kind=0)
+    assert st["residual"] <= 1e-10 and st["constraint_residual"] <= 1e-9
+    ey, ek, _ = oracle.errors(m, ft, u, lam, kind=0)
+    g = goldens["level1_errors"]
+    assert ey == pytest.approx(g["err_u"], rel=1e-6)
+    assert ek == pytest.approx(g["err_kappa"], rel=1e-6)
+
+
+def test_patch_and_zero_golden(oracle):
+    for lv in (1, 2):
+        m = refine_n(oracle, cube5(), lv)
+        ft = oracle.faces(m)
+        s = oracle.assemble(m, ft, kind=1)
+        u, lam, st = oracle.solve(m, s, kind=1, tol=1e-12)
+        exact = m.coords[m.tets] @ np.array([1.0, 2.0, 3.0]) + 4.0
+        assert np.abs(u - exact.ravel()).max() <= 1e-9
+        ey, ek, el2 = oracle.errors(m, ft, u, lam, kind=1)
+        assert ey <= 1e-9 and ek <= 1e-9
+    m = oracle.refine(cube5())[0]
+    ft = oracle.faces(m)
+    s = oracle.assemble(m, ft, kind=2)
+    u, lam, st = oracle.solve(m, s, kind=2)
+    assert st["iterations"] == 0 and np.all(u == 0) and np.all(lam == 0)
+    s = oracle.assemble(m, ft, kind=0)
+    with pytest.raises(CheckerError) as e:
+        oracle.solve(m, s, kind=0, max_iter=2)
+    assert e.value.code == 3
+
+
+def test_dirichlet_flux_golden(oracle, goldens):
+    m = refine_n(oracle, cube5(), 3)
+    ft = oracle.faces(m)
+    s = oracle.assemble(m, ft, kind=0)
+    u, lam, st = oracle.solve(m, s, kind=0)
+    dir_f = np.nonzero(ft["face_class"] == 1)[0]
+    tri = m.coords[ft["faces"][dir_f]]
+    n = np.cross(tri[:, 2] - tri[:, 0], tri[:, 1] - tri[:, 0])
+    n /= np.linalg.norm(n, axis=1)[:, None]
+    c = tri.mean(axis=1)
+    grad = np.stack([2 * c[:, 0] * c[:, 1] ** 2 * c[:, 2] ** 2, 2 * c[:, 0] ** 2 * c[:, 1] * c[:, 2] ** 2,
+                     2 * c[:, 0] ** 2 * c[:, 1] ** 2 * c[:, 2]], axis=1)
+    d = lam[ft["mrow"][dir_f]] - np.sum(grad * n, axis=1)
+    g = goldens["level3_dirichlet_flux"]
+    assert len(dir_f) == g["count"] and math.sqrt(np.mean(d * d)) <= g["rms_max"]
+
+
+def test_error_paths(oracle):
+    m = cube5()
+    bad = MeshArrays(m.coords, m.tets, m.db, np.vstack([m.nb, [[7, 2, 1]]]).astype(np.int32))
+    with pytest.raises(CheckerError, match="interior"):
+        oracle.faces(bad)
+    bad = MeshArrays(m.coords, m.tets, m.db, np.vstack([m.nb, [[0, 1, 6]]]).astype(np.int32))
+    with pytest.raises(CheckerError, match="matches no element face"):
+        oracle.faces(bad)
+    bad = MeshArrays(m.coords, m.tets, m.db, m.nb[:-1].copy())
+    with pytest.raises(CheckerError, match="neither"):
+        oracle.faces(bad)
+    bad = MeshArrays(m.coords, m.tets, m.db, np.vstack([m.nb, m.db[:1]]).astype(np.int32))
+    with pytest.raises(CheckerError, match="listed twice"):
+        oracle.faces(bad)
+    dup = MeshArrays(m.coords, np.vstack([m.tets[:1], m.tets[:1]]).astype(np.int32), m.db, m.nb)
+    with pytest.raises(CheckerError, match="claim the same oriented face"):
+        oracle.faces(dup)
+
+
+# --------------------------------------------------------------------------
+# 2. against the reference library itself
+
+
+def _kuhn_coef(oracle, kind, n):
+    if kind == 4:
+        m = oracle.kuhn(n, n, n, jitter=0.2, seed=2509, dmask=0x3)
+        a = 10.0 ** (4.0 * np.array([oracle.uniform(11133, t) for t in range(m.ne)]) - 2.0)
+        return m, dict(a_elem=a)
+    if kind == 5:
+        m = oracle.kuhn(4 * n, n, n, lx=8.0, dmask=0x1)
+        ch = np.array([oracle.uniform(11133, t) < 0.5 for t in range(m.ne)])
+        ad = np.where(ch[:, None], [1.0, 1.0, 100.0], [100.0, 1.0, 1.0])
+        return m, dict(a_diag=np.ascontiguousarray(ad))
+    return oracle.kuhn(n, n, n, dmask=0x10 if kind == 3 else 0x3F), {}
+
+
+CASES = [("cube", 0, 0), ("cube", 1, 0), ("cube", 2, 0), ("cube", 3, 0), ("kuhn", 3, 4), ("kuhn", 4, 8),
+         ("kuhn", 5, 4), ("kuhn-c0", 3, 3)]
+
+
+@needs_ref
+@pytest.mark.parametrize("name,arg,n", CASES)
+def test_oracle_matches_reference(oracle, name, arg, n):
+    coef, kind, c = {}, 0, 1.0
+    if name == "cube":
+        m = refine_n(oracle, cube5(), arg)
+    elif name == "kuhn-c0":
+        m, kind, c = oracle.kuhn(n, n, n, dmask=0x10), 3, 1.0
+    else:
+        kind = arg
+        m, coef = _kuhn_coef(oracle, kind, n)
+    r = RefCtx(m)
+    r.connectivity()
+    en_r, eos_r = r.edges()
+    en_o, eos_o = oracle.edges(m)
+    assert np.array_equal(en_r, en_o) and np.array_equal(eos_r, eos_o)
+    kr, er = r.e2t()
+    ko, eo = oracle.e2t(m)
+    assert np.array_equal(kr, ko) and np.array_equal(er, eo)
+    fr, fo = r.faces(), oracle.faces(m)
+    for k in ("faces", "face_of_slot", "sigma", "face_slots", "face_class", "mrow", "area"):
+        assert np.array_equal(fr[k], fo[k]), k
+    r.set_coefficients(coef.get("a_elem"), coef.get("a_diag"), c)
+    sr = r.assemble(kind)
+    so = oracle.assemble(m, fo, kind, c, coef.get("a_elem"), coef.get("a_diag"))
+    for k in ("a_blocks", "slot_coef", "slot_mrow", "rhs", "bd", "c_rowptr", "c_col", "c_val"):
+        assert np.array_equal(sr[k], so[k]), k
+    hr = r.build_schur(1)
+    for k in ("s_rowptr", "s_col", "s_val", "rhs_neg"):
+        assert np.array_equal(hr[k], so[k]), k
+    if m.ne <= 3000:
+        tol = 1e-10
+        outs = []
+        for fn in (lambda: r.solve(tol=tol), lambda: oracle.solve(m, so, kind, c, coef.get("a_elem"),
+                                                                  coef.get("a_diag"), tol=tol)):
+            try:
+                outs.append(fn())
+            except CheckerError as e:  # the reference may refuse a converged solve (SURVEY finding 8)
+                outs.append(e.code)
+        if isinstance(outs[0], int):
+            assert outs[1] == outs[0]
+        else:
+            (ur, lr, str_), (uo, lo, sto) = outs
+            assert str_["iterations"] == sto["iterations"]
+            assert np.array_equal(ur, uo) and np.array_equal(lr, lo)
+            if not coef:
+                np.testing.assert_array_equal(r.errors(), oracle.errors(m, fo, uo, lo, kind, c))
+
+
+@needs_ref
+def test_refine_matches_reference(oracle):
+    for m in (cube5(), oracle.kuhn(1, 1, 1), oracle.kuhn(3, 2, 2, jitter=0.2, dmask=0x5)):
+        for _ in range(2):
+            mo, mid_o, cen_o = oracle.refine(m)
+            r = RefCtx(m)
+            mid_r, cen_r, _ = r.refine()
+            mr = r.mesh()
+            for k in ("coords", "tets", "db", "nb"):
+                assert np.array_equal(getattr(mo, k), getattr(mr, k)), k
+            assert np.array_equal(mid_o, mid_r) and np.array_equal(cen_o, cen_r)
+            m = mo
+
+
+def test_c_zero_is_singular(oracle):
+    """c = 0 (configs 1/4 as written) has no element-local Schur complement:
+    the reference raises 'degenerate element block' (SURVEY finding 2)."""
+    m = oracle.kuhn(2, 2, 2, dmask=0x3F)
+    ft = oracle.faces(m)
+    with pytest.raises(CheckerError, match="degenerate element block"):
+        oracle.assemble(m, ft, kind=3, c=0.0)
+
+
+def test_kuhn_generator_properties(oracle):
+    m = oracle.kuhn(3, 4, 5, lx=2.0, ly=1.0, lz=0.5, jitter=0.2, seed=2509, dmask=0x21)
+    p = m.coords[m.tets]
+    det = np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0])
+    assert np.all(det > 0)
+    vol = (det / 6).sum()
+    assert vol == pytest.approx(1.0, rel=1e-12)
+    ft = oracle.faces(m)  # classification succeeds: boundary lists are complete and outward
+    assert ft["n_dirichlet"] == len(m.db) and ft["n_neumann"] == len(m.nb)
