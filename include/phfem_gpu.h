@@ -1,0 +1,234 @@
+/* phfem_gpu.h — the thin C ABI between the host runtime (capi.cpp) and the
+ * sm_100a kernels of the phfem hot path.
+ *
+ * Every entry point takes device pointers, sizes and a cudaStream_t (passed
+ * as void*), launches kernels on that stream and returns without
+ * synchronising.  None allocates memory: the host runtime sizes every buffer
+ * (reading back the few device counts it needs) and owns it.
+ *
+ * Each launcher names the reference function whose semantics it implements
+ * (paths relative to /root/reference/proj/src).  Layout conventions (device):
+ *   coords  double[3 nC]  (x,y,z per node, AoS: one 24-byte gather per vertex)
+ *   tets    int32[4 nE]   (16-byte aligned, loaded as int4)
+ *   db, nb  int32[3 n]    boundary triangles, outward oriented
+ *   slot    s = 4t+k for faces, 6t+k for edges (element-major)
+ *   S       SELL-32, width 7, column-major within each 32-row chunk:
+ *           entry (row, pos) at (row/32)*224 + pos*32 + row%32; pos 0 is the
+ *           diagonal, 1-3 the other faces of the owner element, 4-6 those of
+ *           the second element; padding has col == row and value 0.
+ */
+#ifndef PHFEM_GPU_H
+#define PHFEM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error slots of the device error vector (unsigned long long[PHG_ERR_COUNT],
+ * initialised to all ones); each keeps the minimum offending key. */
+enum phg_err_slot {
+    PHG_ERR_DUP_ORIENT = 0,  /* key = t1<<32 | t2: two elements claim one oriented face (connectivity.cpp:62-68) */
+    PHG_ERR_CLASSIFY = 1,    /* key = entry<<2 | kind (0 no match, 1 listed twice, 2 interior) (connectivity.cpp:156-175) */
+    PHG_ERR_FACE = 2,        /* key = face<<2 | kind (0 degenerate, 1 unclassified boundary) (connectivity.cpp:177-194, mesh.cpp:80-82) */
+    PHG_ERR_ZERO_VOLUME = 3, /* key = element (assembly.cpp:13-14) */
+    PHG_ERR_SINGULAR = 4,    /* key = element (solver.cpp:103-109, 128-129) */
+    PHG_ERR_BOUNDARY_EDGE = 5, /* key = (list index)<<2 | pair (refine.cpp:80-85) */
+    PHG_ERR_VALENCE = 6,     /* key = vertex: star larger than the supported maximum */
+    PHG_ERR_COUNT = 7
+};
+
+#define PHG_SELL_C 32
+#define PHG_SELL_W 7
+
+/* Problem data (oracle/problems.h restates the same formulas on the CPU). */
+typedef struct phg_problem {
+    int kind;              /* 0 manufactured, 1 linear, 2 zero, 3 sin3, 4 expcos, 5 polysin */
+    double c;              /* reaction coefficient */
+    const double* a_elem;  /* device [nE] scalar diffusion, or NULL */
+    const double* a_diag;  /* device [3 nE] diagonal diffusion, or NULL (wins) */
+} phg_problem;
+
+/* ---------------------------------------------------------------- scans */
+/* Exclusive scan of n int32 counts into int64 offsets (out[n] = total).
+ * scratch needs phfem_gpu_scan_scratch(n) bytes. */
+size_t phfem_gpu_scan_scratch(int64_t n);
+int phfem_gpu_scan_i32(const int32_t* in, int64_t* out, int64_t n, void* scratch, void* stream);
+
+/* ------------------------------------------------------------ mesh input */
+/* Kuhn mesh generator (oracle: or_kuhn_mesh). */
+int phfem_gpu_kuhn_nodes(int nx, int ny, int nz, double lx, double ly, double lz, double jitter,
+                         uint64_t seed, double* coords, void* stream);
+/* tets + per-element boundary-face counts packed (nDir | nNeu<<8) */
+int phfem_gpu_kuhn_tets(int nx, int ny, int nz, uint32_t dirichlet_mask, int32_t* tets,
+                        int32_t* bcount, void* stream);
+/* boundary lists in element/slot order from the exclusive scans of the
+ * Dirichlet and Neumann counts */
+int phfem_gpu_kuhn_boundary(int nx, int ny, int nz, uint32_t dirichlet_mask, const int32_t* tets,
+                            const int64_t* dir_off, const int64_t* neu_off, int32_t* db,
+                            int32_t* nb, void* stream);
+int phfem_gpu_split_counts(const int32_t* packed, int32_t* dir, int32_t* neu, int64_t n, void* stream);
+
+/* max element diameter (mesh.cpp:90-106); out: one double (device) */
+int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, double* out,
+                       double* partials, void* stream);
+
+/* -------------------------------------------------------- connectivity */
+/* vertex -> (element, local vertex) incidence ("star"), CSR by vertex */
+int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream);
+int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_t* star,
+                        void* stream);
+
+/* Per vertex v, group the edges (v,b), b>v and the faces whose smallest
+ * vertex is v among the incident element slots: edge_first[6t+k] = smallest
+ * slot of the edge (first occurrence, connectivity.cpp:22-37); slot_mate[4t+k]
+ * = the other slot of the face or -1 (faces_up/full_face_table,
+ * connectivity.cpp:72-153).  Either output may be NULL to skip that part.
+ * Vertices with stars larger than the fast path's limit are appended to
+ * big_list (device int32, count in big_count) and handled by
+ * phfem_gpu_star_groups_big. */
+int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star,
+                          const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
+                          int32_t* big_list, int32_t* big_count, unsigned long long* err,
+                          void* stream);
+int phfem_gpu_star_groups_big(int32_t n_big, const int32_t* big_list, const int64_t* star_ptr,
+                              const int32_t* star, const int32_t* tets, int32_t* edge_first,
+                              int32_t* slot_mate, int max_star, unsigned long long* err,
+                              void* stream);
+
+/* Per element counts of first-occurrence edges (low 8 bits) and owned faces
+ * (next 8 bits): packed[t]. */
+int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
+                             int32_t* edge_count, int32_t* face_count, void* stream);
+
+/* Numbering of first-occurrence edges and owned faces from the exclusive
+ * offsets (edge ids = rank of the first slot; face ids = rank of the owner
+ * slot, the faces_up order).  Writes the owner-side entries; the others are
+ * filled by phfem_gpu_fill_slots.  Any output group may be NULL. */
+int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords,
+                     const int32_t* edge_first, const int64_t* edge_off, int32_t* edge_of_slot,
+                     int32_t* edge_nodes, const int32_t* slot_mate, const int64_t* face_off,
+                     int32_t* face_of_slot, int8_t* sigma, int32_t* faces, int32_t* face_slots,
+                     double* face_area, unsigned long long* err, void* stream);
+int phfem_gpu_fill_slots(int64_t ne, const int32_t* edge_first, int32_t* edge_of_slot,
+                         const int32_t* slot_mate, int32_t* face_of_slot, int8_t* sigma,
+                         void* stream);
+
+/* Boundary classification (connectivity.cpp:156-175): entries of db then nb
+ * are matched through the star of their smallest vertex. */
+int phfem_gpu_classify(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
+                       const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                       const int32_t* face_of_slot, const int32_t* face_slots, uint32_t* claim,
+                       unsigned long long* err, void* stream);
+int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
+                             const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                             const int32_t* face_of_slot, const uint32_t* claim,
+                             unsigned long long* err, void* stream);
+/* face classes + non-Neumann flags (connectivity.cpp:177-201); claim[f] is
+ * the first list entry naming face f (all ones: none);
+ * counts[3] += interior, dirichlet, neumann (device int64) */
+int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const int32_t* face_slots,
+                         const double* face_area, uint8_t* face_class, int32_t* is_row,
+                         unsigned long long* counts, unsigned long long* err, void* stream);
+/* multiplier rows from the exclusive scan of is_row (rank among
+ * non-Neumann faces) and the inverse map row -> face */
+int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const int64_t* row_off,
+                        int32_t* face_mrow, int32_t* row_face, void* stream);
+
+/* ----------------------------------------------------------- refinement */
+/* red_refine (refine.cpp:16-74): one thread per parent; child 0 at row t,
+ * children 1..11 at rows nE + 11t + q-1; new nodes by the closed form
+ * centroid(t) = nC + t + E_t, midpoint(e) = nC + firstElem(e) + 1 + e.
+ * coords_out must hold nC + nEd + nE nodes; the first nC are copied. */
+int phfem_gpu_refine(int64_t nc, int64_t ne, const double* coords, const int32_t* tets,
+                     const int32_t* edge_first, const int32_t* edge_of_slot,
+                     const int64_t* edge_off, double* coords_out, int32_t* tets_out,
+                     int32_t* midpoint_node, int32_t* centroid_node, void* stream);
+/* refine_boundary_faces (refine.cpp:76-96) over one list; list_base offsets
+ * the error key (0 for db, nd for nb). */
+int phfem_gpu_refine_boundary(int64_t nf, const int32_t* faces, int64_t list_base, int64_t nc,
+                              const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                              const int32_t* edge_first, const int32_t* edge_of_slot,
+                              int32_t* out, unsigned long long* err, void* stream);
+
+/* ------------------------------------------------- assembly + condensation */
+/* Upload tet_rule(5) and tet_rule(9) (quadrature.cpp:36-62), built on the
+ * host exactly like the reference, into constant memory. */
+int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const double* lam9,
+                        const double* w9, int n9);
+
+/* Fused assemble_system + build_schur local part (assembly.cpp:7-138,
+ * solver.cpp:90-127) with the direct scatter into SELL S and rhs_neg.
+ * sell_val's diagonal slots and rhs_neg must be zeroed first.  Optional
+ * debug outputs (may be NULL): a_blocks [16 nE], slot_coef [4 nE],
+ * slot_mrow [4 nE].  rhs [4 nE] (= b + LN) is always written (recovery).
+ * norms [2] (device) receive sum(rhs^2), sum(bd^2) partials, reduced
+ * deterministically through partials[grid]. */
+int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
+                                const phg_problem* prob, const int32_t* face_of_slot,
+                                const int32_t* slot_mate, const int32_t* face_mrow,
+                                const double* face_area, int32_t* sell_col, double* sell_val,
+                                double* rhs_neg, double* bd, double* rhs, double* a_blocks,
+                                double* slot_coef, int32_t* slot_mrow, double* norms,
+                                double* partials, unsigned long long* err, void* stream);
+int phfem_gpu_assemble_grid(int64_t ne);
+
+/* --------------------------------------------------------------- solver */
+typedef struct phg_cg_state {
+    double rz, pq, alpha, beta, rnorm, bnorm, stop, rel_residual;
+    long long it, max_iter;
+    int done, converged, not_spd, pad;
+    unsigned int counter[4];
+} phg_cg_state;
+
+/* Jacobi-PCG on S (pcg_jacobi, sparse.cpp:163-212; stopping rule of
+ * inner_cg_options, solver.cpp:78-86).  cg_init sets x=0, r=b, z=d r, p=z,
+ * d = 1/diag (1 where the diagonal is 0), computes ||b|| and the stop
+ * level from tol, abs_tol (<= 0 means none) and max_iter.  cg_iterations
+ * enqueues n iterations (kernels turn into no-ops once done). */
+int phfem_gpu_cg_init(int64_t l, const int32_t* sell_col, const double* sell_val, const double* b,
+                      double* x, double* r, double* p, double* d, double tol, double abs_tol,
+                      long long max_iter, phg_cg_state* st, double* partials, void* stream);
+int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col, const double* sell_val,
+                            double* x, double* r, double* p, double* q, const double* d,
+                            phg_cg_state* st, double* partials, void* stream);
+
+/* Element-local recovery U_T = A_T^-1 (B_T + C_T' Lambda_T) (solver.cpp:168-181)
+ * fused with the primal block residual of verify_solution (solver.cpp:44-53):
+ * sums [0] += ||A U - rhs - C' Lambda||^2. */
+int phfem_gpu_recover(int64_t ne, const double* coords, const int32_t* tets,
+                      const phg_problem* prob, const int32_t* face_of_slot,
+                      const int32_t* slot_mate, const int32_t* face_mrow,
+                      const double* face_area, const double* rhs, const double* lambda,
+                      double* u, double* sums, double* partials, unsigned long long* err,
+                      void* stream);
+/* Constraint residual r2 = C U - b_D per multiplier row (solver.cpp:54-62):
+ * out[0] = ||r2||^2, out[1] = max|r2|, out[2] = max|b_D| */
+int phfem_gpu_constraint_residual(int64_t l, const int32_t* row_face, const int32_t* face_slots,
+                                  const int32_t* slot_mate, const int32_t* face_of_slot,
+                                  const double* face_area, const int32_t* tets, const double* u,
+                                  const double* bd, double* out, double* partials, void* stream);
+
+/* Error norms (analysis.cpp:51-105 + L2 extension): out [y^2, kappa^2, l2^2] */
+int phfem_gpu_errors(int64_t ne, const double* coords, const int32_t* tets,
+                     const phg_problem* prob, const int32_t* face_of_slot,
+                     const int32_t* slot_mate, const int32_t* face_mrow, const double* u,
+                     const double* lambda, double h, double* out, double* partials,
+                     void* stream);
+
+/* SELL -> CSR export of S for parity checks (host orchestrated; dense rows
+ * sorted by column, padding dropped). row_nnz [L] */
+int phfem_gpu_sell_row_nnz(int64_t l, const int32_t* sell_col, int32_t* row_nnz, void* stream);
+int phfem_gpu_sell_to_csr(int64_t l, const int32_t* sell_col, const double* sell_val,
+                          const int64_t* row_ptr, int32_t* col, double* val, void* stream);
+
+/* last CUDA error as text (for the host runtime's messages) */
+const char* phfem_gpu_error_string(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

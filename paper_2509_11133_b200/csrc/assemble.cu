@@ -1,0 +1,275 @@
+// Fused assembly + element-local Schur condensation, one thread per element
+// (assemble_system, assembly.cpp:7-138, and the local part of build_schur,
+// solver.cpp:90-127), scattering straight into the SELL-32 Schur matrix.
+//
+// Per element the thread builds A_T = K_T(A) + c M_T, the C_T rows
+// sigma*|F|/3, the Gauss-64 load vector plus the Neumann terms (B_T), the
+// Dirichlet data, the partial-pivot LU of A_T, S_T = C A^-1 C' and
+// r_T = C A^-1 B, all in registers with the reference's operation order.
+// Nothing element-sized besides B_T (kept for the recovery) is written back.
+//
+// Scatter (each S entry has one contribution except interior diagonals,
+// which have two; a two-term sum is order free, so atomics stay exact):
+//   row R of face f, owner slot -> positions 0 (diag, atomic), 1-3
+//   second slot               -> positions 0 (diag, atomic), 4-6
+//   rhs_neg[R] = b_D - r_T (Dirichlet) or -(r_T1 + r_T2) via two atomics.
+#include <cuda_runtime.h>
+
+#include "problems.cuh"
+
+namespace phg {
+__constant__ double c_lam5[64 * 4];
+__constant__ double c_w5[64];
+}  // namespace phg
+
+extern "C" int phfem_gpu_set_rules_errors(const double* lam9, const double* w9);
+
+namespace {
+
+using namespace phg;
+
+constexpr int kAsmThreads = 128;
+
+__device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
+    return (row >> 5) * (PHG_SELL_C * PHG_SELL_W) + pos * PHG_SELL_C + (row & 31);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = add(s, sh[i]);
+    return s;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kAsmThreads)
+    assemble_condense(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets,
+                      phg_problem prob, const int32_t* __restrict__ face_of_slot,
+                      const int32_t* __restrict__ slot_mate, const int32_t* __restrict__ face_mrow,
+                      const double* __restrict__ face_area, int32_t* __restrict__ sell_col,
+                      double* __restrict__ sell_val, double* __restrict__ rhs_neg, double* __restrict__ bd,
+                      double* __restrict__ rhs_out, double* __restrict__ a_blocks, double* __restrict__ slot_coef,
+                      int32_t* __restrict__ slot_mrow, double* __restrict__ partials, unsigned long long* err) {
+    __shared__ double sh[kAsmThreads / 32];
+    double acc_rhs = 0.0, acc_bd = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 e = ldtet(tets, t);
+        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+        const Coef k = load_coef(prob, t);
+        Local L;
+        local_matrices(p, k, L);
+        if (L.degenerate) {
+            report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
+            continue;
+        }
+        // slot data: multiplier row, C_T entry (assembly.cpp:121-126)
+        const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
+        int32_t row[4];
+        double coef[4];
+        bool owner[4], bnd[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int32_t s = (int32_t)(4 * t + q);
+            const int32_t mate = tv(mate4, q);
+            const int32_t f = tv(fos4, q);
+            row[q] = __ldg(face_mrow + f);
+            owner[q] = mate < 0 || mate > s;
+            bnd[q] = mate < 0;
+            const double sg = owner[q] ? 1.0 : -1.0;
+            coef[q] = dvd(mul(sg, __ldg(face_area + f)), 3.0);
+        }
+        if (a_blocks) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a_blocks[16 * t + 4 * i + j] = L.a[i][j];
+        }
+        if (slot_coef) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) slot_coef[4 * t + q] = coef[q];
+        }
+        if (slot_mrow) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = row[q];
+        }
+
+        // load vector, Gauss branch (assembly.cpp:64-78)
+        double b[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+        for (int qp = 0; qp < 64; ++qp) {
+            const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2], l3 = c_lam5[4 * qp + 3];
+            const V3 x = vadd(vadd(vadd(vmul(p[0], l0), vmul(p[1], l1)), vmul(p[2], l2)), vmul(p[3], l3));
+            const double fw = mul(mul(L.vol, c_w5[qp]), prob_f<KIND>(x.x, x.y, x.z, k));
+            b[0] = add(b[0], mul(fw, l0));
+            b[1] = add(b[1], mul(fw, l1));
+            b[2] = add(b[2], mul(fw, l2));
+            b[3] = add(b[3], mul(fw, l3));
+        }
+        // Neumann (assembly.cpp:81-94) and Dirichlet (96-104) face data
+        double ln[4] = {0.0, 0.0, 0.0, 0.0};
+        double bdv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!bnd[q]) continue;
+            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+            const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
+            const V3 cen = vdiv(vadd(vadd(q0, q1), q2), 3.0);
+            if (row[q] < 0) {
+                const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+                const double len = __dsqrt_rn(vdot(n, n));
+                const double ar = mul(0.5, len);
+                const V3 un = vdiv(n, len);
+                const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+                const double contrib = dvd(mul(ar, gc), 3.0);
+                ln[i0] = add(ln[i0], contrib);
+                ln[i1] = add(ln[i1], contrib);
+                ln[i2] = add(ln[i2], contrib);
+            } else {
+                bdv[q] = mul(__ldg(face_area + tv(fos4, q)), prob_u<KIND>(cen.x, cen.y, cen.z));
+            }
+        }
+        double rhs[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            rhs[v] = add(b[v], ln[v]);
+            acc_rhs = add(acc_rhs, mul(rhs[v], rhs[v]));
+        }
+        reinterpret_cast<double2*>(rhs_out)[2 * t] = make_double2(rhs[0], rhs[1]);
+        reinterpret_cast<double2*>(rhs_out)[2 * t + 1] = make_double2(rhs[2], rhs[3]);
+
+        // local Schur complement (solver.cpp:101-127)
+        Lu4 lu;
+        lu_factor(L.a, lu);
+        if (lu.singular) {
+            report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
+            continue;
+        }
+        double cr[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const bool on = row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
+                cr[r][v] = on ? coef[r] : 0.0;
+            }
+        double ainv_c[4][4], ainv_b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) lu_solve(lu, cr[q], ainv_c[q]);
+        lu_solve(lu, rhs, ainv_b);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (row[r] < 0) continue;
+            double rb = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr[r][pp], ainv_b[pp]));
+            const int64_t R = row[r];
+            const int base = owner[r] ? 0 : 3;
+            int j = 1;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double s = 0.0;
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr[r][pp], ainv_c[q][pp]));
+                if (q == r) {
+                    atomicAdd(sell_val + sell_idx(R, 0), s);
+                    sell_col[sell_idx(R, 0)] = (int32_t)R;
+                } else {
+                    const int64_t ix = sell_idx(R, base + j);
+                    ++j;
+                    if (row[q] >= 0) {
+                        sell_col[ix] = row[q];
+                        sell_val[ix] = s;
+                    } else {
+                        sell_col[ix] = (int32_t)R;
+                        sell_val[ix] = 0.0;
+                    }
+                }
+            }
+            if (bnd[r]) {
+#pragma unroll
+                for (int pos = 4; pos < 7; ++pos) {
+                    sell_col[sell_idx(R, pos)] = (int32_t)R;
+                    sell_val[sell_idx(R, pos)] = 0.0;
+                }
+                // rhs_neg = b_D - r_T (solver.cpp:131-138), single contributor
+                rhs_neg[R] = sub(bdv[r], rb);
+                bd[R] = bdv[r];
+                acc_bd = add(acc_bd, mul(bdv[r], bdv[r]));
+            } else {
+                atomicAdd(rhs_neg + R, -rb);
+            }
+        }
+    }
+    // deterministic block partials of ||rhs||^2 and ||b_D||^2
+    const double s0 = block_sum(acc_rhs, sh);
+    const double s1 = block_sum(acc_bd, sh);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = s0;
+        partials[2 * blockIdx.x + 1] = s1;
+    }
+}
+
+__global__ void reduce_pairs(const double* __restrict__ partials, int n, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        a = add(a, partials[2 * i]);
+        b = add(b, partials[2 * i + 1]);
+    }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) {
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+}  // namespace
+
+extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const double* lam9, const double* w9,
+                                   int n9) {
+    if (n5 != 64 || n9 != 216) return (int)cudaErrorInvalidValue;
+    cudaMemcpyToSymbol(phg::c_lam5, lam5, sizeof(double) * 4 * 64);
+    cudaMemcpyToSymbol(phg::c_w5, w5, sizeof(double) * 64);
+    const int rc = (int)cudaGetLastError();
+    return rc ? rc : phfem_gpu_set_rules_errors(lam9, w9);
+}
+
+extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
+    const int g = grid_for(ne, kAsmThreads);
+    return g < kSMs * 16 ? g : kSMs * 16;
+}
+
+extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
+                                           const phg_problem* prob, const int32_t* face_of_slot,
+                                           const int32_t* slot_mate, const int32_t* face_mrow,
+                                           const double* face_area, int32_t* sell_col, double* sell_val,
+                                           double* rhs_neg, double* bd, double* rhs, double* a_blocks,
+                                           double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
+                                           unsigned long long* err, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int grid = phfem_gpu_assemble_grid(ne);
+    const phg_problem p = *prob;
+#define PHG_ASM(K)                                                                                             \
+    assemble_condense<K><<<grid, kAsmThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, \
+                                                      face_area, sell_col, sell_val, rhs_neg, bd, rhs, a_blocks,   \
+                                                      slot_coef, slot_mrow, partials, err)
+    switch (p.kind) {
+        case 0: PHG_ASM(0); break;
+        case 1: PHG_ASM(1); break;
+        case 2: PHG_ASM(2); break;
+        case 3: PHG_ASM(3); break;
+        case 4: PHG_ASM(4); break;
+        case 5: PHG_ASM(5); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+#undef PHG_ASM
+    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms);
+    return (int)cudaGetLastError();
+}

@@ -1,0 +1,220 @@
+// Jacobi-preconditioned CG on the SELL-32 Schur matrix (pcg_jacobi,
+// sparse.cpp:163-212, with the stopping rule of inner_cg_options,
+// solver.cpp:78-86).  Three kernels per iteration:
+//   spmv   q = S p, partial p.q; last block: alpha = rz / pq
+//   update x += alpha p, r -= alpha q, z = d r, partials r.r, r.z;
+//          last block: stop test, beta = rz'/rz
+//   pdir   p = d r + beta p
+// Scalars live in device memory (phg_cg_state); kernels become no-ops once
+// `done` is set, so the host can enqueue batches of iterations (captured in
+// a CUDA graph) and poll rarely.  Every reduction is a fixed-shape tree over
+// fixed-grid block partials finished by the last block to arrive, so the
+// iterates are bit-reproducible run to run.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace {
+
+using namespace phg;
+
+constexpr int kThreads = 256;
+
+inline int cg_grid(int64_t l) {
+    const int g = grid_for(l, kThreads);
+    return g < kSMs * 8 ? g : kSMs * 8;
+}
+
+__device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
+    return (row >> 5) * (PHG_SELL_C * PHG_SELL_W) + pos * PHG_SELL_C + (row & 31);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block sum, valid in thread 0
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double sh[kThreads / 32];
+    v = warp_sum(v);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < kThreads / 32 ? sh[threadIdx.x] : 0.0;
+        s = warp_sum(s);
+    }
+    return s;
+}
+
+// Writes the block partials of NV values and returns true in every thread
+// of the last block to finish; that block then has the totals in tot[].
+template <int NV>
+__device__ __forceinline__ bool finish(const double (&v)[NV], double* partials, unsigned* counter, double (&tot)[NV]) {
+    __shared__ bool last;
+    __shared__ double shtot[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const double s = block_sum(v[i]);
+        if (threadIdx.x == 0) partials[NV * blockIdx.x + i] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        double s = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += __ldcg(partials + NV * b + i);
+        s = block_sum(s);
+        if (threadIdx.x == 0) shtot[i] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) tot[i] = shtot[i];
+    if (threadIdx.x == 0) *counter = 0;
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_init(int64_t l, const double* __restrict__ sell_val, const double* __restrict__ b, double* __restrict__ x,
+            double* __restrict__ r, double* __restrict__ p, double* __restrict__ d, double tol, double abs_tol,
+            long long max_iter, phg_cg_state* st, double* partials) {
+    double acc[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        const double diag = sell_val[sell_idx(i, 0)];
+        const double di = diag != 0.0 ? 1.0 / diag : 1.0;
+        const double bi = b[i];
+        d[i] = di;
+        x[i] = 0.0;
+        r[i] = bi;
+        const double z = di * bi;
+        p[i] = z;
+        acc[0] += bi * bi;
+        acc[1] += bi * z;
+    }
+    double tot[2];
+    if (!finish<2>(acc, partials, &st->counter[0], tot)) return;
+    if (threadIdx.x == 0) {
+        const double bnorm = sqrt(tot[0]);
+        st->bnorm = bnorm;
+        st->rz = tot[1];
+        st->it = 0;
+        st->max_iter = max_iter;
+        st->converged = 0;
+        st->not_spd = 0;
+        st->rel_residual = 1.0;
+        st->rnorm = bnorm;
+        const double rel = tol * bnorm;
+        st->stop = abs_tol > 0.0 ? fmin(rel, abs_tol) : rel;
+        if (bnorm == 0.0) {  // sparse.cpp:168: zero rhs, zero solution
+            st->done = 1;
+            st->converged = 1;
+            st->rel_residual = 0.0;
+        } else {
+            st->done = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_spmv(int64_t l, const int32_t* __restrict__ sell_col, const double* __restrict__ sell_val,
+            const double* __restrict__ p, double* __restrict__ q, phg_cg_state* st, double* partials) {
+    if (st->done) return;
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = (i >> 5) * (PHG_SELL_C * PHG_SELL_W) + (i & 31);
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < PHG_SELL_W; ++k) {
+            const int32_t c = __ldg(sell_col + base + k * PHG_SELL_C);
+            const double v = __ldg(sell_val + base + k * PHG_SELL_C);
+            s += v * __ldg(p + c);
+        }
+        q[i] = s;
+        acc[0] += p[i] * s;
+    }
+    double tot[1];
+    if (!finish<1>(acc, partials, &st->counter[1], tot)) return;
+    if (threadIdx.x == 0) {
+        st->pq = tot[0];
+        if (tot[0] <= 0.0) {  // sparse.cpp:185
+            st->not_spd = 1;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / tot[0];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_update(int64_t l, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+              const double* __restrict__ q, const double* __restrict__ d, phg_cg_state* st, double* partials) {
+    if (st->done) return;
+    const double alpha = st->alpha;
+    double acc[2] = {0.0, 0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        const double pi = p[i];
+        x[i] += alpha * pi;
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        acc[0] += ri * ri;
+        acc[1] += ri * (d[i] * ri);
+    }
+    double tot[2];
+    if (!finish<2>(acc, partials, &st->counter[2], tot)) return;
+    if (threadIdx.x == 0) {
+        const long long it = st->it + 1;
+        st->it = it;
+        const double rnorm = sqrt(tot[0]);
+        st->rnorm = rnorm;
+        st->rel_residual = rnorm / st->bnorm;
+        if (rnorm <= st->stop) {
+            st->converged = 1;
+            st->done = 1;
+        } else if (it >= st->max_iter) {
+            st->done = 1;
+        } else {
+            st->beta = tot[1] / st->rz;
+            st->rz = tot[1];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_pdir(int64_t l, const double* __restrict__ r, double* __restrict__ p, const double* __restrict__ d,
+            const phg_cg_state* st) {
+    if (st->done) return;
+    const double beta = st->beta;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = d[i] * r[i] + beta * p[i];
+}
+
+}  // namespace
+
+extern "C" int phfem_gpu_cg_init(int64_t l, const int32_t* sell_col, const double* sell_val, const double* b,
+                                 double* x, double* r, double* p, double* d, double tol, double abs_tol,
+                                 long long max_iter, phg_cg_state* st, double* partials, void* stream) {
+    (void)sell_col;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(st, 0, sizeof(phg_cg_state), s);
+    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, sell_val, b, x, r, p, d, tol, abs_tol, max_iter, st, partials);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col, const double* sell_val, double* x,
+                                       double* r, double* p, double* q, const double* d, phg_cg_state* st,
+                                       double* partials, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = cg_grid(l);
+    for (int i = 0; i < n; ++i) {
+        cg_spmv<<<g, kThreads, 0, s>>>(l, sell_col, sell_val, p, q, st, partials);
+        cg_update<<<g, kThreads, 0, s>>>(l, x, r, p, q, d, st, partials);
+        cg_pdir<<<g, kThreads, 0, s>>>(l, r, p, d, st);
+    }
+    return (int)cudaGetLastError();
+}

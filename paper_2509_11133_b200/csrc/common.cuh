@@ -1,0 +1,86 @@
+// Shared device-side definitions of the phfem B200 path.
+//
+// All element arithmetic that must be bit-exact with the reference uses the
+// explicitly rounded intrinsics below (no FMA contraction, true division), so
+// the result does not depend on -fmad (SURVEY.md 8(a')).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "phfem_gpu.h"
+
+namespace phg {
+
+// ---------------------------------------------------------------- exact fp64
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+
+struct V3 {
+    double x, y, z;
+};
+__device__ __forceinline__ V3 vsub(V3 a, V3 b) { return {sub(a.x, b.x), sub(a.y, b.y), sub(a.z, b.z)}; }
+__device__ __forceinline__ V3 vadd(V3 a, V3 b) { return {add(a.x, b.x), add(a.y, b.y), add(a.z, b.z)}; }
+__device__ __forceinline__ V3 vmul(V3 a, double s) { return {mul(a.x, s), mul(a.y, s), mul(a.z, s)}; }
+__device__ __forceinline__ V3 vdiv(V3 a, double s) { return {dvd(a.x, s), dvd(a.y, s), dvd(a.z, s)}; }
+// dot(a,b) = (ax*bx + ay*by) + az*bz  (geom.hpp:22)
+__device__ __forceinline__ double vdot(V3 a, V3 b) {
+    return add(add(mul(a.x, b.x), mul(a.y, b.y)), mul(a.z, b.z));
+}
+// cross (geom.hpp:25)
+__device__ __forceinline__ V3 vcross(V3 a, V3 b) {
+    return {sub(mul(a.y, b.z), mul(a.z, b.y)), sub(mul(a.z, b.x), mul(a.x, b.z)),
+            sub(mul(a.x, b.y), mul(a.y, b.x))};
+}
+__device__ __forceinline__ V3 ldnode(const double* __restrict__ c, int32_t n) {
+    const double* p = c + 3 * (int64_t)n;
+    return {__ldg(p), __ldg(p + 1), __ldg(p + 2)};
+}
+
+// local faces [abc],[acd],[adb],[dcb] (mesh.cpp:34-37, assembly.hpp:29)
+static __constant__ int kFaceVerts[4][3] = {{0, 1, 2}, {0, 2, 3}, {0, 3, 1}, {3, 2, 1}};
+// local edge pairs (connectivity.cpp:15-18)
+static __constant__ int kEdgeVerts[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+__device__ __forceinline__ int face_vert(int k, int j) {
+    // kFaceVerts without a constant-memory lookup (divergent k)
+    switch (k) {
+        case 0: return j;                       // 0 1 2
+        case 1: return j == 0 ? 0 : j + 1;      // 0 2 3
+        case 2: return j == 0 ? 0 : (j == 1 ? 3 : 1);  // 0 3 1
+        default: return 3 - j;                  // 3 2 1
+    }
+}
+// local edge index of the pair (a, b) of local vertices, a != b
+__device__ __forceinline__ int edge_index(int a, int b) {
+    if (a > b) { const int t = a; a = b; b = t; }
+    // (0,1)0 (0,2)1 (0,3)2 (1,2)3 (1,3)4 (2,3)5
+    return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
+}
+
+__device__ __forceinline__ int4 ldtet(const int32_t* __restrict__ tets, int64_t t) {
+    return __ldg(reinterpret_cast<const int4*>(tets) + t);
+}
+__device__ __forceinline__ int tv(const int4& t, int i) {
+    return i == 0 ? t.x : (i == 1 ? t.y : (i == 2 ? t.z : t.w));
+}
+
+// ----------------------------------------------------------- error reporting
+// Device error slots, each holding the minimum offending key (ULLONG_MAX =
+// none); the host replays them in the reference's check order.
+__device__ __forceinline__ void report(unsigned long long* err, int slot, unsigned long long key) {
+    if (err) atomicMin(err + slot, key);
+}
+
+// ------------------------------------------------------------- launch sizes
+constexpr int kSMs = 148;
+inline int grid_for(int64_t n, int block, int per_thread = 1) {
+    int64_t g = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
+    if (g < 1) g = 1;
+    if (g > 0x7fffffff) g = 0x7fffffff;
+    return (int)g;
+}
+
+}  // namespace phg

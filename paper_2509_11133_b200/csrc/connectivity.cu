@@ -1,0 +1,562 @@
+// Edge and face connectivity on the device, bit-exact with the reference's
+// num_edges / edge_pairs_to_elems / faces_up / full_face_table
+// (connectivity.cpp:22-203).
+//
+// The reference numbers edges and faces by first occurrence over the
+// element-major slot sequence.  Here that order is reproduced without a hash
+// map or a global sort:
+//   1. vertex star: CSR of (element, local vertex) incidences by vertex;
+//   2. per vertex v, the edges (v,b) with b>v and the faces whose smallest
+//      vertex is v are grouped in a small shared-memory hash table; the group
+//      minimum is the first occurrence (edges) or the owner slot (faces: the
+//      lower element, i.e. the slot faces_up emits) and the other face slot is
+//      the neighbour across it;
+//   3. ids = exclusive scan over elements of the first-occurrence / owner
+//      counts (scan.cu), assigned in local slot order;
+//   4. the remaining slots copy the id of their group's first slot.
+// The directed edge-pair map (E2T) is never materialised; its only check
+// (two elements claiming the same oriented face) is the orientation test in 2.
+#include <climits>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace {
+
+using namespace phg;
+
+__global__ void star_count(const int32_t* __restrict__ tets, int64_t ne, int32_t* __restrict__ count) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 e = ldtet(tets, t);
+        atomicAdd(count + e.x, 1);
+        atomicAdd(count + e.y, 1);
+        atomicAdd(count + e.z, 1);
+        atomicAdd(count + e.w, 1);
+    }
+}
+
+__global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, unsigned long long* __restrict__ cursor,
+                          int32_t* __restrict__ star) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 e = ldtet(tets, t);
+        const int32_t base = (int32_t)(4 * t);
+        star[atomicAdd(cursor + e.x, 1ull)] = base + 0;
+        star[atomicAdd(cursor + e.y, 1ull)] = base + 1;
+        star[atomicAdd(cursor + e.z, 1ull)] = base + 2;
+        star[atomicAdd(cursor + e.w, 1ull)] = base + 3;
+    }
+}
+
+// ------------------------------------------------------------ star groups
+
+constexpr int kWarpStarMax = 64;  // fast path: stars up to this size
+constexpr int kWarpCap = 256;     // hash capacity per warp (>= 3 * kWarpStarMax + 1)
+constexpr int kWarpsPerBlock = 4;
+
+struct FaceTab {
+    unsigned long long* key;
+    int32_t* lo;
+    int32_t* hi;
+    int32_t* cnt;  // count << 2 | orientation bits
+};
+
+__device__ __forceinline__ unsigned hash32(uint32_t k) { return k * 0x9E3779B1u; }
+__device__ __forceinline__ unsigned hash64(unsigned long long k) {
+    k ^= k >> 29;
+    k *= 0xBF58476D1CE4E5B9ull;
+    return (unsigned)(k >> 32);
+}
+
+__device__ __forceinline__ int edge_slot_insert(int32_t* key, unsigned mask, int32_t b) {
+    unsigned h = hash32((uint32_t)b) & mask;
+    for (;;) {
+        const int32_t old = atomicCAS(key + h, -1, b);
+        if (old == -1 || old == b) return (int)h;
+        h = (h + 1) & mask;
+    }
+}
+__device__ __forceinline__ int edge_slot_find(const int32_t* key, unsigned mask, int32_t b) {
+    unsigned h = hash32((uint32_t)b) & mask;
+    while (key[h] != b) h = (h + 1) & mask;
+    return (int)h;
+}
+__device__ __forceinline__ int face_slot_insert(unsigned long long* key, unsigned mask, unsigned long long k) {
+    unsigned h = hash64(k) & mask;
+    for (;;) {
+        const unsigned long long old = atomicCAS(key + h, ~0ull, k);
+        if (old == ~0ull || old == k) return (int)h;
+        h = (h + 1) & mask;
+    }
+}
+__device__ __forceinline__ int face_slot_find(const unsigned long long* key, unsigned mask, unsigned long long k) {
+    unsigned h = hash64(k) & mask;
+    while (key[h] != k) h = (h + 1) & mask;
+    return (int)h;
+}
+
+// Face candidate of incidence (t, lv) and local face k containing lv:
+// the two other vertices x (following v in the oriented cycle) and y.
+__device__ __forceinline__ void face_other(const int4& tet, int k, int lv, int32_t& x, int32_t& y) {
+    int j = 0;
+    while (face_vert(k, j) != lv) ++j;
+    x = tv(tet, face_vert(k, (j + 1) % 3));
+    y = tv(tet, face_vert(k, (j + 2) % 3));
+}
+// the local face opposite local vertex lv
+__device__ __forceinline__ int opposite_face(int lv) { return lv == 0 ? 3 : (lv == 3 ? 0 : lv); }
+
+// One group (a warp, or a whole block for big stars) processes vertex v.
+template <int NT, typename Sync>
+__device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int32_t* __restrict__ star,
+                             const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
+                             int32_t* __restrict__ slot_mate, int32_t* ekey, int32_t* eval, FaceTab ft,
+                             unsigned mask, unsigned cap, unsigned long long* err, Sync sync) {
+    if (edge_first) {
+        for (unsigned i = rank; i < cap; i += NT) {
+            ekey[i] = -1;
+            eval[i] = INT_MAX;
+        }
+        sync();
+        for (int e = rank; e < m; e += NT) {
+            const int32_t inc = star[beg + e];
+            const int64_t t = inc >> 2;
+            const int lv = inc & 3;
+            const int4 tet = ldtet(tets, t);
+            for (int w = 0; w < 4; ++w) {
+                const int32_t b = tv(tet, w);
+                if (w == lv || b <= v) continue;
+                const int h = edge_slot_insert(ekey, mask, b);
+                atomicMin(eval + h, (int32_t)(6 * t + edge_index(lv, w)));
+            }
+        }
+        sync();
+        for (int e = rank; e < m; e += NT) {
+            const int32_t inc = star[beg + e];
+            const int64_t t = inc >> 2;
+            const int lv = inc & 3;
+            const int4 tet = ldtet(tets, t);
+            for (int w = 0; w < 4; ++w) {
+                const int32_t b = tv(tet, w);
+                if (w == lv || b <= v) continue;
+                edge_first[6 * t + edge_index(lv, w)] = eval[edge_slot_find(ekey, mask, b)];
+            }
+        }
+        sync();
+    }
+    if (slot_mate) {
+        for (unsigned i = rank; i < cap; i += NT) {
+            ft.key[i] = ~0ull;
+            ft.lo[i] = INT_MAX;
+            ft.hi[i] = -1;
+            ft.cnt[i] = 0;
+        }
+        sync();
+        for (int e = rank; e < m; e += NT) {
+            const int32_t inc = star[beg + e];
+            const int64_t t = inc >> 2;
+            const int lv = inc & 3;
+            const int4 tet = ldtet(tets, t);
+            const int opp = opposite_face(lv);
+            for (int k = 0; k < 4; ++k) {
+                if (k == opp) continue;
+                int32_t x, y;
+                face_other(tet, k, lv, x, y);
+                if (x <= v || y <= v) continue;
+                const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
+                                                     : ((unsigned long long)y << 32 | (uint32_t)x);
+                const int h = face_slot_insert(ft.key, mask, key);
+                const int32_t slot = (int32_t)(4 * t + k);
+                atomicMin(ft.lo + h, slot);
+                atomicMax(ft.hi + h, slot);
+                atomicAdd(ft.cnt + h, 4);
+                atomicOr(ft.cnt + h, x < y ? 1 : 2);
+            }
+        }
+        sync();
+        for (int e = rank; e < m; e += NT) {
+            const int32_t inc = star[beg + e];
+            const int64_t t = inc >> 2;
+            const int lv = inc & 3;
+            const int4 tet = ldtet(tets, t);
+            const int opp = opposite_face(lv);
+            for (int k = 0; k < 4; ++k) {
+                if (k == opp) continue;
+                int32_t x, y;
+                face_other(tet, k, lv, x, y);
+                if (x <= v || y <= v) continue;
+                const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
+                                                     : ((unsigned long long)y << 32 | (uint32_t)x);
+                const int h = face_slot_find(ft.key, mask, key);
+                const int32_t slot = (int32_t)(4 * t + k);
+                const int32_t c = ft.cnt[h];
+                const int32_t lo = ft.lo[h], hi = ft.hi[h];
+                const int count = c >> 2;
+                if (count > 2 || (count == 2 && (c & 3) != 3)) {
+                    // same orientation twice: "elements A and B claim the
+                    // same oriented face" (connectivity.cpp:62-68)
+                    const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
+                    report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
+                }
+                slot_mate[slot] = count >= 2 ? (slot == lo ? hi : lo) : -1;
+            }
+        }
+        sync();
+    }
+}
+
+struct WarpSync {
+    __device__ void operator()() const { __syncwarp(); }
+};
+struct BlockSync {
+    __device__ void operator()() const { __syncthreads(); }
+};
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock)
+    star_groups(int64_t nc, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first, int32_t* __restrict__ slot_mate,
+                int32_t* __restrict__ big_list, int32_t* __restrict__ big_count, unsigned long long* err) {
+    // per warp: union of the edge table (2 KB) and the face table (5 KB)
+    __shared__ __align__(16) unsigned char smem[kWarpsPerBlock][kWarpCap * 20];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem[warp];
+    int32_t* ekey = reinterpret_cast<int32_t*>(base);
+    int32_t* eval = ekey + kWarpCap;
+    FaceTab ft;
+    ft.key = reinterpret_cast<unsigned long long*>(base);
+    ft.lo = reinterpret_cast<int32_t*>(base + kWarpCap * 8);
+    ft.hi = ft.lo + kWarpCap;
+    ft.cnt = ft.hi + kWarpCap;
+    const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
+    for (int64_t v = (int64_t)blockIdx.x * kWarpsPerBlock + warp; v < nc; v += nwarps) {
+        const int64_t beg = star_ptr[v];
+        const int m = (int)(star_ptr[v + 1] - beg);
+        if (m > kWarpStarMax) {
+            if (lane == 0) big_list[atomicAdd(big_count, 1)] = (int32_t)v;
+            continue;
+        }
+        group_vertex<32>((int32_t)v, beg, m, lane, star, tets, edge_first, slot_mate, ekey, eval, ft,
+                         kWarpCap - 1, kWarpCap, err, WarpSync{});
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    star_groups_big(const int32_t* __restrict__ big_list, const int64_t* __restrict__ star_ptr,
+                    const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
+                    int32_t* __restrict__ edge_first, int32_t* __restrict__ slot_mate, unsigned cap,
+                    unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int32_t v = big_list[blockIdx.x];
+    const int64_t beg = star_ptr[v];
+    const int m = (int)(star_ptr[v + 1] - beg);
+    if ((unsigned)(3 * m) >= cap) {
+        if (threadIdx.x == 0) report(err, PHG_ERR_VALENCE, (unsigned long long)v);
+        return;
+    }
+    int32_t* ekey = reinterpret_cast<int32_t*>(dsm);
+    int32_t* eval = ekey + cap;
+    FaceTab ft;
+    ft.key = reinterpret_cast<unsigned long long*>(dsm);
+    ft.lo = reinterpret_cast<int32_t*>(dsm + (size_t)cap * 8);
+    ft.hi = ft.lo + cap;
+    ft.cnt = ft.hi + cap;
+    group_vertex<256>(v, beg, m, threadIdx.x, star, tets, edge_first, slot_mate, ekey, eval, ft, cap - 1, cap, err,
+                      BlockSync{});
+}
+
+// -------------------------------------------------------------- numbering
+
+__device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mate < 0 || mate > s; }
+
+__global__ void element_counts(int64_t ne, const int32_t* __restrict__ edge_first,
+                               const int32_t* __restrict__ slot_mate, int32_t* __restrict__ edge_count,
+                               int32_t* __restrict__ face_count) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        if (edge_first) {
+            int c = 0;
+            for (int k = 0; k < 6; ++k) c += edge_first[6 * t + k] == (int32_t)(6 * t + k);
+            edge_count[t] = c;
+        }
+        if (slot_mate) {
+            const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+            const int32_t s = (int32_t)(4 * t);
+            face_count[t] = face_owner(s, m.x) + face_owner(s + 1, m.y) + face_owner(s + 2, m.z) +
+                            face_owner(s + 3, m.w);
+        }
+    }
+}
+
+__global__ void number(int64_t ne, const int32_t* __restrict__ tets, const double* __restrict__ coords,
+                       const int32_t* __restrict__ edge_first, const int64_t* __restrict__ edge_off,
+                       int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
+                       const int32_t* __restrict__ slot_mate, const int64_t* __restrict__ face_off,
+                       int32_t* __restrict__ face_of_slot, int8_t* __restrict__ sigma, int32_t* __restrict__ faces,
+                       int32_t* __restrict__ face_slots, double* __restrict__ face_area,
+                       unsigned long long* err) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 tet = ldtet(tets, t);
+        if (edge_first) {
+            int64_t id = edge_off[t];
+            for (int k = 0; k < 6; ++k) {
+                const int64_t s = 6 * t + k;
+                if (edge_first[s] != (int32_t)s) continue;
+                edge_of_slot[s] = (int32_t)id;
+                int32_t a = tv(tet, k < 3 ? 0 : (k < 5 ? 1 : 2));
+                int32_t b = tv(tet, k < 3 ? k + 1 : (k < 5 ? k - 1 : 3));
+                if (a > b) { const int32_t tmp = a; a = b; b = tmp; }
+                reinterpret_cast<int2*>(edge_nodes)[id] = make_int2(a, b);
+                ++id;
+            }
+        }
+        if (slot_mate) {
+            int64_t id = face_off[t];
+            const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+            for (int k = 0; k < 4; ++k) {
+                const int32_t s = (int32_t)(4 * t + k);
+                const int32_t mate = tv(m, k);
+                if (!face_owner(s, mate)) continue;
+                face_of_slot[s] = (int32_t)id;
+                sigma[s] = 1;
+                const int32_t f0 = tv(tet, face_vert(k, 0)), f1 = tv(tet, face_vert(k, 1)), f2 = tv(tet, face_vert(k, 2));
+                faces[3 * id] = f0;
+                faces[3 * id + 1] = f1;
+                faces[3 * id + 2] = f2;
+                reinterpret_cast<int2*>(face_slots)[id] = make_int2(s, mate);
+                // face_area_and_normal (mesh.cpp:76-84): area = 0.5*|(z-x)x(y-x)|
+                const V3 p0 = ldnode(coords, f0), p1 = ldnode(coords, f1), p2 = ldnode(coords, f2);
+                const V3 n = vcross(vsub(p2, p0), vsub(p1, p0));
+                const double len = __dsqrt_rn(vdot(n, n));
+                if (len == 0.0) report(err, PHG_ERR_FACE, (unsigned long long)id << 2 | 0);
+                face_area[id] = mul(0.5, len);
+                ++id;
+            }
+        }
+    }
+}
+
+__global__ void fill_slots(int64_t ne, const int32_t* __restrict__ edge_first, int32_t* __restrict__ edge_of_slot,
+                           const int32_t* __restrict__ slot_mate, int32_t* __restrict__ face_of_slot,
+                           int8_t* __restrict__ sigma) {
+    const int64_t n6 = edge_first ? 6 * ne : 0;
+    const int64_t n4 = slot_mate ? 4 * ne : 0;
+    const int64_t n = n6 > n4 ? n6 : n4;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        if (s < n6) {
+            const int32_t f = edge_first[s];
+            if (f != (int32_t)s) edge_of_slot[s] = edge_of_slot[f];
+        }
+        if (s < n4) {
+            const int32_t mate = slot_mate[s];
+            if (mate >= 0 && mate < (int32_t)s) {
+                face_of_slot[s] = face_of_slot[mate];
+                sigma[s] = -1;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------- classification
+
+// Face id of the element face with vertex set {a,b,c}, searched through the
+// star of its smallest vertex, or -1.
+__device__ int32_t find_face(int32_t a, int32_t b, int32_t c, const int64_t* __restrict__ star_ptr,
+                             const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
+                             const int32_t* __restrict__ face_of_slot) {
+    int32_t lo = a, mid = b, hi = c;
+    if (lo > mid) { const int32_t t = lo; lo = mid; mid = t; }
+    if (mid > hi) { const int32_t t = mid; mid = hi; hi = t; }
+    if (lo > mid) { const int32_t t = lo; lo = mid; mid = t; }
+    if (lo == mid || mid == hi) return -1;
+    const int64_t beg = star_ptr[lo], end = star_ptr[lo + 1];
+    for (int64_t i = beg; i < end; ++i) {
+        const int32_t inc = star[i];
+        const int64_t t = inc >> 2;
+        const int4 tet = ldtet(tets, t);
+        int pos_mid = -1, pos_hi = -1;
+        for (int w = 0; w < 4; ++w) {
+            if (tv(tet, w) == mid) pos_mid = w;
+            if (tv(tet, w) == hi) pos_hi = w;
+        }
+        if (pos_mid < 0 || pos_hi < 0) continue;
+        const int lv = inc & 3;
+        const int opp = 6 - lv - pos_mid - pos_hi;  // the fourth local vertex
+        return face_of_slot[4 * t + opposite_face(opp)];
+    }
+    return -1;
+}
+
+__global__ void classify(int64_t nd, const int32_t* __restrict__ db, int64_t nn, const int32_t* __restrict__ nb,
+                         const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                         const int32_t* __restrict__ tets, const int32_t* __restrict__ face_of_slot,
+                         const int32_t* __restrict__ face_slots, uint32_t* __restrict__ claim,
+                         unsigned long long* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd + nn; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* tri = i < nd ? db + 3 * i : nb + 3 * (i - nd);
+        const int32_t f = find_face(tri[0], tri[1], tri[2], star_ptr, star, tets, face_of_slot);
+        if (f < 0) {
+            report(err, PHG_ERR_CLASSIFY, (unsigned long long)i << 2 | 0);
+            continue;
+        }
+        atomicMin(claim + f, (uint32_t)i);
+        if (face_slots[2 * (int64_t)f + 1] >= 0) report(err, PHG_ERR_CLASSIFY, (unsigned long long)i << 2 | 2);
+    }
+}
+
+__global__ void classify_check(int64_t nd, const int32_t* __restrict__ db, int64_t nn,
+                               const int32_t* __restrict__ nb, const int64_t* __restrict__ star_ptr,
+                               const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
+                               const int32_t* __restrict__ face_of_slot, const uint32_t* __restrict__ claim,
+                               unsigned long long* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd + nn; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t* tri = i < nd ? db + 3 * i : nb + 3 * (i - nd);
+        const int32_t f = find_face(tri[0], tri[1], tri[2], star_ptr, star, tets, face_of_slot);
+        if (f >= 0 && claim[f] != (uint32_t)i) report(err, PHG_ERR_CLASSIFY, (unsigned long long)i << 2 | 1);
+    }
+}
+
+__global__ void face_class_k(int64_t nf, int64_t nd, const uint32_t* __restrict__ claim,
+                             const int32_t* __restrict__ face_slots, uint8_t* __restrict__ face_class,
+                             int32_t* __restrict__ is_row, unsigned long long* __restrict__ counts,
+                             unsigned long long* err) {
+    int c0 = 0, c1 = 0, c2 = 0;
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t cl = claim[f];
+        const bool boundary = face_slots[2 * f + 1] < 0;
+        uint8_t cls = 0;
+        if (cl != 0xffffffffu) cls = (int64_t)cl < nd ? 1 : 2;
+        else if (boundary) report(err, PHG_ERR_FACE, (unsigned long long)f << 2 | 1);
+        face_class[f] = cls;
+        is_row[f] = cls != 2;
+        c0 += cls == 0;
+        c1 += cls == 1;
+        c2 += cls == 2;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(counts + 0, (unsigned long long)c0);
+        atomicAdd(counts + 1, (unsigned long long)c1);
+        atomicAdd(counts + 2, (unsigned long long)c2);
+    }
+}
+
+__global__ void face_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, const int64_t* __restrict__ row_off,
+                            int32_t* __restrict__ face_mrow, int32_t* __restrict__ row_face) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        if (face_class[f] != 2) {
+            const int64_t r = row_off[f];
+            face_mrow[f] = (int32_t)r;
+            row_face[r] = (int32_t)f;
+        } else {
+            face_mrow[f] = -1;
+        }
+    }
+}
+
+inline int grid_cap(int64_t n, int block) {
+    const int g = grid_for(n, block);
+    return g < kSMs * 32 ? g : kSMs * 32;
+}
+
+}  // namespace
+
+extern "C" int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream) {
+    star_count<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, count);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_t* star, void* stream) {
+    star_fill<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(
+        tets, ne, reinterpret_cast<unsigned long long*>(cursor), star);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                                     int32_t* edge_first, int32_t* slot_mate, int32_t* big_list, int32_t* big_count,
+                                     unsigned long long* err, void* stream) {
+    const int64_t blocks = (nc + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int grid = (int)(blocks < kSMs * 64 ? blocks : kSMs * 64);
+    star_groups<<<grid, 32 * kWarpsPerBlock, 0, (cudaStream_t)stream>>>(nc, star_ptr, star, tets, edge_first,
+                                                                        slot_mate, big_list, big_count, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_star_groups_big(int32_t n_big, const int32_t* big_list, const int64_t* star_ptr,
+                                         const int32_t* star, const int32_t* tets, int32_t* edge_first,
+                                         int32_t* slot_mate, int max_star, unsigned long long* err, void* stream) {
+    if (n_big <= 0) return 0;
+    unsigned cap = 512;
+    while (cap < 3u * (unsigned)max_star + 1u) cap <<= 1;
+    const size_t smem = (size_t)cap * 20;
+    if (smem > 200 * 1024) {
+        cap = 8192;
+    }
+    const size_t bytes = (size_t)cap * 20;
+    cudaFuncSetAttribute(star_groups_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    star_groups_big<<<n_big, 256, bytes, (cudaStream_t)stream>>>(big_list, star_ptr, star, tets, edge_first,
+                                                                 slot_mate, cap, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
+                                        int32_t* edge_count, int32_t* face_count, void* stream) {
+    element_counts<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, slot_mate, edge_count,
+                                                                        face_count);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords, const int32_t* edge_first,
+                                const int64_t* edge_off, int32_t* edge_of_slot, int32_t* edge_nodes,
+                                const int32_t* slot_mate, const int64_t* face_off, int32_t* face_of_slot,
+                                int8_t* sigma, int32_t* faces, int32_t* face_slots, double* face_area,
+                                unsigned long long* err, void* stream) {
+    number<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, tets, coords, edge_first, edge_off, edge_of_slot,
+                                                                edge_nodes, slot_mate, face_off, face_of_slot, sigma,
+                                                                faces, face_slots, face_area, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_fill_slots(int64_t ne, const int32_t* edge_first, int32_t* edge_of_slot,
+                                    const int32_t* slot_mate, int32_t* face_of_slot, int8_t* sigma, void* stream) {
+    const int64_t n = (edge_first ? 6 : 4) * ne;
+    fill_slots<<<grid_cap(n, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, edge_of_slot, slot_mate,
+                                                                   face_of_slot, sigma);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_classify(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
+                                  const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                                  const int32_t* face_of_slot, const int32_t* face_slots, uint32_t* claim,
+                                  unsigned long long* err, void* stream) {
+    if (nd + nn == 0) return 0;
+    classify<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
+                                                                      face_of_slot, face_slots, claim, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
+                                        const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                                        const int32_t* face_of_slot, const uint32_t* claim, unsigned long long* err,
+                                        void* stream) {
+    if (nd + nn == 0) return 0;
+    classify_check<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
+                                                                            face_of_slot, claim, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const int32_t* face_slots,
+                                    const double* face_area, uint8_t* face_class, int32_t* is_row,
+                                    unsigned long long* counts, unsigned long long* err, void* stream) {
+    (void)face_area;
+    face_class_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, nd, claim, face_slots, face_class, is_row,
+                                                                      counts, err);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const int64_t* row_off, int32_t* face_mrow,
+                                   int32_t* row_face, void* stream) {
+    face_rows_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_class, row_off, face_mrow, row_face);
+    return (int)cudaGetLastError();
+}

@@ -1,0 +1,218 @@
+// Device problem data: f, u_D, g and the exact solution of the six problem
+// kinds (reference built-ins analysis.cpp:9-49 plus the config problems of
+// BASELINE.json).  Same expression trees as the CPU restatement
+// (oracle/problems.h) with explicitly rounded arithmetic, so the polynomial
+// kinds are bit-identical to the reference; the transcendental kinds differ
+// only by the libm-vs-libdevice ulp of sin/cos/exp.
+#pragma once
+
+#include "common.cuh"
+
+namespace phg {
+
+constexpr double kPi = 3.14159265358979323846;
+
+struct Coef {
+    double a0, a1, a2;  // diagonal diffusion
+    double c;           // reaction
+};
+
+template <int KIND>
+__device__ __forceinline__ double prob_u(double x, double y, double z) {
+    if constexpr (KIND == 0) {
+        return mul(mul(mul(mul(mul(x, x), y), y), z), z);
+    } else if constexpr (KIND == 1) {
+        return add(add(add(x, mul(2.0, y)), mul(3.0, z)), 4.0);
+    } else if constexpr (KIND == 3) {
+        return mul(mul(sin(mul(kPi, x)), sin(mul(kPi, y))), sin(mul(kPi, z)));
+    } else if constexpr (KIND == 4) {
+        return mul(mul(exp(x), cos(mul(kPi, y))), mul(z, z));
+    } else if constexpr (KIND == 5) {
+        return mul(mul(mul(x, sub(8.0, x)), sin(mul(kPi, y))), sin(mul(kPi, z)));
+    } else {
+        return 0.0;
+    }
+}
+
+template <int KIND>
+__device__ __forceinline__ V3 prob_grad(double x, double y, double z) {
+    if constexpr (KIND == 0) {
+        return {mul(mul(mul(mul(mul(2.0, x), y), y), z), z), mul(mul(mul(mul(mul(2.0, x), x), y), z), z),
+                mul(mul(mul(mul(mul(2.0, x), x), y), y), z)};
+    } else if constexpr (KIND == 1) {
+        return {1.0, 2.0, 3.0};
+    } else if constexpr (KIND == 3) {
+        const double sx = sin(mul(kPi, x)), sy = sin(mul(kPi, y)), sz = sin(mul(kPi, z));
+        const double cx = cos(mul(kPi, x)), cy = cos(mul(kPi, y)), cz = cos(mul(kPi, z));
+        return {mul(mul(mul(kPi, cx), sy), sz), mul(mul(mul(kPi, sx), cy), sz), mul(mul(mul(kPi, sx), sy), cz)};
+    } else if constexpr (KIND == 4) {
+        const double ex = exp(x), cy = cos(mul(kPi, y)), sy = sin(mul(kPi, y));
+        return {mul(mul(ex, cy), mul(z, z)), mul(mul(mul(-kPi, ex), sy), mul(z, z)), mul(mul(mul(2.0, ex), cy), z)};
+    } else if constexpr (KIND == 5) {
+        const double q = mul(x, sub(8.0, x));
+        const double sy = sin(mul(kPi, y)), sz = sin(mul(kPi, z));
+        const double cy = cos(mul(kPi, y)), cz = cos(mul(kPi, z));
+        return {mul(mul(sub(8.0, mul(2.0, x)), sy), sz), mul(mul(mul(kPi, q), cy), sz), mul(mul(mul(kPi, q), sy), cz)};
+    } else {
+        return {0.0, 0.0, 0.0};
+    }
+}
+
+// f = -div(A grad u) + c u
+template <int KIND>
+__device__ __forceinline__ double prob_f(double x, double y, double z, const Coef& k) {
+    if constexpr (KIND == 0) {
+        const double u = mul(mul(mul(mul(mul(x, x), y), y), z), z);
+        const double yyzz = mul(mul(mul(y, y), z), z);
+        const double xxzz = mul(mul(mul(x, x), z), z);
+        const double xxyy = mul(mul(mul(x, x), y), y);
+        return add(mul(-2.0, add(add(mul(k.a0, yyzz), mul(k.a1, xxzz)), mul(k.a2, xxyy))), mul(k.c, u));
+    } else if constexpr (KIND == 1) {
+        return mul(k.c, add(add(add(x, mul(2.0, y)), mul(3.0, z)), 4.0));
+    } else if constexpr (KIND == 3) {
+        const double u = mul(mul(sin(mul(kPi, x)), sin(mul(kPi, y))), sin(mul(kPi, z)));
+        return mul(add(mul(mul(kPi, kPi), add(add(k.a0, k.a1), k.a2)), k.c), u);
+    } else if constexpr (KIND == 4) {
+        const double ex = exp(x), cy = cos(mul(kPi, y));
+        const double u = mul(mul(ex, cy), mul(z, z));
+        const double uxx = u, uyy = mul(-mul(kPi, kPi), u), uzz = mul(mul(2.0, ex), cy);
+        return add(-add(add(mul(k.a0, uxx), mul(k.a1, uyy)), mul(k.a2, uzz)), mul(k.c, u));
+    } else if constexpr (KIND == 5) {
+        const double sy = sin(mul(kPi, y)), sz = sin(mul(kPi, z));
+        const double u = mul(mul(mul(x, sub(8.0, x)), sy), sz);
+        const double uxx = mul(mul(-2.0, sy), sz), uyy = mul(-mul(kPi, kPi), u);
+        return add(-add(add(mul(k.a0, uxx), mul(k.a1, uyy)), mul(k.a2, uyy)), mul(k.c, u));
+    } else {
+        return 0.0;
+    }
+}
+
+// g = (A grad u) . n
+template <int KIND>
+__device__ __forceinline__ double prob_g(double x, double y, double z, V3 n, const Coef& k) {
+    const V3 g = prob_grad<KIND>(x, y, z);
+    return add(add(mul(mul(k.a0, g.x), n.x), mul(mul(k.a1, g.y), n.y)), mul(mul(k.a2, g.z), n.z));
+}
+
+__device__ __forceinline__ Coef load_coef(const phg_problem& p, int64_t t) {
+    Coef k;
+    if (p.a_diag) {
+        k.a0 = __ldg(p.a_diag + 3 * t);
+        k.a1 = __ldg(p.a_diag + 3 * t + 1);
+        k.a2 = __ldg(p.a_diag + 3 * t + 2);
+    } else if (p.a_elem) {
+        k.a0 = k.a1 = k.a2 = __ldg(p.a_elem + t);
+    } else {
+        k.a0 = k.a1 = k.a2 = 1.0;
+    }
+    k.c = p.c;
+    return k;
+}
+
+// -------------------------------------------------------------- element core
+
+// local_stiffness_mass (assembly.cpp:7-33) with A_T = K(A) + c M
+struct Local {
+    double a[4][4];
+    double vol;
+    V3 g[4];
+    bool degenerate;
+};
+
+__device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Local& L) {
+    const V3 d1 = vsub(p[1], p[0]), d2 = vsub(p[2], p[0]), d3 = vsub(p[3], p[0]);
+    const double det = vdot(vcross(d1, d2), d3);
+    L.degenerate = det == 0.0;
+    L.vol = dvd(fabs(det), 6.0);
+    L.g[1] = vdiv(vcross(d2, d3), det);
+    L.g[2] = vdiv(vcross(d3, d1), det);
+    L.g[3] = vdiv(vcross(d1, d2), det);
+    L.g[0] = vmul(vadd(vadd(L.g[1], L.g[2]), L.g[3]), -1.0);
+    const double m20 = dvd(L.vol, 20.0);
+    const double mdiag = mul(k.c, mul(m20, 2.0)), moff = mul(k.c, mul(m20, 1.0));
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const V3 gi = L.g[i], gj = L.g[j];
+            const double d = add(add(mul(k.a0, mul(gi.x, gj.x)), mul(k.a1, mul(gi.y, gj.y))), mul(k.a2, mul(gi.z, gj.z)));
+            L.a[i][j] = add(mul(L.vol, d), i == j ? mdiag : moff);
+        }
+}
+
+// Mat4Lu::factor / solve (geom.hpp:48-87)
+struct Lu4 {
+    double lu[4][4];
+    int perm[4];
+    bool singular;
+};
+
+__device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f.perm[i] = i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f.lu[i][j] = a[i][j];
+    }
+    f.singular = false;
+#pragma unroll
+    for (int col = 0; col < 4; ++col) {
+        int piv = col;
+        double best = fabs(f.lu[col][col]);
+#pragma unroll
+        for (int r = col + 1; r < 4; ++r) {
+            const double v = fabs(f.lu[r][col]);
+            if (v > best) { best = v; piv = r; }
+        }
+        if (best == 0.0) { f.singular = true; return; }
+        if (piv != col) {
+            // swap rows piv and col (register arrays: select instead of
+            // dynamic indexing)
+#pragma unroll
+            for (int r = col + 1; r < 4; ++r) {
+                if (r == piv) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double t = f.lu[r][c];
+                        f.lu[r][c] = f.lu[col][c];
+                        f.lu[col][c] = t;
+                    }
+                    const int tp = f.perm[r];
+                    f.perm[r] = f.perm[col];
+                    f.perm[col] = tp;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = col + 1; r < 4; ++r) {
+            const double m = dvd(f.lu[r][col], f.lu[col][col]);
+            f.lu[r][col] = m;
+#pragma unroll
+            for (int c = col + 1; c < 4; ++c) f.lu[r][c] = sub(f.lu[r][c], mul(m, f.lu[col][c]));
+        }
+    }
+}
+
+__device__ __forceinline__ double sel4(const double b[4], int i) {
+    return i == 0 ? b[0] : (i == 1 ? b[1] : (i == 2 ? b[2] : b[3]));
+}
+
+__device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double x[4]) {
+    double y[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        double s = sel4(b, f.perm[i]);
+#pragma unroll
+        for (int j = 0; j < i; ++j) s = sub(s, mul(f.lu[i][j], y[j]));
+        y[i] = s;
+    }
+#pragma unroll
+    for (int i = 3; i >= 0; --i) {
+        double s = y[i];
+#pragma unroll
+        for (int j = i + 1; j < 4; ++j) s = sub(s, mul(f.lu[i][j], x[j]));
+        x[i] = dvd(s, f.lu[i][i]);
+    }
+}
+
+}  // namespace phg

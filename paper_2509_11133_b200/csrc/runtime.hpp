@@ -1,0 +1,209 @@
+// Host runtime of the B200 phfem library: device buffers, the mesh /
+// connectivity / system objects behind the C ABI handles, and the stage
+// orchestration that calls the kernels through phfem_gpu.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "phfem_gpu.h"
+
+namespace phb {
+
+// Error taxonomy of the reference (errors.hpp:9-27), mapped 1:1 onto the C
+// status codes by the C ABI wrapper.
+struct InvalidArgument : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct MeshError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct SolverError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what);
+inline void check(int e, const char* what) { check(static_cast<cudaError_t>(e), what); }
+
+// One stream per process; every call synchronises on it before returning.
+struct Runtime {
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    Runtime();
+};
+Runtime& rt();
+inline cudaStream_t S() { return rt().stream; }
+inline void* SV() { return static_cast<void*>(rt().stream); }
+void sync();
+
+// Stream-ordered device buffer (cudaMallocAsync on the library stream,
+// served from the device memory pool between pipeline passes).
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    int64_t n = 0;
+    DBuf() = default;
+    explicit DBuf(int64_t count) { alloc(count); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(int64_t count) {
+        release();
+        n = count;
+        if (count > 0) check(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, S()), "allocate");
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, S());
+        p = nullptr;
+        n = 0;
+    }
+    void zero() {
+        if (n) check(cudaMemsetAsync(p, 0, sizeof(T) * (size_t)n, S()), "memset");
+    }
+    void fill_bytes(int byte) {
+        if (n) check(cudaMemsetAsync(p, byte, sizeof(T) * (size_t)n, S()), "memset");
+    }
+    void upload(const T* h, int64_t count) {
+        alloc(count);
+        if (count) check(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, S()), "H2D");
+    }
+    std::vector<T> download() const {
+        std::vector<T> h((size_t)n);
+        if (n) check(cudaMemcpyAsync(h.data(), p, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, S()), "D2H");
+        sync();
+        return h;
+    }
+    void download_to(T* h, int64_t count) const {
+        if (count) check(cudaMemcpyAsync(h, p, sizeof(T) * (size_t)count, cudaMemcpyDeviceToHost, S()), "D2H");
+    }
+};
+
+template <class T>
+T read_scalar(const T* dptr) {
+    T v{};
+    check(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    return v;
+}
+
+// Device events for stage timing on the library stream.
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Timer();
+    ~Timer();
+    void start();
+    double stop_ms();  // records b, synchronises, returns ms
+};
+
+// ---------------------------------------------------------------- objects
+
+struct MeshData {
+    int64_t nc = 0, ne = 0, nd = 0, nn = 0;
+    int level = 0;
+    DBuf<double> coords;  // [3 nC]
+    DBuf<int32_t> tets;   // [4 nE]
+    DBuf<int32_t> db, nb; // [3 nD], [3 nN]
+};
+
+struct Coefs {
+    DBuf<double> a_elem, a_diag;
+    bool has_elem = false, has_diag = false;
+    double c = 1.0;
+    uint64_t version = 0;
+};
+
+struct Connectivity {
+    // vertex star
+    DBuf<int64_t> star_ptr;
+    DBuf<int32_t> star;
+    // edges
+    bool has_edges = false;
+    int64_t ned = 0;
+    DBuf<int32_t> edge_first, edge_of_slot, edge_nodes;
+    DBuf<int64_t> edge_off;
+    // faces
+    bool has_faces = false;
+    int64_t nf = 0, n_int = 0, n_dir = 0, n_neu = 0, l = 0;
+    DBuf<int32_t> slot_mate, face_of_slot, faces, face_slots, face_mrow, row_face;
+    DBuf<int8_t> sigma;
+    DBuf<uint8_t> face_class;
+    DBuf<double> face_area;
+    // timings (seconds)
+    double t_edges = 0.0, t_faces = 0.0;
+};
+
+struct System {
+    int problem = -1;
+    uint64_t coef_version = 0;
+    int64_t n = 0, l = 0, nchunks = 0;
+    DBuf<int32_t> sell_col;
+    DBuf<double> sell_val, rhs_neg, bd, rhs;
+    double sum_rhs2 = 0.0, sum_bd2 = 0.0;
+    // debug views (filled only on request)
+    DBuf<double> a_blocks, slot_coef;
+    DBuf<int32_t> slot_mrow;
+};
+
+struct RefineMap {
+    DBuf<int32_t> midpoint, centroid;
+};
+
+struct Stages {
+    double star = 0, groups = 0, number = 0, classify = 0, assemble = 0, refine = 0;
+};
+
+// --------------------------------------------------------------- pipeline
+
+std::shared_ptr<MeshData> upload_mesh(const double* coords, int64_t nc, const int32_t* tets, int64_t ne,
+                                      const int32_t* db, int64_t nd, const int32_t* nb, int64_t nn, int level);
+std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly, double lz, double jitter,
+                                    uint64_t seed, uint32_t mask);
+
+// star + edges (+ faces, classification and multiplier rows)
+void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st = nullptr);
+// red refinement; needs edges
+std::shared_ptr<MeshData> refine_mesh(const MeshData& m, const Connectivity& c, RefineMap* map,
+                                      Stages* st = nullptr);
+// fused assembly + condensation
+void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
+                     bool debug_views, Stages* st = nullptr);
+phg_problem device_problem(const Coefs& k, int problem);
+
+struct SolveResult {
+    DBuf<double> u, lambda;
+    int64_t iterations = 0;
+    double residual = 0.0, constraint_residual = 0.0, seconds = 0.0, cg_ms = 0.0;
+    bool converged = false;
+};
+void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const System& sys, int problem,
+                 double tol, int64_t max_iter, const std::string& method, SolveResult& out);
+
+double mesh_diameter(const MeshData& m);
+// [y-norm, kappa-norm, L2]
+void error_norms(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, const double* u,
+                 const double* lambda, double out[3]);
+
+// host helpers
+std::string format_double(double v);
+void tet_rule(int degree, std::vector<double>& lam, std::vector<double>& w);
+
+}  // namespace phb
