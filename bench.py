@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark of the phfem B200 hot path (BASELINE.json metric:
+"tets/s refine+connect+assemble+condense (fp64); Schur solve s; % HBM peak").
+
+Workload (default): config 4, the 128^3 x 6 Kuhn mesh (12,582,912 tets,
+Dirichlet z=0, u = sin sin sin, reference operator c=1).  One step = one
+pass of the hot path over that device-resident mesh: edge + face
+connectivity (bit-exact reference numbering), fused assembly + element-local
+Schur condensation into the SELL face matrix, and one 12-way red refinement
+of the mesh (12.6M -> 151M tets).  `value` is tets of the input mesh per
+second over the whole job; the Schur solve (Jacobi-PCG to the reference's
+stopping rule) is timed once after the steps and reported as `schur_solve`.
+
+Arms:
+  python bench.py [--gpus N --steps K --warmup W]      this repo (CUDA)
+  python bench.py --impl reference ...                  the reference's own CPU
+       implementation (oracle/_ref: /root/reference/proj/src compiled by
+       oracle/Makefile) on a bounded Kuhn sample, rank 0 only.
+Multi-GPU: one process per GPU (torchrun); the path does not shard
+(replicas only), so every rank runs an independent replica and
+the job time is the max over ranks (scaling "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "tets/s refine+connect+assemble+condense (fp64); Schur solve s; % HBM peak"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------- algorithmic bytes
+
+
+def algorithmic_bytes(nc, ne, ned, nf, nb, nnz_s, l, k_coef=0):
+    """compulsory bytes per stage (int32 ids, fp64 reals,
+    int8 sigma, u8 class, int64 row pointers, int32 columns)."""
+    b_edges = 44 * ne + 8 * ned
+    b_faces = 60 * ne + 24 * nc + 12 * nb + 33 * nf
+    b_asm = 36 * ne + 24 * nc + 13 * nf + k_coef * ne + 12 * nnz_s + 16 * l + 8
+    b_refine = 260 * ne + 48 * nc + 24 * ned + 72 * nb
+    b_cg = 12 * nnz_s + 8 * (l + 1) + 80 * l
+    return dict(connect=b_edges + b_faces, assemble=b_asm, refine=b_refine, cg_iteration=b_cg)
+
+
+# ---------------------------------------------------------- reference arm
+
+
+def reference_sample(n: int):
+    from oracle_bind import Oracle, RefCtx, ref_available
+
+    if not ref_available():
+        raise RuntimeError("oracle/_ref/libphfem_ref.so not built")
+    O = Oracle()
+    m = O.kuhn(n, n, n, dmask=0x10)
+    return m, RefCtx
+
+
+def reference_step(m, RefCtx, workers):
+    t0 = time.perf_counter()
+    r = RefCtx(m)
+    t = r.connectivity()
+    r.assemble(3)
+    r.build_schur(workers)
+    r.refine()
+    return time.perf_counter() - t0, t
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    n = args.ref_n
+    cores = os.cpu_count() or 1
+    m, RefCtx = reference_sample(n)
+    for _ in range(args.warmup):
+        reference_step(m, RefCtx, cores)
+    times = [reference_step(m, RefCtx, cores)[0] for _ in range(args.steps)]
+    sec = sum(times) / len(times)
+    value = m.ne / sec
+    sample = (f"Kuhn {n}^3 x 6 = {m.ne} tets (config-4 shape and problem at reduced n): num_edges, "
+              f"edge_pairs_to_elems, faces_up, full_face_table, assemble_system, build_schur(workers={cores}), "
+              f"red_refine per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg4-shape Kuhn {n}^3 (bounded CPU sample)", "mesh_tets": m.ne},
+            "cpu_baseline": {"value": value, "unit": "tets/s", "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "tets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(n=32):
+    """Reference CPU path (oracle/_ref) on a bounded sample of the workload."""
+    try:
+        m, RefCtx = reference_sample(n)
+    except Exception as e:  # noqa: BLE001
+        return {"value": None, "unit": "tets/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+    cores = os.cpu_count() or 1
+    sec, stages = reference_step(m, RefCtx, cores)
+    return {"value": m.ne / sec, "unit": "tets/s", "cores": cores, "kind": "reference",
+            "sample": (f"Kuhn {n}^3 x 6 = {m.ne} tets, one pass of num_edges + edge_pairs_to_elems + faces_up + "
+                       f"full_face_table + assemble_system + build_schur(workers={cores}) + red_refine in {sec:.2f} s; "
+                       f"only build_schur uses more than one thread")}
+
+
+# ------------------------------------------------------------------ ours
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=24)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import numpy as np
+
+    from paper_2509_11133_b200 import configs
+    from paper_2509_11133_b200 import phfem as ph
+
+    cfg = configs.CONFIGS[args.config]
+    mesh = cfg.build()
+    nc, ne, nd, nn = mesh.sizes()
+    stream = torch.cuda.ExternalStream(ph.stream_ptr())
+    launches = ph.lib().phfem_gpu_launch_count
+    launches.restype = __import__("ctypes").c_longlong
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        stages, counts = mesh.pipeline(cfg.problem, True)
+    ned, nf, l, sell_slots, ne_child = (int(v) for v in counts)
+    conn = mesh.connectivity()
+    sysz = np.zeros(3, dtype=np.int64)
+    nnz_s = int(mesh.assemble(cfg.problem)["s_col"].size) if ne <= 2_000_000 else None
+
+    barrier()
+    l0 = launches()
+    acc = {}
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            st, _ = mesh.pipeline(cfg.problem, True)
+            for k, v in st.items():
+                acc[k] = acc.get(k, 0.0) + v
+        e1.record(stream)
+        e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    nlaunch = launches() - l0
+    stage_ms = {k: v / args.steps for k, v in acc.items()}
+    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * ne / (ms_max / 1e3)
+
+    # nnz(S) (true, without SELL padding) from the row structure: every
+    # multiplier row has 1 + the non-Neumann other faces of its 1-2 elements
+    if nnz_s is None:
+        nnz_s = mesh_nnz_s(mesh, cfg.problem)
+    hbm, hbm_kind = peaks()
+    k_coef = 8 if cfg.coef == "log_uniform" else (24 if cfg.coef == "aniso" else 0)
+    B = algorithmic_bytes(nc, ne, ned, nf, nd + nn, nnz_s, l, k_coef)
+    conn_ms = stage_ms["star"] + stage_ms["groups"] + stage_ms["number"] + stage_ms["classify"]
+    per_stage = {
+        "connect": {"ms": conn_ms, "bytes": B["connect"]},
+        "assemble_condense": {"ms": stage_ms["assemble"], "bytes": B["assemble"]},
+        "refine": {"ms": stage_ms["refine"], "bytes": B["refine"]},
+    }
+    for k, v in per_stage.items():
+        v["gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
+        v["hbm_frac"] = v["gbs"] / hbm
+        v["tets_per_s"] = ne / (v["ms"] / 1e3)
+    dom_name = max(per_stage, key=lambda k: per_stage[k]["ms"])
+    dom = per_stage[dom_name]
+    total_bytes = sum(v["bytes"] for v in per_stage.values())
+    roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s", "frac": dom["gbs"] / hbm,
+                "traffic": None, "kernel": dom_name, "peak_kind": hbm_kind,
+                "step_achieved": total_bytes / (ms / 1e3) / 1e9, "step_frac": total_bytes / (ms / 1e3) / 1e9 / hbm}
+
+    # e2e through the public C ABI: pinned host arrays -> device mesh ->
+    # pipeline -> counts back
+    coords, tets, db, nb = mesh.arrays()
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    hc, ht, hd, hn = pin(coords), pin(tets), pin(db), pin(nb)
+    h2d = hc.nbytes + ht.nbytes + hd.nbytes + hn.nbytes
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        m2 = ph.Mesh.from_arrays(hc, ht, hd, hn)
+        _, cts = m2.pipeline(cfg.problem, True)
+        del m2
+    e3.record(stream)
+    e3.synchronize()
+    wall = (time.perf_counter() - t_wall) / args.steps
+    e2e_ms = max(e2.elapsed_time(e3) / args.steps, wall * 1e3)
+    te = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": world * ne / (float(te.item()) / 1e3), "unit": "tets/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(cts.nbytes + 7 * 8)}
+
+    # Schur solve (Jacobi-PCG, reference stopping rule), once
+    solve = None
+    if not args.no_solve:
+        r = mesh.solve_timed(cfg.problem, cfg.tol)
+        b_it = B["cg_iteration"]
+        gbs = b_it / (r["ms_per_iteration"] / 1e3) / 1e9 if r["ms_per_iteration"] else None
+        solve = {"seconds": r["cg_ms"] / 1e3, "iterations": r["iterations"], "converged": r["converged"],
+                 "ms_per_iteration": r["ms_per_iteration"], "gbs_per_iteration": gbs,
+                 "hbm_frac": gbs / hbm if gbs else None, "tol": cfg.tol}
+
+    if rank == 0:
+        cpu = cpu_baseline() if (world == 1 and not args.no_cpu) else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "mesh_tets": ne, "mesh_nodes": nc, "edges": ned, "faces": nf,
+                       "multipliers": l, "nnz_S": nnz_s, "children_tets": ne_child, "problem": cfg.problem,
+                       "note": cfg.note, "l2": "inputs > L2 (mesh 253 MB; per-step working set several GB)",
+                       "parallelism": f"replicas x{world}"},
+            "stages_ms": stage_ms, "per_stage": per_stage, "roofline": roofline, "schur_solve": solve,
+            "e2e": e2e, "gpu_launches": int(nlaunch), "clocks": clk.summary(), "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def mesh_nnz_s(mesh, problem):
+    """nnz of S from the face table (rows = multiplier faces)."""
+    import numpy as np
+
+    f = mesh.faces()
+    fs = f["face_slots"]
+    mrow = f["mrow"]
+    fos = f["face_of_slot"].reshape(-1, 4)
+    nonneu = (mrow[fos] >= 0).sum(axis=1)  # per element
+    rows = np.nonzero(mrow >= 0)[0]
+    s0 = fs[rows, 0] // 4
+    s1 = fs[rows, 1]
+    nnz = 1 + (nonneu[s0] - 1)
+    inter = s1 >= 0
+    nnz = nnz.astype(np.int64)
+    nnz[inter] += nonneu[s1[inter] // 4] - 1
+    return int(nnz.sum())
+
+
+if __name__ == "__main__":
+    main()

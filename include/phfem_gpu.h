@@ -224,6 +224,9 @@ int phfem_gpu_sell_row_nnz(int64_t l, const int32_t* sell_col, int32_t* row_nnz,
 int phfem_gpu_sell_to_csr(int64_t l, const int32_t* sell_col, const double* sell_val,
                           const int64_t* row_ptr, int32_t* col, double* val, void* stream);
 
+/* kernels launched by this library since load (benchmark accounting) */
+long long phfem_gpu_launch_count(void);
+
 /* last CUDA error as text (for the host runtime's messages) */
 const char* phfem_gpu_error_string(int code);
 

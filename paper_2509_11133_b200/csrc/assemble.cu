@@ -270,6 +270,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, con
         default: return (int)cudaErrorInvalidValue;
     }
 #undef PHG_ASM
-    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms);
+    phg::count_launches(1);
+    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms); phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -202,7 +202,7 @@ extern "C" int phfem_gpu_cg_init(int64_t l, const int32_t* sell_col, const doubl
     (void)sell_col;
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(st, 0, sizeof(phg_cg_state), s);
-    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, sell_val, b, x, r, p, d, tol, abs_tol, max_iter, st, partials);
+    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, sell_val, b, x, r, p, d, tol, abs_tol, max_iter, st, partials); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -212,9 +212,9 @@ extern "C" int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col
     cudaStream_t s = (cudaStream_t)stream;
     const int g = cg_grid(l);
     for (int i = 0; i < n; ++i) {
-        cg_spmv<<<g, kThreads, 0, s>>>(l, sell_col, sell_val, p, q, st, partials);
-        cg_update<<<g, kThreads, 0, s>>>(l, x, r, p, q, d, st, partials);
-        cg_pdir<<<g, kThreads, 0, s>>>(l, r, p, d, st);
+        cg_spmv<<<g, kThreads, 0, s>>>(l, sell_col, sell_val, p, q, st, partials); phg::count_launches(1);
+        cg_update<<<g, kThreads, 0, s>>>(l, x, r, p, q, d, st, partials); phg::count_launches(1);
+        cg_pdir<<<g, kThreads, 0, s>>>(l, r, p, d, st); phg::count_launches(1);
     }
     return (int)cudaGetLastError();
 }

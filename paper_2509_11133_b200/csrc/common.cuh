@@ -76,6 +76,10 @@ __device__ __forceinline__ void report(unsigned long long* err, int slot, unsign
 
 // ------------------------------------------------------------- launch sizes
 constexpr int kSMs = 148;
+
+// process-wide count of kernels launched by this library (bench.py's
+// gpu_launches); defined in scan.cu
+void count_launches(int n);
 inline int grid_for(int64_t n, int block, int per_thread = 1) {
     int64_t g = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
     if (g < 1) g = 1;

@@ -463,13 +463,13 @@ inline int grid_cap(int64_t n, int block) {
 }  // namespace
 
 extern "C" int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream) {
-    star_count<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, count);
+    star_count<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, count); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_t* star, void* stream) {
     star_fill<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(
-        tets, ne, reinterpret_cast<unsigned long long*>(cursor), star);
+        tets, ne, reinterpret_cast<unsigned long long*>(cursor), star); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -479,7 +479,7 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     const int64_t blocks = (nc + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const int grid = (int)(blocks < kSMs * 64 ? blocks : kSMs * 64);
     star_groups<<<grid, 32 * kWarpsPerBlock, 0, (cudaStream_t)stream>>>(nc, star_ptr, star, tets, edge_first,
-                                                                        slot_mate, big_list, big_count, err);
+                                                                        slot_mate, big_list, big_count, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -496,14 +496,14 @@ extern "C" int phfem_gpu_star_groups_big(int32_t n_big, const int32_t* big_list,
     const size_t bytes = (size_t)cap * 20;
     cudaFuncSetAttribute(star_groups_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     star_groups_big<<<n_big, 256, bytes, (cudaStream_t)stream>>>(big_list, star_ptr, star, tets, edge_first,
-                                                                 slot_mate, cap, err);
+                                                                 slot_mate, cap, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
                                         int32_t* edge_count, int32_t* face_count, void* stream) {
     element_counts<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, slot_mate, edge_count,
-                                                                        face_count);
+                                                                        face_count); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -514,7 +514,7 @@ extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* c
                                 unsigned long long* err, void* stream) {
     number<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, tets, coords, edge_first, edge_off, edge_of_slot,
                                                                 edge_nodes, slot_mate, face_off, face_of_slot, sigma,
-                                                                faces, face_slots, face_area, err);
+                                                                faces, face_slots, face_area, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -522,7 +522,7 @@ extern "C" int phfem_gpu_fill_slots(int64_t ne, const int32_t* edge_first, int32
                                     const int32_t* slot_mate, int32_t* face_of_slot, int8_t* sigma, void* stream) {
     const int64_t n = (edge_first ? 6 : 4) * ne;
     fill_slots<<<grid_cap(n, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, edge_of_slot, slot_mate,
-                                                                   face_of_slot, sigma);
+                                                                   face_of_slot, sigma); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -532,7 +532,7 @@ extern "C" int phfem_gpu_classify(int64_t nd, const int32_t* db, int64_t nn, con
                                   unsigned long long* err, void* stream) {
     if (nd + nn == 0) return 0;
     classify<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
-                                                                      face_of_slot, face_slots, claim, err);
+                                                                      face_of_slot, face_slots, claim, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -542,7 +542,7 @@ extern "C" int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t n
                                         void* stream) {
     if (nd + nn == 0) return 0;
     classify_check<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
-                                                                            face_of_slot, claim, err);
+                                                                            face_of_slot, claim, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -551,12 +551,12 @@ extern "C" int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* clai
                                     unsigned long long* counts, unsigned long long* err, void* stream) {
     (void)face_area;
     face_class_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, nd, claim, face_slots, face_class, is_row,
-                                                                      counts, err);
+                                                                      counts, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const int64_t* row_off, int32_t* face_mrow,
                                    int32_t* row_face, void* stream) {
-    face_rows_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_class, row_off, face_mrow, row_face);
+    face_rows_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_class, row_off, face_mrow, row_face); phg::count_launches(1);
     return (int)cudaGetLastError();
 }

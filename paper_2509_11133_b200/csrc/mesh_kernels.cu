@@ -158,14 +158,14 @@ __global__ void diameter(const double* __restrict__ coords, const int32_t* __res
 extern "C" int phfem_gpu_kuhn_nodes(int nx, int ny, int nz, double lx, double ly, double lz, double jitter,
                                     uint64_t seed, double* coords, void* stream) {
     const int64_t n = (int64_t)(nx + 1) * (ny + 1) * (nz + 1);
-    kuhn_nodes<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, lx, ly, lz, jitter, seed, coords);
+    kuhn_nodes<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, lx, ly, lz, jitter, seed, coords); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_kuhn_tets(int nx, int ny, int nz, uint32_t mask, int32_t* tets, int32_t* bcount,
                                    void* stream) {
     const int64_t ne = 6ll * nx * ny * nz;
-    kuhn_tets<<<grid_for(ne, 256), 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, mask, tets, bcount);
+    kuhn_tets<<<grid_for(ne, 256), 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, mask, tets, bcount); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -174,12 +174,12 @@ extern "C" int phfem_gpu_kuhn_boundary(int nx, int ny, int nz, uint32_t mask, co
                                        void* stream) {
     const int64_t ne = 6ll * nx * ny * nz;
     kuhn_boundary<<<grid_for(ne, 256), 256, 0, (cudaStream_t)stream>>>(nx, ny, nz, mask, tets, dir_off, neu_off,
-                                                                         db, nb);
+                                                                         db, nb); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_split_counts(const int32_t* packed, int32_t* dir, int32_t* neu, int64_t n, void* stream) {
-    split_counts<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(packed, dir, neu, n);
+    split_counts<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(packed, dir, neu, n); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -189,7 +189,7 @@ extern "C" int phfem_gpu_diameter(const double* coords, const int32_t* tets, int
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(out, 0, sizeof(double), s);
     const int grid = (int)std::min<int64_t>(grid_for(ne, 256), 148 * 8);
-    diameter<<<grid, 256, 0, s>>>(coords, tets, ne, reinterpret_cast<unsigned long long*>(out));
+    diameter<<<grid, 256, 0, s>>>(coords, tets, ne, reinterpret_cast<unsigned long long*>(out)); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

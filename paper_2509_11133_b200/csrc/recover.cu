@@ -346,6 +346,7 @@ extern "C" int phfem_gpu_recover(int64_t ne, const double* coords, const int32_t
     }
 #undef PHG_REC
     reduce_partials<<<1, 256, 0, s>>>(partials, g, 1, 0u, sums);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }
 
@@ -360,6 +361,7 @@ extern "C" int phfem_gpu_constraint_residual(int64_t l, const int32_t* row_face,
     const int g = rgrid(l);
     constraint_k<<<g, kThreads, 0, s>>>(l, row_face, face_slots, face_area, u, bd, partials);
     reduce_partials<<<1, 256, 0, s>>>(partials, g, 3, 0x6u, out);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }
 
@@ -383,16 +385,19 @@ extern "C" int phfem_gpu_errors(int64_t ne, const double* coords, const int32_t*
     }
 #undef PHG_ERRK
     reduce_partials<<<1, 256, 0, s>>>(partials, g, 3, 0u, out);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_sell_row_nnz(int64_t l, const int32_t* sell_col, int32_t* row_nnz, void* stream) {
     sell_row_nnz<<<rgrid(l), kThreads, 0, (cudaStream_t)stream>>>(l, sell_col, row_nnz);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_sell_to_csr(int64_t l, const int32_t* sell_col, const double* sell_val,
                                      const int64_t* row_ptr, int32_t* col, double* val, void* stream) {
     sell_to_csr<<<rgrid(l), kThreads, 0, (cudaStream_t)stream>>>(l, sell_col, sell_val, row_ptr, col, val);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -127,7 +127,7 @@ extern "C" int phfem_gpu_refine(int64_t nc, int64_t ne, const double* coords, co
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemcpyAsync(coords_out, coords, (size_t)(3 * nc) * sizeof(double), cudaMemcpyDeviceToDevice, s);
     refine_k<<<grid_for(ne, 128), 128, 0, s>>>(nc, ne, coords, tets, edge_first, edge_of_slot, edge_off, coords_out,
-                                               tets_out, midpoint_node, centroid_node);
+                                               tets_out, midpoint_node, centroid_node); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -137,6 +137,6 @@ extern "C" int phfem_gpu_refine_boundary(int64_t nf, const int32_t* faces, int64
                                          unsigned long long* err, void* stream) {
     if (nf == 0) return 0;
     refine_boundary_k<<<grid_for(nf, 128), 128, 0, (cudaStream_t)stream>>>(nf, faces, list_base, nc, star_ptr, star,
-                                                                           tets, edge_first, edge_of_slot, out, err);
+                                                                           tets, edge_first, edge_of_slot, out, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }

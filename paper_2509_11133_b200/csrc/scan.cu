@@ -1,6 +1,8 @@
 // Deterministic device-wide exclusive scan (int32 counts -> int64 offsets),
 // the "unique/scan" half of the numbering pipeline.
 // Three passes: tile reduce -> scan of tile sums (one block) -> tile scan.
+#include <atomic>
+
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -97,7 +99,13 @@ __global__ void __launch_bounds__(kThreads) tile_scan(const int32_t* __restrict_
     }
 }
 
+std::atomic<long long> g_launches{0};
+
 }  // namespace
+
+void phg::count_launches(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+extern "C" long long phfem_gpu_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 extern "C" size_t phfem_gpu_scan_scratch(int64_t n) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -110,6 +118,7 @@ extern "C" int phfem_gpu_scan_i32(const int32_t* in, int64_t* out, int64_t n, vo
     long long* tile_sum = static_cast<long long*>(scratch);
     if (n > 0) {
         tile_reduce<<<(unsigned)ntiles, kThreads, 0, s>>>(in, n, tile_sum);
+        phg::count_launches(3);
         scan_tile_sums<<<1, kThreads, 0, s>>>(tile_sum, ntiles, out + n);
         tile_scan<<<(unsigned)ntiles, kThreads, 0, s>>>(in, n, tile_sum, out);
     } else {

@@ -161,11 +161,16 @@ def test_config_parity(oracle, cid, factor):
         g.set_coefficients(k["a_elem"], k["a_diag"], cfg.c)
     fo = check_connectivity(g, m, oracle)
     so = check_system(g, m, fo, oracle, cfg.problem, cfg.c, k["a_elem"], k["a_diag"])
-    tol = cfg.tol if cid in (1, 4) else 1e-12
-    try:
-        uo, lo, st_o = oracle.solve(m, so, cfg.problem, cfg.c, k["a_elem"], k["a_diag"], tol=tol)
-    except Exception as e:  # the reference may refuse a converged solve (SURVEY finding 8)
-        pytest.skip(f"oracle refuses at tol {tol}: {e}")
+    # the reference may refuse a converged solve through verify_solution
+    # (SURVEY finding 8); tighten the tolerance until the oracle accepts
+    for tol in (cfg.tol, 1e-11, 1e-12):
+        try:
+            uo, lo, st_o = oracle.solve(m, so, cfg.problem, cfg.c, k["a_elem"], k["a_diag"], tol=tol)
+            break
+        except Exception as e:  # noqa: BLE001
+            last = e
+    else:
+        pytest.fail(f"oracle refuses at every tolerance: {last}")
     sol = g.solve_ex(cfg.problem, tol=tol)
     ug, lg = sol.values()
     assert rel_l2(ug, uo) <= 1e-9, rel_l2(ug, uo)
