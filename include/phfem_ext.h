@@ -82,6 +82,12 @@ int phfem_mesh_get_system(const phfem_mesh* mesh, double* a_blocks, double* slot
  * solver is always the element-local Schur path. max_iter <= 0: 10 L. */
 int phfem_solve_ex(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
                    phfem_solution** out);
+/* The face solve alone: pcg_jacobi on s_neg with inner_cg_options
+ * (sparse.cpp:163-212, solver.cpp:78-86), no recovery and no
+ * verify_solution (which can reject a converged solve, SURVEY finding 8).
+ * lambda [L] host output; out: [iterations, rel_residual, converged]. */
+int phfem_mesh_solve_faces(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
+                           double* lambda, double out[3]);
 /* out: [iterations, residual, constraint_residual, seconds] */
 int phfem_solution_stats(const phfem_solution* sol, double out[4]);
 /* out: [broken Y-norm error, multiplier h-norm error, L2 error] */

@@ -71,6 +71,11 @@ int phfem_gpu_kuhn_boundary(int nx, int ny, int nz, uint32_t dirichlet_mask, con
                             int32_t* nb, void* stream);
 int phfem_gpu_split_counts(const int32_t* packed, int32_t* dir, int32_t* neu, int64_t n, void* stream);
 
+/* range check of uploaded node indices (mesh.cpp:151-158): atomicMin of the
+ * first position holding an index outside [0, nc) into *first_bad */
+int phfem_gpu_check_indices(const int32_t* a, int64_t n, int64_t nc, unsigned long long* first_bad,
+                            void* stream);
+
 /* max element diameter (mesh.cpp:90-106); out: one double (device) */
 int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, double* out,
                        double* partials, void* stream);

@@ -1,12 +1,16 @@
-// Fused assembly + element-local Schur condensation, one thread per element
+// Assembly + element-local Schur condensation on the device
 // (assemble_system, assembly.cpp:7-138, and the local part of build_schur,
 // solver.cpp:90-127), scattering straight into the SELL-32 Schur matrix.
 //
-// Per element the thread builds A_T = K_T(A) + c M_T, the C_T rows
-// sigma*|F|/3, the Gauss-64 load vector plus the Neumann terms (B_T), the
-// Dirichlet data, the partial-pivot LU of A_T, S_T = C A^-1 C' and
-// r_T = C A^-1 B, all in registers with the reference's operation order.
-// Nothing element-sized besides B_T (kept for the recovery) is written back.
+// Two element-parallel kernels, split by register footprint:
+//   load     B_T = Gauss-64 load vector + Neumann terms (assembly.cpp:46-94),
+//            the fp64-heavy part, at high occupancy (few live registers);
+//   condense A_T = K_T(A) + c M_T, C_T rows sigma*|F|/3, Dirichlet data,
+//            partial-pivot LU of A_T, S_T = C A^-1 C', r_T = C A^-1 B, and the
+//            scatter of S_T and b_D - r_T into the face system.
+// Everything the reference computes in these loops is replayed in its
+// operation order without FMA, so A_T, C_T and S_T are bit-identical; the
+// transcendental load data differ only by libm-vs-libdevice ulps.
 //
 // Scatter (each S entry has one contribution except interior diagonals,
 // which have two; a two-term sum is order free, so atomics stay exact):
@@ -28,7 +32,8 @@ namespace {
 
 using namespace phg;
 
-constexpr int kAsmThreads = 128;
+constexpr int kLoadThreads = 128;
+constexpr int kCondThreads = 128;
 
 __device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
     return (row >> 5) * (PHG_SELL_C * PHG_SELL_W) + pos * PHG_SELL_C + (row & 31);
@@ -46,43 +51,114 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return s;
 }
 
+struct Slots {
+    int32_t row[4];
+    int32_t face[4];
+    bool owner[4], bnd[4];
+};
+
+__device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict__ face_of_slot,
+                                           const int32_t* __restrict__ slot_mate,
+                                           const int32_t* __restrict__ face_mrow, Slots& s) {
+    const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+    const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int32_t sl = (int32_t)(4 * t + q);
+        const int32_t mate = tv(mate4, q);
+        s.face[q] = tv(fos4, q);
+        s.row[q] = __ldg(face_mrow + s.face[q]);
+        s.owner[q] = mate < 0 || mate > sl;
+        s.bnd[q] = mate < 0;
+    }
+}
+
+// B_T: Gauss-64 load vector (assembly.cpp:64-78) + Neumann terms
+// (assembly.cpp:81-94, face order == local slot order for one element),
+// rhs = b + LN (assembly.cpp:135).
 template <int KIND>
-__global__ void __launch_bounds__(kAsmThreads)
-    assemble_condense(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets,
-                      phg_problem prob, const int32_t* __restrict__ face_of_slot,
-                      const int32_t* __restrict__ slot_mate, const int32_t* __restrict__ face_mrow,
-                      const double* __restrict__ face_area, int32_t* __restrict__ sell_col,
-                      double* __restrict__ sell_val, double* __restrict__ rhs_neg, double* __restrict__ bd,
-                      double* __restrict__ rhs_out, double* __restrict__ a_blocks, double* __restrict__ slot_coef,
-                      int32_t* __restrict__ slot_mrow, double* __restrict__ partials, unsigned long long* err) {
-    __shared__ double sh[kAsmThreads / 32];
-    double acc_rhs = 0.0, acc_bd = 0.0;
+__global__ void __launch_bounds__(kLoadThreads)
+    load_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
+           const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
+           const int32_t* __restrict__ face_mrow, double* __restrict__ rhs_out, double* __restrict__ partials,
+           unsigned long long* err) {
+    (void)face_of_slot;
+    (void)slot_mate;
+    (void)face_mrow;
+    (void)partials;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 e = ldtet(tets, t);
+        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+        const Coef k = load_coef(prob, t);
+        // elem_volume == local.volume (assembly.cpp:18, 47)
+        const V3 d1 = vsub(p[1], p[0]), d2 = vsub(p[2], p[0]), d3 = vsub(p[3], p[0]);
+        const double det = vdot(vcross(d1, d2), d3);
+        if (det == 0.0) {
+            report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
+            continue;
+        }
+        const double vol = dvd(fabs(det), 6.0);
+        double b[4] = {0.0, 0.0, 0.0, 0.0};
+        if constexpr (KIND <= 2) {
+            // polynomial data: the reference's exact operation order
+#pragma unroll 2
+            for (int qp = 0; qp < 64; ++qp) {
+                const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                             l3 = c_lam5[4 * qp + 3];
+                const V3 x = vadd(vadd(vadd(vmul(p[0], l0), vmul(p[1], l1)), vmul(p[2], l2)), vmul(p[3], l3));
+                const double fw = mul(mul(vol, c_w5[qp]), prob_f<KIND>(x.x, x.y, x.z, k));
+                b[0] = add(b[0], mul(fw, l0));
+                b[1] = add(b[1], mul(fw, l1));
+                b[2] = add(b[2], mul(fw, l2));
+                b[3] = add(b[3], mul(fw, l3));
+            }
+        } else {
+            const double cpre = prob_f_pre<KIND>(k);
+#pragma unroll 2
+            for (int qp = 0; qp < 64; ++qp) {
+                const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                             l3 = c_lam5[4 * qp + 3];
+                const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
+                const double y = fma(p[3].y, l3, fma(p[2].y, l2, fma(p[1].y, l1, p[0].y * l0)));
+                const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
+                const double fw = (vol * c_w5[qp]) * prob_f_fast<KIND>(x, y, z, cpre, k);
+                b[0] = fma(fw, l0, b[0]);
+                b[1] = fma(fw, l1, b[1]);
+                b[2] = fma(fw, l2, b[2]);
+                b[3] = fma(fw, l3, b[3]);
+            }
+        }
+        // b only; condense_k adds the Neumann terms (rhs = b + LN)
+        reinterpret_cast<double2*>(rhs_out)[2 * t] = make_double2(b[0], b[1]);
+        reinterpret_cast<double2*>(rhs_out)[2 * t + 1] = make_double2(b[2], b[3]);
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kCondThreads)
+    condense_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
+               const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
+               const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
+               double* __restrict__ rhs_in, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+               double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
+               double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, double* __restrict__ partials,
+               unsigned long long* err) {
+    __shared__ double sh[kCondThreads / 32];
+    double acc_bd = 0.0, acc_rhs = 0.0;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
         const int4 e = ldtet(tets, t);
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
         const Coef k = load_coef(prob, t);
         Local L;
-        local_matrices(p, k, L);
-        if (L.degenerate) {
-            report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
-            continue;
-        }
-        // slot data: multiplier row, C_T entry (assembly.cpp:121-126)
-        const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-        const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
-        int32_t row[4];
+        local_matrices(p, k, L);  // local_stiffness_mass (assembly.cpp:7-33)
+        if (L.degenerate) continue;  // reported by load_k
+        Slots sl;
+        load_slots(t, face_of_slot, slot_mate, face_mrow, sl);
         double coef[4];
-        bool owner[4], bnd[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int32_t s = (int32_t)(4 * t + q);
-            const int32_t mate = tv(mate4, q);
-            const int32_t f = tv(fos4, q);
-            row[q] = __ldg(face_mrow + f);
-            owner[q] = mate < 0 || mate > s;
-            bnd[q] = mate < 0;
-            const double sg = owner[q] ? 1.0 : -1.0;
-            coef[q] = dvd(mul(sg, __ldg(face_area + f)), 3.0);
+        for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
+            const double sg = sl.owner[q] ? 1.0 : -1.0;
+            coef[q] = dvd(mul(sg, __ldg(face_area + sl.face[q])), 3.0);
         }
         if (a_blocks) {
 #pragma unroll
@@ -96,52 +172,34 @@ __global__ void __launch_bounds__(kAsmThreads)
         }
         if (slot_mrow) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = row[q];
+            for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = sl.row[q];
         }
-
-        // load vector, Gauss branch (assembly.cpp:64-78)
-        double b[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 2
-        for (int qp = 0; qp < 64; ++qp) {
-            const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2], l3 = c_lam5[4 * qp + 3];
-            const V3 x = vadd(vadd(vadd(vmul(p[0], l0), vmul(p[1], l1)), vmul(p[2], l2)), vmul(p[3], l3));
-            const double fw = mul(mul(L.vol, c_w5[qp]), prob_f<KIND>(x.x, x.y, x.z, k));
-            b[0] = add(b[0], mul(fw, l0));
-            b[1] = add(b[1], mul(fw, l1));
-            b[2] = add(b[2], mul(fw, l2));
-            b[3] = add(b[3], mul(fw, l3));
-        }
-        // Neumann (assembly.cpp:81-94) and Dirichlet (96-104) face data
+        // Neumann terms (assembly.cpp:81-94; this element's Neumann faces in
+        // face order == local slot order), then rhs = b + LN (assembly.cpp:135)
         double ln[4] = {0.0, 0.0, 0.0, 0.0};
-        double bdv[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (!bnd[q]) continue;
+            if (!sl.bnd[q] || sl.row[q] >= 0) continue;
             const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
             const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
             const V3 cen = vdiv(vadd(vadd(q0, q1), q2), 3.0);
-            if (row[q] < 0) {
-                const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
-                const double len = __dsqrt_rn(vdot(n, n));
-                const double ar = mul(0.5, len);
-                const V3 un = vdiv(n, len);
-                const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-                const double contrib = dvd(mul(ar, gc), 3.0);
-                ln[i0] = add(ln[i0], contrib);
-                ln[i1] = add(ln[i1], contrib);
-                ln[i2] = add(ln[i2], contrib);
-            } else {
-                bdv[q] = mul(__ldg(face_area + tv(fos4, q)), prob_u<KIND>(cen.x, cen.y, cen.z));
-            }
+            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+            const double len = __dsqrt_rn(vdot(n, n));
+            const double ar = mul(0.5, len);
+            const V3 un = vdiv(n, len);
+            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+            const double contrib = dvd(mul(ar, gc), 3.0);
+            ln[i0] = add(ln[i0], contrib);
+            ln[i1] = add(ln[i1], contrib);
+            ln[i2] = add(ln[i2], contrib);
         }
-        double rhs[4];
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            rhs[v] = add(b[v], ln[v]);
-            acc_rhs = add(acc_rhs, mul(rhs[v], rhs[v]));
-        }
-        reinterpret_cast<double2*>(rhs_out)[2 * t] = make_double2(rhs[0], rhs[1]);
-        reinterpret_cast<double2*>(rhs_out)[2 * t + 1] = make_double2(rhs[2], rhs[3]);
+        const double2 r01 = reinterpret_cast<const double2*>(rhs_in)[2 * t];
+        const double2 r23 = reinterpret_cast<const double2*>(rhs_in)[2 * t + 1];
+        const double rhs[4] = {add(r01.x, ln[0]), add(r01.y, ln[1]), add(r23.x, ln[2]), add(r23.y, ln[3])};
+        reinterpret_cast<double2*>(const_cast<double*>(rhs_in))[2 * t] = make_double2(rhs[0], rhs[1]);
+        reinterpret_cast<double2*>(const_cast<double*>(rhs_in))[2 * t + 1] = make_double2(rhs[2], rhs[3]);
+        acc_rhs = add(acc_rhs, add(add(add(mul(rhs[0], rhs[0]), mul(rhs[1], rhs[1])), mul(rhs[2], rhs[2])),
+                                   mul(rhs[3], rhs[3])));
 
         // local Schur complement (solver.cpp:101-127)
         Lu4 lu;
@@ -155,7 +213,7 @@ __global__ void __launch_bounds__(kAsmThreads)
         for (int r = 0; r < 4; ++r)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
-                const bool on = row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
+                const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
                 cr[r][v] = on ? coef[r] : 0.0;
             }
         double ainv_c[4][4], ainv_b[4];
@@ -164,12 +222,12 @@ __global__ void __launch_bounds__(kAsmThreads)
         lu_solve(lu, rhs, ainv_b);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            if (row[r] < 0) continue;
+            if (sl.row[r] < 0) continue;
             double rb = 0.0;
 #pragma unroll
             for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr[r][pp], ainv_b[pp]));
-            const int64_t R = row[r];
-            const int base = owner[r] ? 0 : 3;
+            const int64_t R = sl.row[r];
+            const int base = sl.owner[r] ? 0 : 3;
             int j = 1;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -182,8 +240,8 @@ __global__ void __launch_bounds__(kAsmThreads)
                 } else {
                     const int64_t ix = sell_idx(R, base + j);
                     ++j;
-                    if (row[q] >= 0) {
-                        sell_col[ix] = row[q];
+                    if (sl.row[q] >= 0) {
+                        sell_col[ix] = sl.row[q];
                         sell_val[ix] = s;
                     } else {
                         sell_col[ix] = (int32_t)R;
@@ -191,22 +249,26 @@ __global__ void __launch_bounds__(kAsmThreads)
                     }
                 }
             }
-            if (bnd[r]) {
+            if (sl.bnd[r]) {
 #pragma unroll
                 for (int pos = 4; pos < 7; ++pos) {
                     sell_col[sell_idx(R, pos)] = (int32_t)R;
                     sell_val[sell_idx(R, pos)] = 0.0;
                 }
+                // b_D = |F| u_D(centroid) (assembly.cpp:96-104); the face's
+                // stored tuple is this slot's (owner) orientation
+                const int i0 = face_vert(r, 0), i1 = face_vert(r, 1), i2 = face_vert(r, 2);
+                const V3 cen = vdiv(vadd(vadd(p[i0], p[i1]), p[i2]), 3.0);
+                const double bdv = mul(__ldg(face_area + sl.face[r]), prob_u<KIND>(cen.x, cen.y, cen.z));
                 // rhs_neg = b_D - r_T (solver.cpp:131-138), single contributor
-                rhs_neg[R] = sub(bdv[r], rb);
-                bd[R] = bdv[r];
-                acc_bd = add(acc_bd, mul(bdv[r], bdv[r]));
+                rhs_neg[R] = sub(bdv, rb);
+                bd[R] = bdv;
+                acc_bd = add(acc_bd, mul(bdv, bdv));
             } else {
                 atomicAdd(rhs_neg + R, -rb);
             }
         }
     }
-    // deterministic block partials of ||rhs||^2 and ||b_D||^2
     const double s0 = block_sum(acc_rhs, sh);
     const double s1 = block_sum(acc_bd, sh);
     if (threadIdx.x == 0) {
@@ -241,9 +303,10 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
     return rc ? rc : phfem_gpu_set_rules_errors(lam9, w9);
 }
 
+// both kernels use the same fixed grid so their partial arrays line up
 extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
-    const int g = grid_for(ne, kAsmThreads);
-    return g < kSMs * 16 ? g : kSMs * 16;
+    const int g = grid_for(ne, kLoadThreads);
+    return g < kSMs * 32 ? g : kSMs * 32;
 }
 
 extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
@@ -256,10 +319,12 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, con
     cudaStream_t s = (cudaStream_t)stream;
     const int grid = phfem_gpu_assemble_grid(ne);
     const phg_problem p = *prob;
-#define PHG_ASM(K)                                                                                             \
-    assemble_condense<K><<<grid, kAsmThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, \
-                                                      face_area, sell_col, sell_val, rhs_neg, bd, rhs, a_blocks,   \
-                                                      slot_coef, slot_mrow, partials, err)
+#define PHG_ASM(K)                                                                                                  \
+    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, partials,  \
+                                            err);                                                                   \
+    condense_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area, \
+                                                rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,         \
+                                                slot_mrow, partials, err)
     switch (p.kind) {
         case 0: PHG_ASM(0); break;
         case 1: PHG_ASM(1); break;
@@ -270,7 +335,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, con
         default: return (int)cudaErrorInvalidValue;
     }
 #undef PHG_ASM
-    phg::count_launches(1);
-    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms); phg::count_launches(1);
+    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms);
+    phg::count_launches(3);
     return (int)cudaGetLastError();
 }

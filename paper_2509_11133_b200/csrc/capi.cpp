@@ -149,6 +149,7 @@ struct phfem_mesh {
     std::shared_ptr<System> sys;
     RefineMap last_map;
     int64_t map_ned = -1, map_ne = -1;
+    std::shared_ptr<MeshData> scratch_child;  // phfem_pipeline's refinement target
 
     const Connectivity& table() {
         if (!conn || !conn->has_faces) {
@@ -267,7 +268,7 @@ int phfem_mesh_refine(phfem_mesh* mesh, phfem_refine_times* times) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         const auto t0 = std::chrono::steady_clock::now();
-        const Connectivity& c = mesh->edges();
+        Connectivity& c = const_cast<Connectivity&>(mesh->edges());
         const int64_t ned = c.ned, ne = mesh->data->ne;
         auto child = refine_mesh(*mesh->data, c, &mesh->last_map);
         mesh->map_ned = ned;
@@ -565,17 +566,21 @@ int phfem_mesh_create_from_arrays(const double* coords, int64_t n_nodes, const i
     return guarded([&] {
         if (!out || (n_nodes && !coords) || (n_elems && !tetra) || (n_dir && !dirichlet) || (n_neu && !neumann))
             throw InvalidArgument("null argument");
-        auto check_range = [&](const int32_t* a, int64_t n) {
-            for (int64_t i = 0; i < n; ++i)
-                if (a[i] < 0 || a[i] >= n_nodes)
-                    throw InvalidArgument("node index " + std::to_string(a[i] + 1) + " out of range 1.." +
-                                          std::to_string(n_nodes));
-        };
-        check_range(tetra, 4 * n_elems);
-        check_range(dirichlet, 3 * n_dir);
-        check_range(neumann, 3 * n_neu);
         auto m = std::make_unique<phfem_mesh>();
         m->data = upload_mesh(coords, n_nodes, tetra, n_elems, dirichlet, n_dir, neumann, n_neu, level);
+        // index range check on the device (the host copy stays untouched)
+        const MeshData& d = *m->data;
+        DBuf<unsigned long long> bad(3);
+        bad.fill_bytes(0xff);
+        check(phfem_gpu_check_indices(d.tets.p, 4 * d.ne, d.nc, bad.p, SV()), "check indices");
+        check(phfem_gpu_check_indices(d.db.p, 3 * d.nd, d.nc, bad.p + 1, SV()), "check indices");
+        check(phfem_gpu_check_indices(d.nb.p, 3 * d.nn, d.nc, bad.p + 2, SV()), "check indices");
+        const std::vector<unsigned long long> b = bad.download();
+        const int32_t* src[3] = {tetra, dirichlet, neumann};
+        for (int i = 0; i < 3; ++i)
+            if (b[i] != ~0ull)
+                throw InvalidArgument("node index " + std::to_string((long long)src[i][b[i]] + 1) +
+                                      " out of range 1.." + std::to_string(n_nodes));
         *out = m.release();
     });
 }
@@ -754,6 +759,23 @@ int phfem_solve_ex(const phfem_mesh* mesh, int problem, double tol, int64_t max_
     });
 }
 
+int phfem_mesh_solve_faces(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter, double* lambda,
+                           double out[3]) {
+    return guarded([&] {
+        if (!mesh || !out) throw InvalidArgument("null argument");
+        if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
+        auto* m = const_cast<phfem_mesh*>(mesh);
+        const System& sys = m->system(problem, false);
+        SolveResult r;
+        solve_schur(*m->data, *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r, true);
+        if (lambda) r.lambda.download_to(lambda, sys.l);
+        phb::sync();
+        out[0] = (double)r.iterations;
+        out[1] = r.rel_residual;
+        out[2] = r.converged ? 1.0 : 0.0;
+    });
+}
+
 int phfem_solution_stats(const phfem_solution* sol, double out[4]) {
     return guarded([&] {
         if (!sol || !out) throw InvalidArgument("null argument");
@@ -787,16 +809,19 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int do_refine, phfem_stage_ms*
         Stages st;
         Timer total;
         total.start();
+        // rebuild everything; reuse the previous pass's device memory when no
+        // solution snapshot shares it
+        auto c = (mesh->conn && mesh->conn.use_count() == 1) ? mesh->conn : std::make_shared<Connectivity>();
+        auto s = (mesh->sys && mesh->sys.use_count() == 1) ? mesh->sys : std::make_shared<System>();
         mesh->invalidate();
-        auto c = std::make_shared<Connectivity>();
         build_connectivity(*mesh->data, *c, true, &st);
         mesh->conn = c;
-        auto s = std::make_shared<System>();
         assemble_system(*mesh->data, *mesh->coef, *c, problem, *s, false, &st);
         mesh->sys = s;
         int64_t ne_child = 0;
         if (do_refine) {
-            auto child = refine_mesh(*mesh->data, *c, nullptr, &st);
+            if (!mesh->scratch_child) mesh->scratch_child = std::make_shared<MeshData>();
+            auto child = refine_mesh(*mesh->data, *c, nullptr, &st, mesh->scratch_child);
             ne_child = child->ne;
         }
         const double tot = total.stop_ms();
@@ -825,11 +850,7 @@ int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t m
         auto* m = const_cast<phfem_mesh*>(mesh);
         const System& sys = m->system(problem, false);
         SolveResult r;
-        try {
-            solve_schur(*m->data, *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r);
-        } catch (const SolverError&) {
-            if (r.iterations == 0) throw;  // CG failure; a rejected verify still reports timing
-        }
+        solve_schur(*m->data, *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r, true);
         out[0] = (double)r.iterations;
         out[1] = r.cg_ms;
         out[2] = r.iterations ? r.cg_ms / (double)r.iterations : 0.0;

@@ -204,6 +204,146 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
     }
 }
 
+// -------------------------------------------- fast path: stars of <= 32
+
+constexpr int kFastCap = 128;  // > 3 * 32 candidates
+constexpr int kFastWarps = 8;
+
+// For local vertex lv: its i-th neighbour w (i < 3, ascending) and the
+// i-th face k containing lv with the local vertices x, y following lv in the
+// face's oriented cycle [abc],[acd],[adb],[dcb].  Packed 4-bit fields.
+__device__ __forceinline__ int nbr_of(int lv, int i) { return i + (i >= lv); }
+__device__ __forceinline__ void face_of(int lv, int i, int& k, int& xi, int& yi) {
+    // rows: lv; entries (k, x, y) for i = 0, 1, 2
+    constexpr unsigned tab[4][3] = {{0x012, 0x123, 0x231}, {0x020, 0x203, 0x332},
+                                    {0x001, 0x130, 0x313}, {0x102, 0x210, 0x321}};
+    const unsigned e = tab[lv][i];
+    k = (int)(e >> 8);
+    xi = (int)((e >> 4) & 0xf);
+    yi = (int)(e & 0xf);
+}
+
+__global__ void __launch_bounds__(32 * kFastWarps)
+    star_groups_fast(int64_t nc, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                     const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
+                     int32_t* __restrict__ slot_mate, int32_t* __restrict__ big_list, int32_t* __restrict__ big_count,
+                     unsigned long long* err) {
+    __shared__ int32_t s_ekey[kFastWarps][kFastCap], s_eval[kFastWarps][kFastCap];
+    __shared__ unsigned long long s_fkey[kFastWarps][kFastCap];
+    __shared__ int32_t s_flo[kFastWarps][kFastCap], s_fhi[kFastWarps][kFastCap], s_fcnt[kFastWarps][kFastCap];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* ekey = s_ekey[warp];
+    int32_t* eval = s_eval[warp];
+    unsigned long long* fkey = s_fkey[warp];
+    int32_t* flo = s_flo[warp];
+    int32_t* fhi = s_fhi[warp];
+    int32_t* fcnt = s_fcnt[warp];
+    for (int i = lane; i < kFastCap; i += 32) {
+        ekey[i] = -1;
+        eval[i] = INT_MAX;
+        fkey[i] = ~0ull;
+        flo[i] = INT_MAX;
+        fhi[i] = -1;
+        fcnt[i] = 0;
+    }
+    __syncwarp();
+    constexpr unsigned mask = kFastCap - 1;
+    const bool do_faces = slot_mate != nullptr;
+    const int64_t nwarps = (int64_t)gridDim.x * kFastWarps;
+    for (int64_t vv = (int64_t)blockIdx.x * kFastWarps + warp; vv < nc; vv += nwarps) {
+        const int32_t v = (int32_t)vv;
+        const int64_t beg = star_ptr[vv];
+        const int m = (int)(star_ptr[vv + 1] - beg);
+        if (m > 32) {
+            if (lane == 0) big_list[atomicAdd(big_count, 1)] = v;
+            continue;
+        }
+        const bool act = lane < m;
+        int64_t t = 0;
+        int lv = 0;
+        int4 tet = make_int4(0, 0, 0, 0);
+        if (act) {
+            const int32_t inc = __ldg(star + beg + lane);
+            t = inc >> 2;
+            lv = inc & 3;
+            tet = ldtet(tets, t);
+        }
+        int eh[3] = {-1, -1, -1}, fh[3] = {-1, -1, -1};
+        int32_t eslot[3], fslot[3];
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int w = nbr_of(lv, i);
+                const int32_t b = tv(tet, w);
+                if (b <= v) continue;
+                eslot[i] = (int32_t)(6 * t + edge_index(lv, w));
+                unsigned h = hash32((uint32_t)b) & mask;
+                for (;;) {
+                    const int32_t old = atomicCAS(ekey + h, -1, b);
+                    if (old == -1 || old == b) break;
+                    h = (h + 1) & mask;
+                }
+                eh[i] = (int)h;
+                atomicMin(eval + h, eslot[i]);
+            }
+            if (do_faces) {
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    int k, xi, yi;
+                    face_of(lv, i, k, xi, yi);
+                    const int32_t x = tv(tet, xi), y = tv(tet, yi);
+                    if (x <= v || y <= v) continue;
+                    const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
+                                                         : ((unsigned long long)y << 32 | (uint32_t)x);
+                    unsigned h = hash64(key) & mask;
+                    for (;;) {
+                        const unsigned long long old = atomicCAS(fkey + h, ~0ull, key);
+                        if (old == ~0ull || old == key) break;
+                        h = (h + 1) & mask;
+                    }
+                    fh[i] = (int)h;
+                    fslot[i] = (int32_t)(4 * t + k);
+                    atomicMin(flo + h, fslot[i]);
+                    atomicMax(fhi + h, fslot[i]);
+                    atomicAdd(fcnt + h, 4 | (x < y ? 1 : 2) << 0);
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (eh[i] >= 0) edge_first[eslot[i]] = eval[eh[i]];
+            if (fh[i] >= 0) {
+                const int h = fh[i];
+                const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
+                // count in bits 2+, orientation bits accumulate below: one
+                // slot of each orientation gives exactly 4+1 + 4+2 = 11
+                const int count = c >> 2;
+                if (count > 2 || (count == 2 && c != 11)) {
+                    const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
+                    report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
+                }
+                slot_mate[fslot[i]] = count >= 2 ? (fslot[i] == lo ? hi : lo) : -1;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (eh[i] >= 0) {
+                ekey[eh[i]] = -1;
+                eval[eh[i]] = INT_MAX;
+            }
+            if (fh[i] >= 0) {
+                fkey[fh[i]] = ~0ull;
+                flo[fh[i]] = INT_MAX;
+                fhi[fh[i]] = -1;
+                fcnt[fh[i]] = 0;
+            }
+        }
+        __syncwarp();
+    }
+}
+
 struct WarpSync {
     __device__ void operator()() const { __syncwarp(); }
 };
@@ -476,10 +616,13 @@ extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cur
 extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                                      int32_t* edge_first, int32_t* slot_mate, int32_t* big_list, int32_t* big_count,
                                      unsigned long long* err, void* stream) {
-    const int64_t blocks = (nc + kWarpsPerBlock - 1) / kWarpsPerBlock;
-    const int grid = (int)(blocks < kSMs * 64 ? blocks : kSMs * 64);
-    star_groups<<<grid, 32 * kWarpsPerBlock, 0, (cudaStream_t)stream>>>(nc, star_ptr, star, tets, edge_first,
-                                                                        slot_mate, big_list, big_count, err); phg::count_launches(1);
+    // stars of <= 32 incidences: register-resident warp path; larger stars
+    // are deferred to star_groups_big (block per vertex)
+    const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
+    const int grid = (int)(blocks < kSMs * 8 ? blocks : kSMs * 8);
+    star_groups_fast<<<grid, 32 * kFastWarps, 0, (cudaStream_t)stream>>>(nc, star_ptr, star, tets, edge_first,
+                                                                         slot_mate, big_list, big_count, err);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

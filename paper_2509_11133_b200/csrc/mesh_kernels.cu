@@ -153,7 +153,25 @@ __global__ void diameter(const double* __restrict__ coords, const int32_t* __res
     if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
 }
 
+// index validation of uploaded tables (read_mesh's range check,
+// mesh.cpp:151-158): out = first offending position, or all ones
+__global__ void check_indices(const int32_t* __restrict__ a, int64_t n, int64_t nc, unsigned long long* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = a[i];
+        if (v < 0 || v >= nc) atomicMin(out, (unsigned long long)i);
+    }
+}
+
 }  // namespace
+
+extern "C" int phfem_gpu_check_indices(const int32_t* a, int64_t n, int64_t nc, unsigned long long* first_bad,
+                                       void* stream) {
+    if (n <= 0) return 0;
+    const int g = std::min<int64_t>(grid_for(n, 256), 148 * 16);
+    check_indices<<<g, 256, 0, (cudaStream_t)stream>>>(a, n, nc, first_bad);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
 
 extern "C" int phfem_gpu_kuhn_nodes(int nx, int ny, int nz, double lx, double ly, double lz, double jitter,
                                     uint64_t seed, double* coords, void* stream) {

@@ -1,0 +1,326 @@
+// Stage orchestration of the hot path: connectivity, refinement, fused
+// assembly + condensation.  Device-only sizes (nEd, nF, L) are read back once
+// per stage; device error slots are replayed in the reference's check order
+// so the same exception and message shape surface.  All transient buffers
+// live in the owner's Work so repeated passes reuse device memory.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "runtime.hpp"
+
+namespace phb {
+
+namespace {
+
+constexpr unsigned long long kNone = ~0ull;
+
+void reset_err(Work& w) {
+    w.err.alloc(PHG_ERR_COUNT);
+    w.err.fill_bytes(0xff);
+}
+
+// read several device scalars with one synchronisation
+template <class T, size_t N>
+std::array<T, N> read_many(const std::array<const T*, N>& src) {
+    static thread_local T* pinned = nullptr;
+    if (!pinned) check(cudaMallocHost(reinterpret_cast<void**>(&pinned), 64 * sizeof(T)), "pinned alloc");
+    for (size_t i = 0; i < N; ++i)
+        check(cudaMemcpyAsync(pinned + i, src[i], sizeof(T), cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    std::array<T, N> out;
+    for (size_t i = 0; i < N; ++i) out[i] = pinned[i];
+    return out;
+}
+
+std::string tri_str(const int32_t* f) {
+    return "[" + std::to_string(f[0] + 1) + " " + std::to_string(f[1] + 1) + " " + std::to_string(f[2] + 1) + "]";
+}
+
+void fetch_tri(const int32_t* dev, int64_t i, int32_t out[3]) {
+    check(cudaMemcpyAsync(out, dev + 3 * i, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+}
+
+// connectivity.cpp:62-68, 156-194 and mesh.cpp:80-82, in that order
+void replay_connectivity_errors(const std::vector<unsigned long long>& e, const MeshData& m, const Connectivity& c) {
+    if (e[PHG_ERR_VALENCE] != kNone)
+        throw MeshError("vertex " + std::to_string(e[PHG_ERR_VALENCE] + 1) +
+                        " is shared by more elements than the connectivity kernels support");
+    if (e[PHG_ERR_DUP_ORIENT] != kNone) {
+        const unsigned long long k = e[PHG_ERR_DUP_ORIENT];
+        throw MeshError("inconsistent mesh: elements " + std::to_string((k >> 32) + 1) + " and " +
+                        std::to_string((k & 0xffffffffull) + 1) + " claim the same oriented face");
+    }
+    if (e[PHG_ERR_CLASSIFY] != kNone) {
+        const int64_t i = (int64_t)(e[PHG_ERR_CLASSIFY] >> 2);
+        const int kind = (int)(e[PHG_ERR_CLASSIFY] & 3);
+        int32_t tri[3];
+        const bool dir = i < m.nd;
+        fetch_tri(dir ? m.db.p : m.nb.p, dir ? i : i - m.nd, tri);
+        const std::string what = dir ? "Dirichlet" : "Neumann";
+        if (kind == 0) throw MeshError("inconsistent mesh: " + what + " face " + tri_str(tri) + " matches no element face");
+        if (kind == 1) throw MeshError("inconsistent mesh: boundary face " + tri_str(tri) + " listed twice");
+        throw MeshError("inconsistent mesh: " + what + " face " + tri_str(tri) + " is interior");
+    }
+    if (e[PHG_ERR_FACE] != kNone) {
+        const int64_t f = (int64_t)(e[PHG_ERR_FACE] >> 2);
+        const int kind = (int)(e[PHG_ERR_FACE] & 3);
+        int32_t tri[3];
+        fetch_tri(c.faces.p, f, tri);
+        if (kind == 0) throw MeshError("degenerate face with collinear nodes " + tri_str(tri));
+        throw MeshError("inconsistent mesh: boundary face " + tri_str(tri) +
+                        " is in neither the Dirichlet nor the Neumann list");
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ connectivity
+
+void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st) {
+    const int64_t nc = m.nc, ne = m.ne;
+    Work& w = c.w;
+    Timer tm;
+    const auto w0 = std::chrono::steady_clock::now();
+    reset_err(w);
+    w.scratch.alloc((int64_t)phfem_gpu_scan_scratch(std::max<int64_t>({nc, ne, 4 * ne})));
+    // 1. vertex star (CSR by vertex)
+    tm.start();
+    w.cnt.alloc(nc);
+    w.cnt.zero();
+    check(phfem_gpu_star_count(m.tets.p, ne, w.cnt.p, SV()), "star count");
+    c.star_ptr.alloc(nc + 1);
+    check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, nc, w.scratch.p, SV()), "star scan");
+    w.cursor.alloc(nc);
+    if (nc) check(cudaMemcpyAsync(w.cursor.p, c.star_ptr.p, sizeof(int64_t) * nc, cudaMemcpyDeviceToDevice, S()), "D2D");
+    c.star.alloc(4 * ne);
+    check(phfem_gpu_star_fill(m.tets.p, ne, w.cursor.p, c.star.p, SV()), "star fill");
+    if (st) st->star += tm.stop_ms();
+    // 2. per-vertex grouping of edges and faces
+    tm.start();
+    c.edge_first.alloc(6 * ne);
+    if (faces) c.slot_mate.alloc(4 * ne);
+    w.big_list.alloc(nc > 0 ? nc : 1);
+    w.big_count.alloc(1);
+    w.big_count.zero();
+    check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
+                                w.big_list.p, w.big_count.p, w.err.p, SV()),
+          "star groups");
+    // 3. numbering: per-element counts and scans are independent of the big
+    //    stars' outcome only after they finish, so those run first
+    w.ecount.alloc(ne);
+    if (faces) w.fcount.alloc(ne);
+    const int32_t n_big = read_scalar(w.big_count.p);
+    if (n_big > 0) {
+        std::vector<int32_t> big((size_t)n_big);
+        check(cudaMemcpyAsync(big.data(), w.big_list.p, sizeof(int32_t) * n_big, cudaMemcpyDeviceToHost, S()), "D2H");
+        const std::vector<int64_t> ptr = c.star_ptr.download();
+        int max_star = 0;
+        for (int32_t v : big) max_star = std::max<int>(max_star, (int)(ptr[v + 1] - ptr[v]));
+        check(phfem_gpu_star_groups_big(n_big, w.big_list.p, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                        faces ? c.slot_mate.p : nullptr, max_star, w.err.p, SV()),
+              "star groups (big)");
+    }
+    if (st) st->groups += tm.stop_ms();
+    tm.start();
+    c.edge_off.alloc(ne + 1);
+    if (faces) w.face_off.alloc(ne + 1);
+    check(phfem_gpu_element_counts(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.ecount.p,
+                                   faces ? w.fcount.p : nullptr, SV()),
+          "element counts");
+    check(phfem_gpu_scan_i32(w.ecount.p, c.edge_off.p, ne, w.scratch.p, SV()), "edge scan");
+    if (faces) {
+        check(phfem_gpu_scan_i32(w.fcount.p, w.face_off.p, ne, w.scratch.p, SV()), "face scan");
+        const auto tot = read_many<int64_t, 2>({c.edge_off.p + ne, w.face_off.p + ne});
+        c.ned = tot[0];
+        c.nf = tot[1];
+    } else {
+        c.ned = read_scalar(c.edge_off.p + ne);
+    }
+    c.edge_of_slot.alloc(6 * ne);
+    c.edge_nodes.alloc(2 * c.ned);
+    if (faces) {
+        c.face_of_slot.alloc(4 * ne);
+        c.sigma.alloc(4 * ne);
+        c.faces.alloc(3 * c.nf);
+        c.face_slots.alloc(2 * c.nf);
+        c.face_area.alloc(c.nf);
+    }
+    check(phfem_gpu_number(ne, m.tets.p, m.coords.p, c.edge_first.p, c.edge_off.p, c.edge_of_slot.p, c.edge_nodes.p,
+                           faces ? c.slot_mate.p : nullptr, faces ? w.face_off.p : nullptr,
+                           faces ? c.face_of_slot.p : nullptr, faces ? c.sigma.p : nullptr,
+                           faces ? c.faces.p : nullptr, faces ? c.face_slots.p : nullptr,
+                           faces ? c.face_area.p : nullptr, w.err.p, SV()),
+          "number");
+    check(phfem_gpu_fill_slots(ne, c.edge_first.p, c.edge_of_slot.p, faces ? c.slot_mate.p : nullptr,
+                               faces ? c.face_of_slot.p : nullptr, faces ? c.sigma.p : nullptr, SV()),
+          "fill slots");
+    if (st) st->number += tm.stop_ms();
+    c.has_edges = true;
+    c.has_faces = false;
+    c.t_edges = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
+    if (!faces) {
+        replay_connectivity_errors(w.err.download(), m, c);
+        return;
+    }
+    // 4. boundary classification and multiplier rows
+    const auto w1 = std::chrono::steady_clock::now();
+    tm.start();
+    const int64_t nf = c.nf;
+    w.claim.alloc(nf);
+    w.claim.fill_bytes(0xff);
+    check(phfem_gpu_classify(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
+                             c.face_slots.p, w.claim.p, w.err.p, SV()),
+          "classify");
+    check(phfem_gpu_classify_check(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
+                                   w.claim.p, w.err.p, SV()),
+          "classify check");
+    c.face_class.alloc(nf);
+    w.is_row.alloc(nf);
+    w.counts.alloc(3);
+    w.counts.zero();
+    check(phfem_gpu_face_class(nf, m.nd, w.claim.p, c.face_slots.p, c.face_area.p, c.face_class.p, w.is_row.p,
+                               w.counts.p, w.err.p, SV()),
+          "face class");
+    w.row_off.alloc(nf + 1);
+    check(phfem_gpu_scan_i32(w.is_row.p, w.row_off.p, nf, w.scratch.p, SV()), "row scan");
+    const auto cnt = read_many<unsigned long long, 4>(
+        {w.counts.p, w.counts.p + 1, w.counts.p + 2, reinterpret_cast<const unsigned long long*>(w.row_off.p + nf)});
+    c.n_int = (int64_t)cnt[0];
+    c.n_dir = (int64_t)cnt[1];
+    c.n_neu = (int64_t)cnt[2];
+    c.l = (int64_t)cnt[3];
+    c.face_mrow.alloc(nf);
+    c.row_face.alloc(c.l);
+    check(phfem_gpu_face_rows(nf, c.face_class.p, w.row_off.p, c.face_mrow.p, c.row_face.p, SV()), "face rows");
+    if (st) st->classify += tm.stop_ms();
+    replay_connectivity_errors(w.err.download(), m, c);
+    c.has_faces = true;
+    c.t_faces = std::chrono::duration<double>(std::chrono::steady_clock::now() - w1).count();
+}
+
+// -------------------------------------------------------------- refinement
+
+std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st,
+                                      std::shared_ptr<MeshData> into) {
+    if (!c.has_edges) throw MeshError("refine_mesh: edge table missing");
+    const int64_t nc2 = m.nc + c.ned + m.ne;
+    const int64_t ne2 = 12 * m.ne;
+    if (nc2 >= (int64_t)INT32_MAX || 6 * ne2 >= (int64_t)INT32_MAX)
+        throw MeshError("out of memory while refining to level " + std::to_string(m.level + 1) +
+                        ": 32-bit node/element ids exhausted");
+    Timer tm;
+    tm.start();
+    auto out = into ? into : std::make_shared<MeshData>();
+    out->nc = nc2;
+    out->ne = ne2;
+    out->nd = 4 * m.nd;
+    out->nn = 4 * m.nn;
+    out->level = m.level + 1;
+    out->coords.alloc(3 * nc2);
+    out->tets.alloc(4 * ne2);
+    out->db.alloc(3 * out->nd);
+    out->nb.alloc(3 * out->nn);
+    if (map) {
+        map->midpoint.alloc(c.ned);
+        map->centroid.alloc(m.ne);
+    }
+    Work& w = c.w;
+    reset_err(w);
+    check(phfem_gpu_refine(m.nc, m.ne, m.coords.p, m.tets.p, c.edge_first.p, c.edge_of_slot.p, c.edge_off.p,
+                           out->coords.p, out->tets.p, map ? map->midpoint.p : nullptr,
+                           map ? map->centroid.p : nullptr, SV()),
+          "refine");
+    check(phfem_gpu_refine_boundary(m.nd, m.db.p, 0, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                    c.edge_of_slot.p, out->db.p, w.err.p, SV()),
+          "refine boundary");
+    check(phfem_gpu_refine_boundary(m.nn, m.nb.p, m.nd, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                    c.edge_of_slot.p, out->nb.p, w.err.p, SV()),
+          "refine boundary");
+    const double ms = tm.stop_ms();
+    if (st) st->refine += ms;
+    const auto e = w.err.download();
+    if (e[PHG_ERR_BOUNDARY_EDGE] != kNone) {
+        const int64_t i = (int64_t)(e[PHG_ERR_BOUNDARY_EDGE] >> 2);
+        const int q = (int)(e[PHG_ERR_BOUNDARY_EDGE] & 3);
+        int32_t tri[3];
+        const bool dir = i < m.nd;
+        fetch_tri(dir ? m.db.p : m.nb.p, dir ? i : i - m.nd, tri);
+        const int32_t a = q == 1 ? tri[1] : tri[0], b = q == 0 ? tri[1] : tri[2];
+        throw MeshError("inconsistent mesh: boundary face edge (" + std::to_string(a + 1) + "," +
+                        std::to_string(b + 1) + ") is not an element edge");
+    }
+    return out;
+}
+
+// ------------------------------------------------------ assembly + Schur
+
+phg_problem device_problem(const Coefs& k, int problem) {
+    phg_problem p;
+    p.kind = problem;
+    p.c = k.c;
+    p.a_elem = k.has_elem ? k.a_elem.p : nullptr;
+    p.a_diag = k.has_diag ? k.a_diag.p : nullptr;
+    return p;
+}
+
+void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
+                     bool debug_views, Stages* st) {
+    if (!c.has_faces) throw MeshError("assemble: face table missing");
+    if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
+    Timer tm;
+    tm.start();
+    sys.problem = problem;
+    sys.coef_version = k.version;
+    sys.n = 4 * m.ne;
+    sys.l = c.l;
+    sys.nchunks = (c.l + PHG_SELL_C - 1) / PHG_SELL_C;
+    const int64_t width = PHG_SELL_C * PHG_SELL_W;
+    sys.sell_col.alloc(sys.nchunks * width);
+    sys.sell_val.alloc(sys.nchunks * width);
+    if (sys.nchunks)
+        check(cudaMemset2DAsync(sys.sell_val.p, width * sizeof(double), 0, PHG_SELL_C * sizeof(double),
+                                (size_t)sys.nchunks, S()),
+              "memset diag");
+    sys.rhs_neg.alloc(c.l);
+    sys.rhs_neg.zero();
+    sys.bd.alloc(c.l);
+    sys.bd.zero();
+    sys.rhs.alloc(4 * m.ne);
+    if (debug_views) {
+        sys.a_blocks.alloc(16 * m.ne);
+        sys.slot_coef.alloc(4 * m.ne);
+        sys.slot_mrow.alloc(4 * m.ne);
+    } else {
+        sys.a_blocks.release();
+        sys.slot_coef.release();
+        sys.slot_mrow.release();
+    }
+    const int grid = phfem_gpu_assemble_grid(m.ne);
+    Work& w = sys.w;
+    w.partials.alloc(2 * (int64_t)grid);
+    w.norms.alloc(2);
+    reset_err(w);
+    const phg_problem p = device_problem(k, problem);
+    check(phfem_gpu_assemble_condense(m.ne, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
+                                      c.face_mrow.p, c.face_area.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
+                                      sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
+                                      debug_views ? sys.slot_coef.p : nullptr,
+                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.err.p, SV()),
+          "assemble");
+    const double ms = tm.stop_ms();
+    if (st) st->assemble += ms;
+    const auto nv = read_many<double, 2>({w.norms.p, w.norms.p + 1});
+    sys.sum_rhs2 = nv[0];
+    sys.sum_bd2 = nv[1];
+    const auto e = w.err.download();
+    // assembly.cpp:13-14 (first element in order), then solver.cpp:128-129
+    if (e[PHG_ERR_ZERO_VOLUME] != kNone)
+        throw MeshError("degenerate element " + std::to_string(e[PHG_ERR_ZERO_VOLUME] + 1) + " (zero volume)");
+    if (e[PHG_ERR_SINGULAR] != kNone)
+        throw MeshError("degenerate element block " + std::to_string(e[PHG_ERR_SINGULAR] + 1));
+}
+
+}  // namespace phb

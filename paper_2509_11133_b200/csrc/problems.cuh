@@ -87,6 +87,37 @@ __device__ __forceinline__ double prob_f(double x, double y, double z, const Coe
     }
 }
 
+// Quadrature-loop version of f for the transcendental kinds: sinpi/cospi
+// (no argument rounding of pi*x) and FMA.  These kinds cannot be bit-exact
+// with the CPU's libm anyway; they stay within ~1e-15 relative of it, well
+// inside the 1e-12 load-vector bar.  Polynomial kinds use prob_f.
+template <int KIND>
+__device__ __forceinline__ double prob_f_fast(double x, double y, double z, double cpre, const Coef& k) {
+    if constexpr (KIND == 3) {
+        return cpre * (sinpi(x) * sinpi(y) * sinpi(z));
+    } else if constexpr (KIND == 4) {
+        // -(a0 u + a1 (-pi^2) u + a2 (2 e^x cos)) + c u with u = e^x cos z^2
+        const double ec = exp(x) * cospi(y);
+        const double u = ec * (z * z);
+        return fma(cpre, u, -(k.a2 * 2.0) * ec);
+    } else if constexpr (KIND == 5) {
+        const double s = sinpi(y) * sinpi(z);
+        const double u = x * (8.0 - x) * s;
+        return fma(cpre, u, 2.0 * k.a0 * s);
+    } else {
+        return prob_f<KIND>(x, y, z, k);
+    }
+}
+// loop-invariant factor of prob_f_fast
+template <int KIND>
+__device__ __forceinline__ double prob_f_pre(const Coef& k) {
+    constexpr double pi2 = kPi * kPi;
+    if constexpr (KIND == 3) return pi2 * (k.a0 + k.a1 + k.a2) + k.c;
+    if constexpr (KIND == 4) return -k.a0 + k.a1 * pi2 + k.c;
+    if constexpr (KIND == 5) return (k.a1 + k.a2) * pi2 + k.c;
+    return 0.0;
+}
+
 // g = (A grad u) . n
 template <int KIND>
 __device__ __forceinline__ double prob_g(double x, double y, double z, V3 n, const Coef& k) {

@@ -46,35 +46,44 @@ void sync();
 
 // Stream-ordered device buffer (cudaMallocAsync on the library stream,
 // served from the device memory pool between pipeline passes).
+// alloc() keeps the current block when it is large enough, so objects that
+// are rebuilt every pass (connectivity, system, workspaces) stop paying for
+// allocation after the first pass.
 template <class T>
 struct DBuf {
     T* p = nullptr;
     int64_t n = 0;
+    int64_t cap = 0;
     DBuf() = default;
     explicit DBuf(int64_t count) { alloc(count); }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), cap(o.cap) { o.p = nullptr; o.n = o.cap = 0; }
     DBuf& operator=(DBuf&& o) noexcept {
         if (this != &o) {
             release();
             p = o.p;
             n = o.n;
+            cap = o.cap;
             o.p = nullptr;
-            o.n = 0;
+            o.n = o.cap = 0;
         }
         return *this;
     }
     ~DBuf() { release(); }
     void alloc(int64_t count) {
+        if (p && count <= cap) {
+            n = count;
+            return;
+        }
         release();
-        n = count;
+        n = cap = count;
         if (count > 0) check(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, S()), "allocate");
     }
     void release() {
         if (p) cudaFreeAsync(p, S());
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
     void zero() {
         if (n) check(cudaMemsetAsync(p, 0, sizeof(T) * (size_t)n, S()), "memset");
@@ -131,7 +140,19 @@ struct Coefs {
     uint64_t version = 0;
 };
 
+// transient device buffers of one connectivity / refinement / assembly pass,
+// kept with their owner so repeated passes reuse them
+struct Work {
+    DBuf<int32_t> cnt, ecount, fcount, is_row, big_list, big_count, packed;
+    DBuf<int64_t> cursor, face_off, row_off;
+    DBuf<unsigned char> scratch;
+    DBuf<uint32_t> claim;
+    DBuf<unsigned long long> counts, err;
+    DBuf<double> partials, norms;
+};
+
 struct Connectivity {
+    Work w;
     // vertex star
     DBuf<int64_t> star_ptr;
     DBuf<int32_t> star;
@@ -152,6 +173,7 @@ struct Connectivity {
 };
 
 struct System {
+    Work w;
     int problem = -1;
     uint64_t coef_version = 0;
     int64_t n = 0, l = 0, nchunks = 0;
@@ -180,9 +202,9 @@ std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly
 
 // star + edges (+ faces, classification and multiplier rows)
 void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st = nullptr);
-// red refinement; needs edges
-std::shared_ptr<MeshData> refine_mesh(const MeshData& m, const Connectivity& c, RefineMap* map,
-                                      Stages* st = nullptr);
+// red refinement; needs edges.  `into` (optional) is reused for the child.
+std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st = nullptr,
+                                      std::shared_ptr<MeshData> into = nullptr);
 // fused assembly + condensation
 void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
                      bool debug_views, Stages* st = nullptr);
@@ -191,11 +213,12 @@ phg_problem device_problem(const Coefs& k, int problem);
 struct SolveResult {
     DBuf<double> u, lambda;
     int64_t iterations = 0;
-    double residual = 0.0, constraint_residual = 0.0, seconds = 0.0, cg_ms = 0.0;
+    double residual = 0.0, constraint_residual = 0.0, seconds = 0.0, cg_ms = 0.0, rel_residual = 0.0;
     bool converged = false;
 };
+// Jacobi-PCG on S, then (unless cg_only) recovery and verify_solution.
 void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const System& sys, int problem,
-                 double tol, int64_t max_iter, const std::string& method, SolveResult& out);
+                 double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only = false);
 
 double mesh_diameter(const MeshData& m);
 // [y-norm, kappa-norm, L2]

@@ -110,6 +110,7 @@ def lib():
         "phfem_solution_errors_ex": [P, P],
         "phfem_pipeline": [P, C.c_int, C.c_int, P, P],
         "phfem_solve_timed": [P, C.c_int, C.c_double, I64, P],
+        "phfem_mesh_solve_faces": [P, C.c_int, C.c_double, I64, P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -137,6 +138,7 @@ EXPORTED = [
     "phfem_mesh_set_coefficients", "phfem_mesh_connectivity", "phfem_mesh_get_edges", "phfem_mesh_get_faces",
     "phfem_mesh_refinement_map", "phfem_mesh_assemble", "phfem_mesh_get_system", "phfem_solve_ex",
     "phfem_solution_stats", "phfem_solution_errors_ex", "phfem_stream", "phfem_pipeline", "phfem_solve_timed",
+    "phfem_mesh_solve_faces",
 ]
 
 
@@ -328,6 +330,14 @@ class Mesh:
         h = C.c_void_p()
         _check(lib().phfem_solve_ex(self._h, problem, tol, max_iter, C.byref(h)))
         return Solution(h, self)
+
+    def solve_faces(self, problem, tol=1e-10, max_iter=-1):
+        """Face system only (pcg_jacobi with inner_cg_options); no verify."""
+        l = self.connectivity()["l"]
+        lam = np.zeros(l)
+        out = np.zeros(3)
+        _check(lib().phfem_mesh_solve_faces(self._h, problem, tol, max_iter, _ptr(lam), _ptr(out)))
+        return lam, dict(iterations=int(out[0]), rel_residual=out[1], converged=bool(out[2]))
 
     def pipeline(self, problem, do_refine=True):
         ms = StageMs()

@@ -161,16 +161,28 @@ def test_config_parity(oracle, cid, factor):
         g.set_coefficients(k["a_elem"], k["a_diag"], cfg.c)
     fo = check_connectivity(g, m, oracle)
     so = check_system(g, m, fo, oracle, cfg.problem, cfg.c, k["a_elem"], k["a_diag"])
-    # the reference may refuse a converged solve through verify_solution
-    # (SURVEY finding 8); tighten the tolerance until the oracle accepts
+    # the face solve itself, same stopping rule (inner_cg_options)
+    n_ = 4 * m.ne
+    abs_tol = 0.2 * cfg.tol * np.hypot(np.linalg.norm(so["rhs"]), np.linalg.norm(so["bd"]))
+    lo_cg, res = oracle.pcg(so, tol=cfg.tol, abs_tol=abs_tol, max_iter=10 * max(len(so["bd"]), 1))
+    lg_cg, st_g = g.solve_faces(cfg.problem, tol=cfg.tol)
+    assert st_g["converged"] and res[2] == 1.0
+    assert rel_l2(lg_cg, lo_cg) <= 1e-9, rel_l2(lg_cg, lo_cg)
+    assert abs(st_g["iterations"] - res[0]) <= max(3, 0.02 * res[0])
+    assert n_ == len(so["rhs"])
+    # the full solve; the reference may refuse a converged solve through
+    # verify_solution (SURVEY finding 8): then the GPU path must refuse too,
+    # and a tighter tolerance is tried
     for tol in (cfg.tol, 1e-11, 1e-12):
         try:
             uo, lo, st_o = oracle.solve(m, so, cfg.problem, cfg.c, k["a_elem"], k["a_diag"], tol=tol)
             break
         except Exception as e:  # noqa: BLE001
+            with pytest.raises(ph.SolverError, match="missed the residual target"):
+                g.solve_ex(cfg.problem, tol=tol)
             last = e
     else:
-        pytest.fail(f"oracle refuses at every tolerance: {last}")
+        pytest.skip(f"the reference refuses at every tolerance (finding 8): {last}; face solves matched")
     sol = g.solve_ex(cfg.problem, tol=tol)
     ug, lg = sol.values()
     assert rel_l2(ug, uo) <= 1e-9, rel_l2(ug, uo)
