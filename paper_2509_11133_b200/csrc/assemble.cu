@@ -208,47 +208,57 @@ __global__ void __launch_bounds__(kCondThreads)
             report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
             continue;
         }
-        double cr[4][4];
+        // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
+        // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
+        auto cr = [&](int r, int v) -> double {
+            const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
+            return on ? coef[r] : 0.0;
+        };
+        // one solved column x = A^-1 c_q at a time: S_T[r][q] for all r,
+        // accumulated over p = 0..3 exactly as solver.cpp:121-125
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int q = 0; q < 4; ++q) {
+            if (sl.row[q] < 0) {
+                // Neumann column: padding in the rows of the other faces
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
-                cr[r][v] = on ? coef[r] : 0.0;
+                for (int r = 0; r < 4; ++r) {
+                    if (r == q || sl.row[r] < 0) continue;
+                    const int64_t R = sl.row[r];
+                    const int64_t ix = sell_idx(R, (sl.owner[r] ? 0 : 3) + 1 + (q < r ? q : q - 1));
+                    sell_col[ix] = (int32_t)R;
+                    sell_val[ix] = 0.0;
+                }
+                continue;
             }
-        double ainv_c[4][4], ainv_b[4];
+            const double cq[4] = {cr(q, 0), cr(q, 1), cr(q, 2), cr(q, 3)};
+            double x[4];
+            lu_solve(lu, cq, x);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) lu_solve(lu, cr[q], ainv_c[q]);
+            for (int r = 0; r < 4; ++r) {
+                if (sl.row[r] < 0) continue;
+                double s = 0.0;
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
+                const int64_t R = sl.row[r];
+                if (q == r) {
+                    atomicAdd(sell_val + sell_idx(R, 0), s);
+                    sell_col[sell_idx(R, 0)] = (int32_t)R;
+                } else {
+                    const int64_t ix = sell_idx(R, (sl.owner[r] ? 0 : 3) + 1 + (q < r ? q : q - 1));
+                    sell_col[ix] = sl.row[q];
+                    sell_val[ix] = s;
+                }
+            }
+        }
+        double ainv_b[4];
         lu_solve(lu, rhs, ainv_b);
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             if (sl.row[r] < 0) continue;
             double rb = 0.0;
 #pragma unroll
-            for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr[r][pp], ainv_b[pp]));
+            for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
             const int64_t R = sl.row[r];
-            const int base = sl.owner[r] ? 0 : 3;
-            int j = 1;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                double s = 0.0;
-#pragma unroll
-                for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr[r][pp], ainv_c[q][pp]));
-                if (q == r) {
-                    atomicAdd(sell_val + sell_idx(R, 0), s);
-                    sell_col[sell_idx(R, 0)] = (int32_t)R;
-                } else {
-                    const int64_t ix = sell_idx(R, base + j);
-                    ++j;
-                    if (sl.row[q] >= 0) {
-                        sell_col[ix] = sl.row[q];
-                        sell_val[ix] = s;
-                    } else {
-                        sell_col[ix] = (int32_t)R;
-                        sell_val[ix] = 0.0;
-                    }
-                }
-            }
             if (sl.bnd[r]) {
 #pragma unroll
                 for (int pos = 4; pos < 7; ++pos) {
@@ -277,13 +287,29 @@ __global__ void __launch_bounds__(kCondThreads)
     }
 }
 
-__global__ void reduce_pairs(const double* __restrict__ partials, int n, double* __restrict__ out) {
+__global__ void __launch_bounds__(1024) reduce_pairs(const double* __restrict__ partials, int n,
+                                                     double* __restrict__ out) {
     __shared__ double sh[32];
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        a = add(a, partials[2 * i]);
-        b = add(b, partials[2 * i + 1]);
+    // fixed-shape tree: 4 independent strided chains per thread, then the
+    // block tree; deterministic for a given n
+    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+    const double2* pp = reinterpret_cast<const double2*>(partials);
+    int i = threadIdx.x;
+    for (; i + 3 * (int)blockDim.x < n; i += 4 * blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double2 v = pp[i + u * blockDim.x];
+            a4[u] = add(a4[u], v.x);
+            b4[u] = add(b4[u], v.y);
+        }
     }
+    for (; i < n; i += blockDim.x) {
+        const double2 v = pp[i];
+        a4[0] = add(a4[0], v.x);
+        b4[0] = add(b4[0], v.y);
+    }
+    double a = add(add(a4[0], a4[1]), add(a4[2], a4[3]));
+    double b = add(add(b4[0], b4[1]), add(b4[2], b4[3]));
     a = block_sum(a, sh);
     b = block_sum(b, sh);
     if (threadIdx.x == 0) {
@@ -303,10 +329,12 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
     return rc ? rc : phfem_gpu_set_rules_errors(lam9, w9);
 }
 
-// both kernels use the same fixed grid so their partial arrays line up
+// One element per thread, blocks in element order: the elements in flight
+// (and so the S rows they scatter into) stay within an L2-resident window;
+// a grid-stride loop spread them over ~600k elements and turned the
+// scattered SELL writes into DRAM read-modify-writes (ncu, profiles/).
 extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
-    const int g = grid_for(ne, kLoadThreads);
-    return g < kSMs * 32 ? g : kSMs * 32;
+    return grid_for(ne, kLoadThreads);
 }
 
 extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
@@ -335,7 +363,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, con
         default: return (int)cudaErrorInvalidValue;
     }
 #undef PHG_ASM
-    reduce_pairs<<<1, 256, 0, s>>>(partials, grid, norms);
+    reduce_pairs<<<1, 1024, 0, s>>>(partials, grid, norms);
     phg::count_launches(3);
     return (int)cudaGetLastError();
 }

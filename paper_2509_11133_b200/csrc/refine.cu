@@ -17,6 +17,82 @@ namespace {
 
 using namespace phg;
 
+// Block-staged version: a block owns kRefBlock consecutive parents, whose
+// children 1..11 form one contiguous run of 11*kRefBlock rows and whose new
+// nodes (centroid + first-seen midpoints, in element order) form one
+// contiguous run of coordinates.  Both runs are assembled in shared memory
+// and streamed out with coalesced 16-byte stores.
+constexpr int kRefBlock = 128;
+
+__global__ void __launch_bounds__(kRefBlock)
+    refine_staged(int64_t nc, int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets,
+                  const int32_t* __restrict__ edge_first, const int32_t* __restrict__ edge_of_slot,
+                  const int64_t* __restrict__ edge_off, double* __restrict__ coords_out,
+                  int32_t* __restrict__ tets_out, int32_t* __restrict__ midpoint_node,
+                  int32_t* __restrict__ centroid_node) {
+    __shared__ int4 s_child[11 * kRefBlock];
+    __shared__ double s_xyz[3 * 7 * kRefBlock];
+    const int64_t t0 = (int64_t)blockIdx.x * kRefBlock;
+    const int64_t t = t0 + threadIdx.x;
+    const int64_t tend = t0 + kRefBlock < ne ? t0 + kRefBlock : ne;
+    // node run of this block: [node0, node1)
+    const int64_t node0 = nc + t0 + edge_off[t0];
+    const int64_t node1 = nc + tend + edge_off[tend];
+    if (t < ne) {
+        const int4 e = ldtet(tets, t);
+        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+        const int64_t c = nc + t + edge_off[t];
+        const V3 ct = vdiv(vadd(vadd(vadd(p[0], p[1]), p[2]), p[3]), 4.0);  // refine.cpp:33-34
+        int64_t loc = c - node0;
+        s_xyz[3 * loc] = ct.x;
+        s_xyz[3 * loc + 1] = ct.y;
+        s_xyz[3 * loc + 2] = ct.z;
+        if (centroid_node) centroid_node[t] = (int32_t)c;
+        int32_t mid[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int64_t s = 6 * t + k;
+            const int32_t first = edge_first[s];
+            const int32_t id = edge_of_slot[s];
+            const int64_t node = nc + first / 6 + 1 + id;
+            mid[k] = (int32_t)node;
+            if (first == (int32_t)s) {
+                const int a = k < 3 ? 0 : (k < 5 ? 1 : 2);
+                const int b = k < 3 ? k + 1 : (k < 5 ? k - 1 : 3);
+                const V3 pm = vdiv(vadd(p[a], p[b]), 2.0);  // refine.cpp:43
+                loc = node - node0;
+                s_xyz[3 * loc] = pm.x;
+                s_xyz[3 * loc + 1] = pm.y;
+                s_xyz[3 * loc + 2] = pm.z;
+                if (midpoint_node) midpoint_node[id] = (int32_t)node;
+            }
+        }
+        const int32_t i = e.x, j = e.y, k = e.z, l = e.w;
+        const int32_t ij = mid[0], ik = mid[1], il = mid[2], jk = mid[3], jl = mid[4], kl = mid[5];
+        const int32_t cc = (int32_t)c;
+        reinterpret_cast<int4*>(tets_out)[t] = make_int4(i, ij, ik, il);  // child 0 keeps slot t
+        int4* rest = s_child + 11 * threadIdx.x;  // refine.cpp:58-61
+        rest[0] = make_int4(j, jk, ij, jl);
+        rest[1] = make_int4(k, ik, jk, kl);
+        rest[2] = make_int4(l, kl, jl, il);
+        rest[3] = make_int4(ij, ik, il, cc);
+        rest[4] = make_int4(jk, ij, jl, cc);
+        rest[5] = make_int4(ik, jk, kl, cc);
+        rest[6] = make_int4(kl, jl, il, cc);
+        rest[7] = make_int4(ij, jk, ik, cc);
+        rest[8] = make_int4(ik, kl, il, cc);
+        rest[9] = make_int4(ij, il, jl, cc);
+        rest[10] = make_int4(kl, jk, jl, cc);
+    }
+    __syncthreads();
+    const int nrows = 11 * (int)(tend - t0);
+    int4* dst = reinterpret_cast<int4*>(tets_out) + ne + 11 * t0;
+    for (int r = threadIdx.x; r < nrows; r += kRefBlock) dst[r] = s_child[r];
+    const int nval = 3 * (int)(node1 - node0);
+    double* dxyz = coords_out + 3 * node0;
+    for (int r = threadIdx.x; r < nval; r += kRefBlock) dxyz[r] = s_xyz[r];
+}
+
 __global__ void __launch_bounds__(128)
     refine_k(int64_t nc, int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets,
              const int32_t* __restrict__ edge_first, const int32_t* __restrict__ edge_of_slot,
@@ -126,7 +202,9 @@ extern "C" int phfem_gpu_refine(int64_t nc, int64_t ne, const double* coords, co
                                 void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemcpyAsync(coords_out, coords, (size_t)(3 * nc) * sizeof(double), cudaMemcpyDeviceToDevice, s);
-    refine_k<<<grid_for(ne, 128), 128, 0, s>>>(nc, ne, coords, tets, edge_first, edge_of_slot, edge_off, coords_out,
+    if (ne == 0) return (int)cudaGetLastError();
+    refine_staged<<<(unsigned)((ne + kRefBlock - 1) / kRefBlock), kRefBlock, 0, s>>>(nc, ne, coords, tets, edge_first,
+                                                                                   edge_of_slot, edge_off, coords_out,
                                                tets_out, midpoint_node, centroid_node); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
