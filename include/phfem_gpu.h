@@ -229,6 +229,10 @@ int phfem_gpu_sell_row_nnz(int64_t l, const int32_t* sell_col, int32_t* row_nnz,
 int phfem_gpu_sell_to_csr(int64_t l, const int32_t* sell_col, const double* sell_val,
                           const int64_t* row_ptr, int32_t* col, double* val, void* stream);
 
+/* self-test: n random quotients of the kernels' shared-reciprocal division
+ * compared bit for bit with IEEE division; *mismatches (device) += count */
+int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream);
+
 /* kernels launched by this library since load (benchmark accounting) */
 long long phfem_gpu_launch_count(void);
 

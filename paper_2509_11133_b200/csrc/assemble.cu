@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kLoadThreads)
             report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
             continue;
         }
-        const double vol = dvd(fabs(det), 6.0);
+        const double vol = dq(fabs(det), kDiv6);
         double b[4] = {0.0, 0.0, 0.0, 0.0};
         if constexpr (KIND <= 2) {
             // polynomial data: the reference's exact operation order
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kCondThreads)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
             const double sg = sl.owner[q] ? 1.0 : -1.0;
-            coef[q] = dvd(mul(sg, __ldg(face_area + sl.face[q])), 3.0);
+            coef[q] = dq(mul(sg, __ldg(face_area + sl.face[q])), kDiv3);
         }
         if (a_blocks) {
 #pragma unroll
@@ -182,13 +182,13 @@ __global__ void __launch_bounds__(kCondThreads)
             if (!sl.bnd[q] || sl.row[q] >= 0) continue;
             const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
             const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
-            const V3 cen = vdiv(vadd(vadd(q0, q1), q2), 3.0);
+            const V3 cen = vdivq(vadd(vadd(q0, q1), q2), kDiv3);
             const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
             const double len = __dsqrt_rn(vdot(n, n));
             const double ar = mul(0.5, len);
-            const V3 un = vdiv(n, len);
+            const V3 un = vdivq(n, make_div(len));
             const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-            const double contrib = dvd(mul(ar, gc), 3.0);
+            const double contrib = dq(mul(ar, gc), kDiv3);
             ln[i0] = add(ln[i0], contrib);
             ln[i1] = add(ln[i1], contrib);
             ln[i2] = add(ln[i2], contrib);
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kCondThreads)
                 // b_D = |F| u_D(centroid) (assembly.cpp:96-104); the face's
                 // stored tuple is this slot's (owner) orientation
                 const int i0 = face_vert(r, 0), i1 = face_vert(r, 1), i2 = face_vert(r, 2);
-                const V3 cen = vdiv(vadd(vadd(p[i0], p[i1]), p[i2]), 3.0);
+                const V3 cen = vdivq(vadd(vadd(p[i0], p[i1]), p[i2]), kDiv3);
                 const double bdv = mul(__ldg(face_area + sl.face[r]), prob_u<KIND>(cen.x, cen.y, cen.z));
                 // rhs_neg = b_D - r_T (solver.cpp:131-138), single contributor
                 rhs_neg[R] = sub(bdv, rb);

@@ -18,6 +18,39 @@ __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, 
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
 
+// Correctly rounded division by a divisor shared by several quotients:
+// r = RN(1/b) once, then per quotient q0 = RN(a r), rem = a - b q0 (FMA,
+// exact), q = RN(q0 + rem r) (Markstein's correction, correctly rounded in
+// binary64 away from under/overflow).  Operands outside a safe exponent
+// window fall back to __ddiv_rn, so the result always equals a / b; the
+// GPU test test_division_matches_ieee checks this against __ddiv_rn.
+struct Div {
+    double b, r;
+    bool safe;
+};
+__device__ __forceinline__ Div make_div(double b) {
+    const double ab = fabs(b);
+    return {b, __drcp_rn(b), ab > 0x1.0p-500 && ab < 0x1.0p+500};
+}
+// constant divisors of the reference formulas with r = RN(1/b)
+static __device__ constexpr Div kDiv3 = {3.0, 0x1.5555555555555p-2, true};
+static __device__ constexpr Div kDiv6 = {6.0, 0x1.5555555555555p-3, true};
+static __device__ constexpr Div kDiv20 = {20.0, 0x1.999999999999ap-5, true};
+static __device__ __noinline__ double div_slow(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dq(double a, const Div& d) {
+    // |a|, |b| in [2^-500, 2^500]: q, a*r and the remainder stay normal
+    const double aa = fabs(a);
+    if (d.safe && aa < 0x1.0p+500) {
+        if (aa > 0x1.0p-500) {
+            const double q0 = __dmul_rn(a, d.r);
+            const double rem = __fma_rn(-d.b, q0, a);
+            return __fma_rn(rem, d.r, q0);
+        }
+        if (a == 0.0) return __dmul_rn(a, d.r);  // signed zero
+    }
+    return div_slow(a, d.b);
+}
+
 struct V3 {
     double x, y, z;
 };
@@ -25,6 +58,7 @@ __device__ __forceinline__ V3 vsub(V3 a, V3 b) { return {sub(a.x, b.x), sub(a.y,
 __device__ __forceinline__ V3 vadd(V3 a, V3 b) { return {add(a.x, b.x), add(a.y, b.y), add(a.z, b.z)}; }
 __device__ __forceinline__ V3 vmul(V3 a, double s) { return {mul(a.x, s), mul(a.y, s), mul(a.z, s)}; }
 __device__ __forceinline__ V3 vdiv(V3 a, double s) { return {dvd(a.x, s), dvd(a.y, s), dvd(a.z, s)}; }
+__device__ __forceinline__ V3 vdivq(V3 a, const Div& d) { return {dq(a.x, d), dq(a.y, d), dq(a.z, d)}; }
 // dot(a,b) = (ax*bx + ay*by) + az*bz  (geom.hpp:22)
 __device__ __forceinline__ double vdot(V3 a, V3 b) {
     return add(add(mul(a.x, b.x), mul(a.y, b.y)), mul(a.z, b.z));

@@ -162,7 +162,40 @@ __global__ void check_indices(const int32_t* __restrict__ a, int64_t n, int64_t 
     }
 }
 
+// self-test of the shared-reciprocal division dq() against IEEE __ddiv_rn on
+// random operands spanning the magnitudes the element kernels see (and the
+// fallback window edges): counts mismatching quotients bit for bit
+__global__ void division_selftest(int64_t n, uint64_t seed, unsigned long long* mismatches) {
+    unsigned long long bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h1 = splitmix64(seed ^ (2 * (uint64_t)i)), h2 = splitmix64(seed ^ (2 * (uint64_t)i + 1));
+        // random significands, exponents in [-560, 560] (covers the window
+        // edges at 2^+-500) with a bias towards the data range [-40, 10]
+        const int e1 = (h1 >> 60) < 12 ? (int)((h1 >> 52) & 63) - 45 : (int)((h1 >> 52) & 1023) - 512 - 48;
+        const int e2 = (h2 >> 60) < 12 ? (int)((h2 >> 52) & 63) - 45 : (int)((h2 >> 52) & 1023) - 512 - 48;
+        double a = __longlong_as_double((long long)((h1 & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+        double b = __longlong_as_double((long long)((h2 & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull));
+        a = ldexp(a, e1) * ((h1 & 1) ? -1.0 : 1.0);
+        b = ldexp(b, e2) * ((h2 & 2) ? -1.0 : 1.0);
+        if ((h1 & 0xff) == 7) a = 0.0;
+        const double q1 = dq(a, make_div(b));
+        const double q2 = __ddiv_rn(a, b);
+        if (__double_as_longlong(q1) != __double_as_longlong(q2)) ++bad;
+        // the constant divisors too
+        if (__double_as_longlong(dq(a, kDiv3)) != __double_as_longlong(__ddiv_rn(a, 3.0))) ++bad;
+        if (__double_as_longlong(dq(a, kDiv6)) != __double_as_longlong(__ddiv_rn(a, 6.0))) ++bad;
+        if (__double_as_longlong(dq(a, kDiv20)) != __double_as_longlong(__ddiv_rn(a, 20.0))) ++bad;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
 }  // namespace
+
+extern "C" int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream) {
+    division_selftest<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(n, seed, mismatches);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
 
 extern "C" int phfem_gpu_check_indices(const int32_t* a, int64_t n, int64_t nc, unsigned long long* first_bad,
                                        void* stream) {

@@ -154,12 +154,14 @@ __device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Loc
     const V3 d1 = vsub(p[1], p[0]), d2 = vsub(p[2], p[0]), d3 = vsub(p[3], p[0]);
     const double det = vdot(vcross(d1, d2), d3);
     L.degenerate = det == 0.0;
-    L.vol = dvd(fabs(det), 6.0);
-    L.g[1] = vdiv(vcross(d2, d3), det);
-    L.g[2] = vdiv(vcross(d3, d1), det);
-    L.g[3] = vdiv(vcross(d1, d2), det);
+    L.vol = dq(fabs(det), kDiv6);
+    const Div ddet = make_div(det);
+    const V3 c1 = vcross(d2, d3), c2 = vcross(d3, d1), c3 = vcross(d1, d2);
+    L.g[1] = {dq(c1.x, ddet), dq(c1.y, ddet), dq(c1.z, ddet)};
+    L.g[2] = {dq(c2.x, ddet), dq(c2.y, ddet), dq(c2.z, ddet)};
+    L.g[3] = {dq(c3.x, ddet), dq(c3.y, ddet), dq(c3.z, ddet)};
     L.g[0] = vmul(vadd(vadd(L.g[1], L.g[2]), L.g[3]), -1.0);
-    const double m20 = dvd(L.vol, 20.0);
+    const double m20 = dq(L.vol, kDiv20);
     const double mdiag = mul(k.c, mul(m20, 2.0)), moff = mul(k.c, mul(m20, 1.0));
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -176,6 +178,7 @@ struct Lu4 {
     double lu[4][4];
     int perm[4];
     bool singular;
+    Div piv[4];  // shared reciprocals of the pivots lu[i][i]
 };
 
 __device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
@@ -214,9 +217,10 @@ __device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
                 }
             }
         }
+        f.piv[col] = make_div(f.lu[col][col]);
 #pragma unroll
         for (int r = col + 1; r < 4; ++r) {
-            const double m = dvd(f.lu[r][col], f.lu[col][col]);
+            const double m = dq(f.lu[r][col], f.piv[col]);
             f.lu[r][col] = m;
 #pragma unroll
             for (int c = col + 1; c < 4; ++c) f.lu[r][c] = sub(f.lu[r][c], mul(m, f.lu[col][c]));
@@ -242,7 +246,7 @@ __device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double
         double s = y[i];
 #pragma unroll
         for (int j = i + 1; j < 4; ++j) s = sub(s, mul(f.lu[i][j], x[j]));
-        x[i] = dvd(s, f.lu[i][i]);
+        x[i] = dq(s, f.piv[i]);
     }
 }
 

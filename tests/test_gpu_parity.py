@@ -78,6 +78,25 @@ def check_system(g, m, fo, oracle, kind, c=1.0, a_elem=None, a_diag=None):
 # ---------------------------------------------------------------------------
 
 
+def test_division_matches_ieee():
+    """The element kernels divide through a shared reciprocal (common.cuh
+    dq()); it must equal IEEE division bit for bit."""
+    import ctypes
+
+    import torch
+
+    L = ph.lib()
+    fn = L.phfem_gpu_division_selftest
+    fn.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    fn.restype = ctypes.c_int
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for seed in (1, 2, 3):
+        assert fn(50_000_000, seed, bad.data_ptr(), s) == 0
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+
+
 def test_kuhn_generator_bit_exact(oracle):
     for args in [(3, 4, 5, 2.0, 1.0, 0.5, 0.2, 2509, 0x21), (8, 8, 8, 1.0, 1.0, 1.0, 0.2, 2509, 0x3),
                  (16, 2, 2, 8.0, 1.0, 1.0, 0.0, 2509, 0x1)]:
