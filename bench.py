@@ -213,6 +213,9 @@ def main():
     from paper_2509_11133_b200 import phfem as ph
 
     cfg = configs.CONFIGS[args.config]
+    if args.config == 2:
+        run_config2(args, ph, torch, rank)
+        return
     mesh = cfg.build()
     nc, ne, nd, nn = mesh.sizes()
     stream = torch.cuda.ExternalStream(ph.stream_ptr())
@@ -329,6 +332,47 @@ def main():
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def run_config2(args, ph, torch, rank):
+    """Config 2: 1 cube -> 6 Kuhn tets refined level by level up to the first
+    level with >= 2e7 tets (level 7, 214,990,848 tets); per level the
+    connectivity (edges + faces + classification) and the red refinement that
+    produced the next level, device-resident, CUDA-event timed."""
+    hbm, hbm_kind = peaks()
+    m = ph.Mesh.kuhn(1, 1, 1, dirichlet_mask=0x3F)
+    levels = []
+    for lv in range(8):
+        nc, ne, nd, nn = m.sizes()
+        reps = max(1, args.steps if ne < 50_000_000 else 1)
+        for _ in range(min(args.warmup, 3) if ne < 50_000_000 else 1):
+            m.pipeline(0, do_refine=lv < 7, assemble=False)
+        acc = {}
+        for _ in range(reps):
+            st, cts = m.pipeline(0, do_refine=lv < 7, assemble=False)
+            for k, v in st.items():
+                acc[k] = acc.get(k, 0.0) + v / reps
+        ned, nf = int(cts[0]), int(cts[1])
+        conn_ms = acc["star"] + acc["groups"] + acc["number"] + acc["classify"]
+        B = algorithmic_bytes(nc, ne, ned, nf, nd + nn, 0, 0)
+        row = {"level": lv, "tets": ne, "nodes": nc, "edges": ned, "faces": nf, "connect_ms": conn_ms,
+               "connect_tets_per_s": ne / (conn_ms / 1e3), "connect_hbm_frac": B["connect"] / (conn_ms / 1e3) / 1e9 / hbm}
+        if lv < 7:
+            row.update(refine_ms=acc["refine"], refine_child_tets_per_s=12 * ne / (acc["refine"] / 1e3),
+                       refine_hbm_frac=B["refine"] / (acc["refine"] / 1e3) / 1e9 / hbm)
+            m.refine()
+        levels.append(row)
+        print(json.dumps(row), file=sys.stderr, flush=True)
+    top = levels[-1]
+    prev = levels[-2]
+    step_ms = top["connect_ms"] + prev["refine_ms"]
+    if rank == 0:
+        print(json.dumps({"metric": "tets/s refine+connect (config 2, level 7)", "value": top["tets"] / (step_ms / 1e3),
+                          "unit": "tets/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "int32/f64", "data": "synthetic",
+                          "config": {"workload": "cfg2_cube6_refine", "levels": levels, "peak_kind": hbm_kind}}),
+              flush=True)
 
 
 def mesh_nnz_s(mesh, problem):

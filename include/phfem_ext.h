@@ -111,11 +111,14 @@ typedef struct phfem_stage_ms {
 } phfem_stage_ms;
 
 /* One full pass on a device-resident mesh: connectivity (edges + faces),
- * assembly + condensation of `problem` and, when do_refine, one red
- * refinement into a scratch mesh that is discarded.  Caches on the handle
- * are rebuilt (not reused).  counts out (may be NULL):
+ * assembly + condensation of `problem` and one red refinement into a scratch
+ * mesh that is discarded.  flags: PHFEM_PIPE_REFINE (1) includes the
+ * refinement, PHFEM_PIPE_NO_ASSEMBLY (2) skips assembly + condensation.
+ * Caches on the handle are rebuilt (not reused).  counts out (may be NULL):
  * [nEd, nF, L, nnz(S) padded, nE children] */
-int phfem_pipeline(phfem_mesh* mesh, int problem, int do_refine, phfem_stage_ms* ms,
+#define PHFEM_PIPE_REFINE 1
+#define PHFEM_PIPE_NO_ASSEMBLY 2
+int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
                    int64_t counts[5]);
 
 /* Schur solve only (assembly cached), timing the CG on the device.

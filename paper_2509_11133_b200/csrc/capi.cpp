@@ -802,10 +802,12 @@ void* phfem_stream(void) {
     }
 }
 
-int phfem_pipeline(phfem_mesh* mesh, int problem, int do_refine, phfem_stage_ms* ms, int64_t counts[5]) {
+int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms, int64_t counts[5]) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
+        const bool do_refine = flags & PHFEM_PIPE_REFINE;
+        const bool do_assemble = !(flags & PHFEM_PIPE_NO_ASSEMBLY);
         Stages st;
         Timer total;
         total.start();
@@ -816,8 +818,10 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int do_refine, phfem_stage_ms*
         mesh->invalidate();
         build_connectivity(*mesh->data, *c, true, &st);
         mesh->conn = c;
-        assemble_system(*mesh->data, *mesh->coef, *c, problem, *s, false, &st);
-        mesh->sys = s;
+        if (do_assemble) {
+            assemble_system(*mesh->data, *mesh->coef, *c, problem, *s, false, &st);
+            mesh->sys = s;
+        }
         int64_t ne_child = 0;
         if (do_refine) {
             if (!mesh->scratch_child) mesh->scratch_child = std::make_shared<MeshData>();
@@ -838,7 +842,7 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int do_refine, phfem_stage_ms*
             counts[0] = c->ned;
             counts[1] = c->nf;
             counts[2] = c->l;
-            counts[3] = s->nchunks * PHG_SELL_C * PHG_SELL_W;
+            counts[3] = do_assemble ? s->nchunks * PHG_SELL_C * PHG_SELL_W : 0;
             counts[4] = ne_child;
         }
     });

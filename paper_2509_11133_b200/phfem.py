@@ -339,10 +339,11 @@ class Mesh:
         _check(lib().phfem_mesh_solve_faces(self._h, problem, tol, max_iter, _ptr(lam), _ptr(out)))
         return lam, dict(iterations=int(out[0]), rel_residual=out[1], converged=bool(out[2]))
 
-    def pipeline(self, problem, do_refine=True):
+    def pipeline(self, problem, do_refine=True, assemble=True):
         ms = StageMs()
         counts = np.zeros(5, dtype=np.int64)
-        _check(lib().phfem_pipeline(self._h, problem, int(do_refine), C.byref(ms), _ptr(counts)))
+        flags = (1 if do_refine else 0) | (0 if assemble else 2)
+        _check(lib().phfem_pipeline(self._h, problem, flags, C.byref(ms), _ptr(counts)))
         return {n: getattr(ms, n) for n, _ in StageMs._fields_}, counts
 
     def solve_timed(self, problem, tol=1e-10, max_iter=-1):
