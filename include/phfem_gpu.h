@@ -90,18 +90,15 @@ int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_
  * vertex is v among the incident element slots: edge_first[6t+k] = smallest
  * slot of the edge (first occurrence, connectivity.cpp:22-37); slot_mate[4t+k]
  * = the other slot of the face or -1 (faces_up/full_face_table,
- * connectivity.cpp:72-153).  Either output may be NULL to skip that part.
- * Vertices with stars larger than the fast path's limit are appended to
- * big_list (device int32, count in big_count) and handled by
- * phfem_gpu_star_groups_big. */
+ * connectivity.cpp:72-153).  slot_mate may be NULL (edges only).  Three
+ * passes without host round trips: warps over stars <= 32, warps over the
+ * deferred stars <= 64, blocks over anything larger (stars above 2730
+ * incidences set PHG_ERR_VALENCE).  defer_list needs 2 nC entries,
+ * defer_count 2. */
 int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star,
                           const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
-                          int32_t* big_list, int32_t* big_count, unsigned long long* err,
+                          int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
                           void* stream);
-int phfem_gpu_star_groups_big(int32_t n_big, const int32_t* big_list, const int64_t* star_ptr,
-                              const int32_t* star, const int32_t* tets, int32_t* edge_first,
-                              int32_t* slot_mate, int max_star, unsigned long long* err,
-                              void* stream);
 
 /* Per element counts of first-occurrence edges (low 8 bits) and owned faces
  * (next 8 bits): packed[t]. */

@@ -49,10 +49,6 @@ __global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, unsigned
 
 // ------------------------------------------------------------ star groups
 
-constexpr int kWarpStarMax = 64;  // fast path: stars up to this size
-constexpr int kWarpCap = 256;     // hash capacity per warp (>= 3 * kWarpStarMax + 1)
-constexpr int kWarpsPerBlock = 4;
-
 struct FaceTab {
     unsigned long long* key;
     int32_t* lo;
@@ -204,10 +200,9 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
     }
 }
 
-// -------------------------------------------- fast path: stars of <= 32
+// ------------------------------------------- warp paths: stars of <= 64
 
-constexpr int kFastCap = 128;  // > 3 * 32 candidates
-constexpr int kFastWarps = 8;
+constexpr int kFastWarps = 4;
 
 // For local vertex lv: its i-th neighbour w (i < 3, ascending) and the
 // i-th face k containing lv with the local vertices x, y following lv in the
@@ -223,14 +218,22 @@ __device__ __forceinline__ void face_of(int lv, int i, int& k, int& xi, int& yi)
     yi = (int)(e & 0xf);
 }
 
+// E entries per lane: E = 1 handles stars of <= 32 incidences (all Kuhn
+// vertices), E = 2 those of <= 64 (refined meshes reach 36).  Vertices come
+// from `list` (or 0..n-1) with n = *count (or nv); larger stars are appended
+// to defer_list for the next pass.  No host round trip between passes.
+template <int E>
 __global__ void __launch_bounds__(32 * kFastWarps)
-    star_groups_fast(int64_t nc, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+    star_groups_warp(int64_t nv, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                     const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
                      const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
-                     int32_t* __restrict__ slot_mate, int32_t* __restrict__ big_list, int32_t* __restrict__ big_count,
-                     unsigned long long* err) {
-    __shared__ int32_t s_ekey[kFastWarps][kFastCap], s_eval[kFastWarps][kFastCap];
-    __shared__ unsigned long long s_fkey[kFastWarps][kFastCap];
-    __shared__ int32_t s_flo[kFastWarps][kFastCap], s_fhi[kFastWarps][kFastCap], s_fcnt[kFastWarps][kFastCap];
+                     int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
+                     int32_t* __restrict__ defer_count, unsigned long long* err) {
+    constexpr int CAP = E == 1 ? 128 : 256;  // > 3 * 32 E candidates
+    constexpr unsigned mask = CAP - 1;
+    __shared__ int32_t s_ekey[kFastWarps][CAP], s_eval[kFastWarps][CAP];
+    __shared__ unsigned long long s_fkey[kFastWarps][CAP];
+    __shared__ int32_t s_flo[kFastWarps][CAP], s_fhi[kFastWarps][CAP], s_fcnt[kFastWarps][CAP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t* ekey = s_ekey[warp];
     int32_t* eval = s_eval[warp];
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
     int32_t* flo = s_flo[warp];
     int32_t* fhi = s_fhi[warp];
     int32_t* fcnt = s_fcnt[warp];
-    for (int i = lane; i < kFastCap; i += 32) {
+    for (int i = lane; i < CAP; i += 32) {
         ekey[i] = -1;
         eval[i] = INT_MAX;
         fkey[i] = ~0ull;
@@ -247,44 +250,43 @@ __global__ void __launch_bounds__(32 * kFastWarps)
         fcnt[i] = 0;
     }
     __syncwarp();
-    constexpr unsigned mask = kFastCap - 1;
     const bool do_faces = slot_mate != nullptr;
+    const int64_t n = count ? (int64_t)*count : nv;
     const int64_t nwarps = (int64_t)gridDim.x * kFastWarps;
-    for (int64_t vv = (int64_t)blockIdx.x * kFastWarps + warp; vv < nc; vv += nwarps) {
-        const int32_t v = (int32_t)vv;
-        const int64_t beg = star_ptr[vv];
-        const int m = (int)(star_ptr[vv + 1] - beg);
-        if (m > 32) {
-            if (lane == 0) big_list[atomicAdd(big_count, 1)] = v;
+    for (int64_t it = (int64_t)blockIdx.x * kFastWarps + warp; it < n; it += nwarps) {
+        const int32_t v = list ? list[it] : (int32_t)it;
+        const int64_t beg = star_ptr[v];
+        const int m = (int)(star_ptr[v + 1] - beg);
+        if (m > 32 * E) {
+            if (lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
             continue;
         }
-        const bool act = lane < m;
-        int64_t t = 0;
-        int lv = 0;
-        int4 tet = make_int4(0, 0, 0, 0);
-        if (act) {
-            const int32_t inc = __ldg(star + beg + lane);
-            t = inc >> 2;
-            lv = inc & 3;
-            tet = ldtet(tets, t);
-        }
-        int eh[3] = {-1, -1, -1}, fh[3] = {-1, -1, -1};
-        int32_t eslot[3], fslot[3];
-        if (act) {
+        int eh[E][3], fh[E][3];
+        int32_t eslot[E][3], fslot[E][3];
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) eh[u][i] = fh[u][i] = -1;
+            const int e = lane + 32 * u;
+            if (e >= m) continue;
+            const int32_t inc = __ldg(star + beg + e);
+            const int64_t t = inc >> 2;
+            const int lv = inc & 3;
+            const int4 tet = ldtet(tets, t);
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int w = nbr_of(lv, i);
                 const int32_t b = tv(tet, w);
                 if (b <= v) continue;
-                eslot[i] = (int32_t)(6 * t + edge_index(lv, w));
+                eslot[u][i] = (int32_t)(6 * t + edge_index(lv, w));
                 unsigned h = hash32((uint32_t)b) & mask;
                 for (;;) {
                     const int32_t old = atomicCAS(ekey + h, -1, b);
                     if (old == -1 || old == b) break;
                     h = (h + 1) & mask;
                 }
-                eh[i] = (int)h;
-                atomicMin(eval + h, eslot[i]);
+                eh[u][i] = (int)h;
+                atomicMin(eval + h, eslot[u][i]);
             }
             if (do_faces) {
 #pragma unroll
@@ -301,45 +303,51 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                         if (old == ~0ull || old == key) break;
                         h = (h + 1) & mask;
                     }
-                    fh[i] = (int)h;
-                    fslot[i] = (int32_t)(4 * t + k);
-                    atomicMin(flo + h, fslot[i]);
-                    atomicMax(fhi + h, fslot[i]);
-                    atomicAdd(fcnt + h, 4 | (x < y ? 1 : 2) << 0);
+                    fh[u][i] = (int)h;
+                    fslot[u][i] = (int32_t)(4 * t + k);
+                    atomicMin(flo + h, fslot[u][i]);
+                    atomicMax(fhi + h, fslot[u][i]);
+                    // count in bits 2+, orientation (x < y: 1, else 2) below:
+                    // exactly one slot of each orientation sums to 11
+                    atomicAdd(fcnt + h, x < y ? 5 : 6);
                 }
             }
         }
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (eh[i] >= 0) edge_first[eslot[i]] = eval[eh[i]];
-            if (fh[i] >= 0) {
-                const int h = fh[i];
-                const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
-                // count in bits 2+, orientation bits accumulate below: one
-                // slot of each orientation gives exactly 4+1 + 4+2 = 11
-                const int count = c >> 2;
-                if (count > 2 || (count == 2 && c != 11)) {
-                    const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
-                    report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
+        for (int u = 0; u < E; ++u)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (eh[u][i] >= 0) edge_first[eslot[u][i]] = eval[eh[u][i]];
+                if (fh[u][i] >= 0) {
+                    const int h = fh[u][i];
+                    const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
+                    const int cnt = c >> 2;
+                    if (cnt > 2 || (cnt == 2 && c != 11)) {
+                        // same orientation twice: "elements A and B claim
+                        // the same oriented face" (connectivity.cpp:62-68)
+                        const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
+                        report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
+                    }
+                    slot_mate[fslot[u][i]] = cnt >= 2 ? (fslot[u][i] == lo ? hi : lo) : -1;
                 }
-                slot_mate[fslot[i]] = count >= 2 ? (fslot[i] == lo ? hi : lo) : -1;
             }
-        }
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            if (eh[i] >= 0) {
-                ekey[eh[i]] = -1;
-                eval[eh[i]] = INT_MAX;
+        for (int u = 0; u < E; ++u)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                if (eh[u][i] >= 0) {
+                    ekey[eh[u][i]] = -1;
+                    eval[eh[u][i]] = INT_MAX;
+                }
+                if (fh[u][i] >= 0) {
+                    fkey[fh[u][i]] = ~0ull;
+                    flo[fh[u][i]] = INT_MAX;
+                    fhi[fh[u][i]] = -1;
+                    fcnt[fh[u][i]] = 0;
+                }
             }
-            if (fh[i] >= 0) {
-                fkey[fh[i]] = ~0ull;
-                flo[fh[i]] = INT_MAX;
-                fhi[fh[i]] = -1;
-                fcnt[fh[i]] = 0;
-            }
-        }
         __syncwarp();
     }
 }
@@ -351,56 +359,34 @@ struct BlockSync {
     __device__ void operator()() const { __syncthreads(); }
 };
 
-__global__ void __launch_bounds__(32 * kWarpsPerBlock)
-    star_groups(int64_t nc, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
-                const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first, int32_t* __restrict__ slot_mate,
-                int32_t* __restrict__ big_list, int32_t* __restrict__ big_count, unsigned long long* err) {
-    // per warp: union of the edge table (2 KB) and the face table (5 KB)
-    __shared__ __align__(16) unsigned char smem[kWarpsPerBlock][kWarpCap * 20];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* base = smem[warp];
-    int32_t* ekey = reinterpret_cast<int32_t*>(base);
-    int32_t* eval = ekey + kWarpCap;
-    FaceTab ft;
-    ft.key = reinterpret_cast<unsigned long long*>(base);
-    ft.lo = reinterpret_cast<int32_t*>(base + kWarpCap * 8);
-    ft.hi = ft.lo + kWarpCap;
-    ft.cnt = ft.hi + kWarpCap;
-    const int64_t nwarps = (int64_t)gridDim.x * kWarpsPerBlock;
-    for (int64_t v = (int64_t)blockIdx.x * kWarpsPerBlock + warp; v < nc; v += nwarps) {
+// stars of more than 64 incidences: one block per vertex, tables in dynamic
+// shared memory of capacity `cap` (> 3 m), vertices from list[0..*count)
+__global__ void __launch_bounds__(256)
+    star_groups_big(const int32_t* __restrict__ big_list, const int32_t* __restrict__ big_count,
+                    const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                    const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
+                    int32_t* __restrict__ slot_mate, unsigned cap, unsigned long long* err) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const int32_t n = *big_count;
+    for (int32_t it = blockIdx.x; it < n; it += gridDim.x) {
+        const int32_t v = big_list[it];
         const int64_t beg = star_ptr[v];
         const int m = (int)(star_ptr[v + 1] - beg);
-        if (m > kWarpStarMax) {
-            if (lane == 0) big_list[atomicAdd(big_count, 1)] = (int32_t)v;
+        if ((unsigned)(3 * m) >= cap) {
+            if (threadIdx.x == 0) report(err, PHG_ERR_VALENCE, (unsigned long long)v);
             continue;
         }
-        group_vertex<32>((int32_t)v, beg, m, lane, star, tets, edge_first, slot_mate, ekey, eval, ft,
-                         kWarpCap - 1, kWarpCap, err, WarpSync{});
+        int32_t* ekey = reinterpret_cast<int32_t*>(dsm);
+        int32_t* eval = ekey + cap;
+        FaceTab ft;
+        ft.key = reinterpret_cast<unsigned long long*>(dsm);
+        ft.lo = reinterpret_cast<int32_t*>(dsm + (size_t)cap * 8);
+        ft.hi = ft.lo + cap;
+        ft.cnt = ft.hi + cap;
+        group_vertex<256>(v, beg, m, threadIdx.x, star, tets, edge_first, slot_mate, ekey, eval, ft, cap - 1, cap,
+                          err, BlockSync{});
+        __syncthreads();
     }
-}
-
-__global__ void __launch_bounds__(256)
-    star_groups_big(const int32_t* __restrict__ big_list, const int64_t* __restrict__ star_ptr,
-                    const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
-                    int32_t* __restrict__ edge_first, int32_t* __restrict__ slot_mate, unsigned cap,
-                    unsigned long long* err) {
-    extern __shared__ __align__(16) unsigned char dsm[];
-    const int32_t v = big_list[blockIdx.x];
-    const int64_t beg = star_ptr[v];
-    const int m = (int)(star_ptr[v + 1] - beg);
-    if ((unsigned)(3 * m) >= cap) {
-        if (threadIdx.x == 0) report(err, PHG_ERR_VALENCE, (unsigned long long)v);
-        return;
-    }
-    int32_t* ekey = reinterpret_cast<int32_t*>(dsm);
-    int32_t* eval = ekey + cap;
-    FaceTab ft;
-    ft.key = reinterpret_cast<unsigned long long*>(dsm);
-    ft.lo = reinterpret_cast<int32_t*>(dsm + (size_t)cap * 8);
-    ft.hi = ft.lo + cap;
-    ft.cnt = ft.hi + cap;
-    group_vertex<256>(v, beg, m, threadIdx.x, star, tets, edge_first, slot_mate, ekey, eval, ft, cap - 1, cap, err,
-                      BlockSync{});
 }
 
 // -------------------------------------------------------------- numbering
@@ -614,32 +600,26 @@ extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cur
 }
 
 extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
-                                     int32_t* edge_first, int32_t* slot_mate, int32_t* big_list, int32_t* big_count,
-                                     unsigned long long* err, void* stream) {
-    // stars of <= 32 incidences: register-resident warp path; larger stars
-    // are deferred to star_groups_big (block per vertex)
+                                     int32_t* edge_first, int32_t* slot_mate, int32_t* defer_list,
+                                     int32_t* defer_count, unsigned long long* err, void* stream) {
+    // pass 1: all vertices, stars <= 32 (warp, one incidence per lane)
+    // pass 2: deferred stars <= 64 (warp, two per lane)
+    // pass 3: anything larger (block per vertex); counts stay on the device
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(defer_count, 0, 2 * sizeof(int32_t), s);
     const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
     const int grid = (int)(blocks < kSMs * 8 ? blocks : kSMs * 8);
-    star_groups_fast<<<grid, 32 * kFastWarps, 0, (cudaStream_t)stream>>>(nc, star_ptr, star, tets, edge_first,
-                                                                         slot_mate, big_list, big_count, err);
-    phg::count_launches(1);
-    return (int)cudaGetLastError();
-}
-
-extern "C" int phfem_gpu_star_groups_big(int32_t n_big, const int32_t* big_list, const int64_t* star_ptr,
-                                         const int32_t* star, const int32_t* tets, int32_t* edge_first,
-                                         int32_t* slot_mate, int max_star, unsigned long long* err, void* stream) {
-    if (n_big <= 0) return 0;
-    unsigned cap = 512;
-    while (cap < 3u * (unsigned)max_star + 1u) cap <<= 1;
-    const size_t smem = (size_t)cap * 20;
-    if (smem > 200 * 1024) {
-        cap = 8192;
-    }
+    star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
+                                                         slot_mate, defer_list, defer_count, err);
+    star_groups_warp<2><<<kSMs * 4, 32 * kFastWarps, 0, s>>>(0, defer_list, defer_count, star_ptr, star, tets,
+                                                             edge_first, slot_mate, defer_list + nc,
+                                                             defer_count + 1, err);
+    constexpr unsigned cap = 8192;  // stars up to 2730 incidences
     const size_t bytes = (size_t)cap * 20;
     cudaFuncSetAttribute(star_groups_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    star_groups_big<<<n_big, 256, bytes, (cudaStream_t)stream>>>(big_list, star_ptr, star, tets, edge_first,
-                                                                 slot_mate, cap, err); phg::count_launches(1);
+    star_groups_big<<<kSMs, 256, bytes, s>>>(defer_list + nc, defer_count + 1, star_ptr, star, tets, edge_first,
+                                             slot_mate, cap, err);
+    phg::count_launches(3);
     return (int)cudaGetLastError();
 }
 

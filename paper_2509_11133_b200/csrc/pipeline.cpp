@@ -102,28 +102,15 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     tm.start();
     c.edge_first.alloc(6 * ne);
     if (faces) c.slot_mate.alloc(4 * ne);
-    w.big_list.alloc(nc > 0 ? nc : 1);
-    w.big_count.alloc(1);
-    w.big_count.zero();
+    w.big_list.alloc(2 * (nc > 0 ? nc : 1));
+    w.big_count.alloc(2);
     check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
                                 w.big_list.p, w.big_count.p, w.err.p, SV()),
           "star groups");
-    // 3. numbering: per-element counts and scans are independent of the big
-    //    stars' outcome only after they finish, so those run first
+    if (st) st->groups += tm.stop_ms();
+    // 3. numbering: per-element counts, scans, ids, remaining slots
     w.ecount.alloc(ne);
     if (faces) w.fcount.alloc(ne);
-    const int32_t n_big = read_scalar(w.big_count.p);
-    if (n_big > 0) {
-        std::vector<int32_t> big((size_t)n_big);
-        check(cudaMemcpyAsync(big.data(), w.big_list.p, sizeof(int32_t) * n_big, cudaMemcpyDeviceToHost, S()), "D2H");
-        const std::vector<int64_t> ptr = c.star_ptr.download();
-        int max_star = 0;
-        for (int32_t v : big) max_star = std::max<int>(max_star, (int)(ptr[v + 1] - ptr[v]));
-        check(phfem_gpu_star_groups_big(n_big, w.big_list.p, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
-                                        faces ? c.slot_mate.p : nullptr, max_star, w.err.p, SV()),
-              "star groups (big)");
-    }
-    if (st) st->groups += tm.stop_ms();
     tm.start();
     c.edge_off.alloc(ne + 1);
     if (faces) w.face_off.alloc(ne + 1);

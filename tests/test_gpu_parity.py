@@ -107,6 +107,45 @@ def test_kuhn_generator_bit_exact(oracle):
         assert np.array_equal(d, o.db) and np.array_equal(n, o.nb)
 
 
+def bipyramid(n: int) -> MeshArrays:
+    """2n tetrahedra around the vertical axis: centre c, apexes top/bottom and
+    a ring of n vertices; c has a star of 2n incidences (n > 32 exercises the
+    block-per-vertex grouping path).  Orientation fixed to det > 0; boundary
+    faces = unshared element faces in their element's orientation, all
+    Dirichlet."""
+    ang = 2 * np.pi * np.arange(n) / n
+    ring = np.stack([np.cos(ang), np.sin(ang), np.zeros(n)], axis=1)
+    coords = np.vstack([[0.0, 0.0, 0.0], [0.0, 0.0, 1.0], [0.0, 0.0, -1.0], ring])
+    tets = []
+    for i in range(n):
+        a, b = 3 + i, 3 + (i + 1) % n
+        tets += [[0, a, b, 1], [0, b, a, 2]]
+    tets = np.array(tets, dtype=np.int32)
+    p = coords[tets]
+    det = np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0])
+    tets[det < 0] = tets[det < 0][:, [0, 1, 3, 2]]
+    fv = [[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]
+    faces = [tuple(t[f]) for t in tets for f in fv]
+    keys = [tuple(sorted(f)) for f in faces]
+    from collections import Counter
+    cnt = Counter(keys)
+    db = np.array([f for f, k in zip(faces, keys) if cnt[k] == 1], dtype=np.int32)
+    return MeshArrays(coords, tets, db, np.zeros((0, 3), np.int32))
+
+
+@pytest.mark.parametrize("n", [20, 40, 200])
+def test_high_valence_stars(oracle, n):
+    m = bipyramid(n)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, kind=0)
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(mo, k)), k
+
+
 @pytest.mark.parametrize("level", [0, 1, 2, 3])
 def test_cube_family_bit_exact(oracle, level):
     m = cube5()
