@@ -105,18 +105,16 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
 int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
                              int32_t* edge_count, int32_t* face_count, void* stream);
 
-/* Numbering of first-occurrence edges and owned faces from the exclusive
- * offsets (edge ids = rank of the first slot; face ids = rank of the owner
- * slot, the faces_up order).  Writes the owner-side entries; the others are
- * filled by phfem_gpu_fill_slots.  Any output group may be NULL. */
+/* Numbering from the exclusive offsets: edge ids = rank of the first slot,
+ * face ids = rank of the owner slot (the faces_up order).  One thread per
+ * element writes the ids of all its slots (the others rank in their group's
+ * first element), the edge/face tables, sigma and the face areas.  Either
+ * output group may be NULL (edge_first / slot_mate NULL). */
 int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords,
                      const int32_t* edge_first, const int64_t* edge_off, int32_t* edge_of_slot,
                      int32_t* edge_nodes, const int32_t* slot_mate, const int64_t* face_off,
                      int32_t* face_of_slot, int8_t* sigma, int32_t* faces, int32_t* face_slots,
                      double* face_area, unsigned long long* err, void* stream);
-int phfem_gpu_fill_slots(int64_t ne, const int32_t* edge_first, int32_t* edge_of_slot,
-                         const int32_t* slot_mate, int32_t* face_of_slot, int8_t* sigma,
-                         void* stream);
 
 /* Boundary classification (connectivity.cpp:156-175): entries of db then nb
  * are matched through the star of their smallest vertex. */

@@ -411,37 +411,63 @@ __global__ void element_counts(int64_t ne, const int32_t* __restrict__ edge_firs
     }
 }
 
-__global__ void number(int64_t ne, const int32_t* __restrict__ tets, const double* __restrict__ coords,
-                       const int32_t* __restrict__ edge_first, const int64_t* __restrict__ edge_off,
-                       int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
-                       const int32_t* __restrict__ slot_mate, const int64_t* __restrict__ face_off,
-                       int32_t* __restrict__ face_of_slot, int8_t* __restrict__ sigma, int32_t* __restrict__ faces,
-                       int32_t* __restrict__ face_slots, double* __restrict__ face_area,
-                       unsigned long long* err) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
-        const int4 tet = ldtet(tets, t);
-        if (edge_first) {
-            int64_t id = edge_off[t];
-            for (int k = 0; k < 6; ++k) {
-                const int64_t s = 6 * t + k;
-                if (edge_first[s] != (int32_t)s) continue;
-                edge_of_slot[s] = (int32_t)id;
+// Ids of all slots of one element (one thread per element, blocks in element
+// order).  Own first-occurrence edge slots and owned face slots get
+// E_t + rank / F_t + rank; the others find their group's first element g < t
+// through edge_first / slot_mate and rank there, so every id is written once,
+// in full 16-24 byte rows (no second pass over the slots).
+__global__ void __launch_bounds__(256)
+    number(int64_t ne, const int32_t* __restrict__ tets, const double* __restrict__ coords,
+           const int32_t* __restrict__ edge_first, const int64_t* __restrict__ edge_off,
+           int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
+           const int32_t* __restrict__ slot_mate, const int64_t* __restrict__ face_off,
+           int32_t* __restrict__ face_of_slot, int8_t* __restrict__ sigma, int32_t* __restrict__ faces,
+           int32_t* __restrict__ face_slots, double* __restrict__ face_area, unsigned long long* err) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= ne) return;
+    const int4 tet = ldtet(tets, t);
+    if (edge_first) {
+        const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
+        const int2 a01 = __ldg(ef2), a23 = __ldg(ef2 + 1), a45 = __ldg(ef2 + 2);
+        const int32_t ef[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
+        int64_t id = edge_off[t];
+        int32_t ids[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int64_t s = 6 * t + k;
+            const int32_t f = ef[k];
+            if (f == (int32_t)s) {
+                ids[k] = (int32_t)id;
                 int32_t a = tv(tet, k < 3 ? 0 : (k < 5 ? 1 : 2));
                 int32_t b = tv(tet, k < 3 ? k + 1 : (k < 5 ? k - 1 : 3));
                 if (a > b) { const int32_t tmp = a; a = b; b = tmp; }
                 reinterpret_cast<int2*>(edge_nodes)[id] = make_int2(a, b);
                 ++id;
+            } else {
+                // rank of slot f among the first-occurrence slots of its element
+                const int64_t g = f / 6;
+                int r = 0;
+                for (int j = 0; j < f - 6 * g; ++j) r += __ldg(edge_first + 6 * g + j) == (int32_t)(6 * g + j);
+                ids[k] = (int32_t)(__ldg(edge_off + g) + r);
             }
         }
-        if (slot_mate) {
-            int64_t id = face_off[t];
-            const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-            for (int k = 0; k < 4; ++k) {
-                const int32_t s = (int32_t)(4 * t + k);
-                const int32_t mate = tv(m, k);
-                if (!face_owner(s, mate)) continue;
-                face_of_slot[s] = (int32_t)id;
-                sigma[s] = 1;
+        int2* eo = reinterpret_cast<int2*>(edge_of_slot) + 3 * t;
+        eo[0] = make_int2(ids[0], ids[1]);
+        eo[1] = make_int2(ids[2], ids[3]);
+        eo[2] = make_int2(ids[4], ids[5]);
+    }
+    if (slot_mate) {
+        int64_t id = face_off[t];
+        const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        int32_t fid[4];
+        int sg[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t s = (int32_t)(4 * t + k);
+            const int32_t mate = tv(m, k);
+            if (face_owner(s, mate)) {
+                fid[k] = (int32_t)id;
+                sg[k] = 1;
                 const int32_t f0 = tv(tet, face_vert(k, 0)), f1 = tv(tet, face_vert(k, 1)), f2 = tv(tet, face_vert(k, 2));
                 faces[3 * id] = f0;
                 faces[3 * id + 1] = f1;
@@ -454,29 +480,23 @@ __global__ void number(int64_t ne, const int32_t* __restrict__ tets, const doubl
                 if (len == 0.0) report(err, PHG_ERR_FACE, (unsigned long long)id << 2 | 0);
                 face_area[id] = mul(0.5, len);
                 ++id;
+            } else {
+                // the owner is slot `mate` of an earlier element g: its rank
+                // among g's owned slots (sigma = -1: opposite orientation,
+                // checked in star_groups)
+                const int64_t g = mate >> 2;
+                const int4 mg = __ldg(reinterpret_cast<const int4*>(slot_mate) + g);
+                int r = 0;
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    if (j < (mate & 3)) r += face_owner((int32_t)(4 * g + j), tv(mg, j));
+                fid[k] = (int32_t)(__ldg(face_off + g) + r);
+                sg[k] = -1;
             }
         }
-    }
-}
-
-__global__ void fill_slots(int64_t ne, const int32_t* __restrict__ edge_first, int32_t* __restrict__ edge_of_slot,
-                           const int32_t* __restrict__ slot_mate, int32_t* __restrict__ face_of_slot,
-                           int8_t* __restrict__ sigma) {
-    const int64_t n6 = edge_first ? 6 * ne : 0;
-    const int64_t n4 = slot_mate ? 4 * ne : 0;
-    const int64_t n = n6 > n4 ? n6 : n4;
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-        if (s < n6) {
-            const int32_t f = edge_first[s];
-            if (f != (int32_t)s) edge_of_slot[s] = edge_of_slot[f];
-        }
-        if (s < n4) {
-            const int32_t mate = slot_mate[s];
-            if (mate >= 0 && mate < (int32_t)s) {
-                face_of_slot[s] = face_of_slot[mate];
-                sigma[s] = -1;
-            }
-        }
+        reinterpret_cast<int4*>(face_of_slot)[t] = make_int4(fid[0], fid[1], fid[2], fid[3]);
+        reinterpret_cast<char4*>(sigma)[t] = make_char4((signed char)sg[0], (signed char)sg[1], (signed char)sg[2],
+                                                        (signed char)sg[3]);
     }
 }
 
@@ -635,17 +655,11 @@ extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* c
                                 const int32_t* slot_mate, const int64_t* face_off, int32_t* face_of_slot,
                                 int8_t* sigma, int32_t* faces, int32_t* face_slots, double* face_area,
                                 unsigned long long* err, void* stream) {
-    number<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, tets, coords, edge_first, edge_off, edge_of_slot,
-                                                                edge_nodes, slot_mate, face_off, face_of_slot, sigma,
-                                                                faces, face_slots, face_area, err); phg::count_launches(1);
-    return (int)cudaGetLastError();
-}
-
-extern "C" int phfem_gpu_fill_slots(int64_t ne, const int32_t* edge_first, int32_t* edge_of_slot,
-                                    const int32_t* slot_mate, int32_t* face_of_slot, int8_t* sigma, void* stream) {
-    const int64_t n = (edge_first ? 6 : 4) * ne;
-    fill_slots<<<grid_cap(n, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, edge_of_slot, slot_mate,
-                                                                   face_of_slot, sigma); phg::count_launches(1);
+    if (ne == 0) return 0;
+    number<<<(unsigned)((ne + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        ne, tets, coords, edge_first, edge_off, edge_of_slot, edge_nodes, slot_mate, face_off, face_of_slot, sigma,
+        faces, face_slots, face_area, err);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

@@ -141,9 +141,6 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
                            faces ? c.faces.p : nullptr, faces ? c.face_slots.p : nullptr,
                            faces ? c.face_area.p : nullptr, w.err.p, SV()),
           "number");
-    check(phfem_gpu_fill_slots(ne, c.edge_first.p, c.edge_of_slot.p, faces ? c.slot_mate.p : nullptr,
-                               faces ? c.face_of_slot.p : nullptr, faces ? c.sigma.p : nullptr, SV()),
-          "fill slots");
     if (st) st->number += tm.stop_ms();
     c.has_edges = true;
     c.has_faces = false;
