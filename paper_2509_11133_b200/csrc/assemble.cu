@@ -114,6 +114,47 @@ __global__ void __launch_bounds__(kLoadThreads)
             }
         } else {
             const double cpre = prob_f_pre<KIND>(k);
+            // trig factors by angle addition from vertex 0 when the element
+            // is small enough (problems.cuh: axis_sincos), else sinpi/cospi
+            const AxisTrig ax = axis_trig(p[0].x, p[1].x, p[2].x, p[3].x);
+            const AxisTrig ay = axis_trig(p[0].y, p[1].y, p[2].y, p[3].y);
+            const AxisTrig az = axis_trig(p[0].z, p[1].z, p[2].z, p[3].z);
+            const double zmax = fmax(axis_zmax(ax), fmax(axis_zmax(ay), axis_zmax(az)));
+            if (zmax <= 0.25) {
+                const double e0 = KIND == 4 ? exp(p[0].x) : 0.0;
+#pragma unroll 2
+                for (int qp = 0; qp < 64; ++qp) {
+                    const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                                 l3 = c_lam5[4 * qp + 3];
+                    double f;
+                    if constexpr (KIND == 3) {
+                        double sx, cx, sy, cy, sz, cz;
+                        axis_sincos(ax, l1, l2, l3, sx, cx);
+                        axis_sincos(ay, l1, l2, l3, sy, cy);
+                        axis_sincos(az, l1, l2, l3, sz, cz);
+                        f = cpre * (sx * sy * sz);
+                    } else if constexpr (KIND == 4) {
+                        const double dx = fma(l3, ax.d3, fma(l2, ax.d2, l1 * ax.d1));
+                        const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
+                        double sy, cy;
+                        axis_sincos(ay, l1, l2, l3, sy, cy);
+                        const double ec = (e0 * exp_small(dx)) * cy;
+                        f = fma(cpre, ec * (z * z), -(k.a2 * 2.0) * ec);
+                    } else {
+                        const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
+                        double sy, cy, sz, cz;
+                        axis_sincos(ay, l1, l2, l3, sy, cy);
+                        axis_sincos(az, l1, l2, l3, sz, cz);
+                        const double s = sy * sz;
+                        f = fma(cpre, x * (8.0 - x) * s, 2.0 * k.a0 * s);
+                    }
+                    const double fw = (vol * c_w5[qp]) * f;
+                    b[0] = fma(fw, l0, b[0]);
+                    b[1] = fma(fw, l1, b[1]);
+                    b[2] = fma(fw, l2, b[2]);
+                    b[3] = fma(fw, l3, b[3]);
+                }
+            } else {
 #pragma unroll 2
             for (int qp = 0; qp < 64; ++qp) {
                 const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
@@ -127,6 +168,7 @@ __global__ void __launch_bounds__(kLoadThreads)
                 b[2] = fma(fw, l2, b[2]);
                 b[3] = fma(fw, l3, b[3]);
             }
+            }
         }
         // b only; condense_k adds the Neumann terms (rhs = b + LN)
         reinterpret_cast<double2*>(rhs_out)[2 * t] = make_double2(b[0], b[1]);
@@ -135,7 +177,7 @@ __global__ void __launch_bounds__(kLoadThreads)
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kCondThreads)
+__global__ void __launch_bounds__(kCondThreads, 4)
     condense_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
@@ -149,11 +191,37 @@ __global__ void __launch_bounds__(kCondThreads)
         const int4 e = ldtet(tets, t);
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
         const Coef k = load_coef(prob, t);
+        Slots sl;
+        load_slots(t, face_of_slot, slot_mate, face_mrow, sl);
+        // boundary data first, while only the coordinates are live:
+        // Neumann terms (assembly.cpp:81-94; this element's Neumann faces in
+        // face order == local slot order) and Dirichlet traces b_D = |F|
+        // u_D(centroid) (assembly.cpp:96-104; stored tuple = owner slot)
+        double ln[4] = {0.0, 0.0, 0.0, 0.0};
+        double bdv[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!sl.bnd[q]) continue;
+            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+            const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
+            const V3 cen = vdivq(vadd(vadd(q0, q1), q2), kDiv3);
+            if (sl.row[q] >= 0) {
+                bdv[q] = mul(__ldg(face_area + sl.face[q]), prob_u<KIND>(cen.x, cen.y, cen.z));
+                continue;
+            }
+            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+            const double len = __dsqrt_rn(vdot(n, n));
+            const double ar = mul(0.5, len);
+            const V3 un = vdivq(n, make_div(len));
+            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+            const double contrib = dq(mul(ar, gc), kDiv3);
+            ln[i0] = add(ln[i0], contrib);
+            ln[i1] = add(ln[i1], contrib);
+            ln[i2] = add(ln[i2], contrib);
+        }
         Local L;
         local_matrices(p, k, L);  // local_stiffness_mass (assembly.cpp:7-33)
         if (L.degenerate) continue;  // reported by load_k
-        Slots sl;
-        load_slots(t, face_of_slot, slot_mate, face_mrow, sl);
         double coef[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
@@ -173,25 +241,6 @@ __global__ void __launch_bounds__(kCondThreads)
         if (slot_mrow) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = sl.row[q];
-        }
-        // Neumann terms (assembly.cpp:81-94; this element's Neumann faces in
-        // face order == local slot order), then rhs = b + LN (assembly.cpp:135)
-        double ln[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!sl.bnd[q] || sl.row[q] >= 0) continue;
-            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
-            const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
-            const V3 cen = vdivq(vadd(vadd(q0, q1), q2), kDiv3);
-            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
-            const double len = __dsqrt_rn(vdot(n, n));
-            const double ar = mul(0.5, len);
-            const V3 un = vdivq(n, make_div(len));
-            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-            const double contrib = dq(mul(ar, gc), kDiv3);
-            ln[i0] = add(ln[i0], contrib);
-            ln[i1] = add(ln[i1], contrib);
-            ln[i2] = add(ln[i2], contrib);
         }
         const double2 r01 = reinterpret_cast<const double2*>(rhs_in)[2 * t];
         const double2 r23 = reinterpret_cast<const double2*>(rhs_in)[2 * t + 1];
@@ -265,15 +314,10 @@ __global__ void __launch_bounds__(kCondThreads)
                     sell_col[sell_idx(R, pos)] = (int32_t)R;
                     sell_val[sell_idx(R, pos)] = 0.0;
                 }
-                // b_D = |F| u_D(centroid) (assembly.cpp:96-104); the face's
-                // stored tuple is this slot's (owner) orientation
-                const int i0 = face_vert(r, 0), i1 = face_vert(r, 1), i2 = face_vert(r, 2);
-                const V3 cen = vdivq(vadd(vadd(p[i0], p[i1]), p[i2]), kDiv3);
-                const double bdv = mul(__ldg(face_area + sl.face[r]), prob_u<KIND>(cen.x, cen.y, cen.z));
                 // rhs_neg = b_D - r_T (solver.cpp:131-138), single contributor
-                rhs_neg[R] = sub(bdv, rb);
-                bd[R] = bdv;
-                acc_bd = add(acc_bd, mul(bdv, bdv));
+                rhs_neg[R] = sub(bdv[r], rb);
+                bd[R] = bdv[r];
+                acc_bd = add(acc_bd, mul(bdv[r], bdv[r]));
             } else {
                 atomicAdd(rhs_neg + R, -rb);
             }

@@ -108,6 +108,65 @@ __device__ __forceinline__ double prob_f_fast(double x, double y, double z, doub
         return prob_f<KIND>(x, y, z, k);
     }
 }
+// sin(pi x), cos(pi x) at the quadrature points of one element by angle
+// addition from the element's vertex 0: x = x0 + delta with
+// delta = l1 d1 + l2 d2 + l3 d3 and z = pi delta, |z| <= pi max_i |d_i| <= zmax.
+// For zmax <= 0.25 the Taylor polynomials below (through z^11 / z^12) are
+// accurate to < 1e-17 relative, i.e. to the last bit before rounding; larger
+// elements keep the direct sinpi/cospi evaluation.
+struct AxisTrig {
+    double s0, c0;    // sinpi(x0), cospi(x0)
+    double d1, d2, d3;
+};
+__device__ __forceinline__ AxisTrig axis_trig(double x0, double x1, double x2, double x3) {
+    AxisTrig a;
+    sincospi(x0, &a.s0, &a.c0);
+    a.d1 = x1 - x0;
+    a.d2 = x2 - x0;
+    a.d3 = x3 - x0;
+    return a;
+}
+__device__ __forceinline__ double axis_zmax(const AxisTrig& a) {
+    return kPi * fmax(fabs(a.d1), fmax(fabs(a.d2), fabs(a.d3)));
+}
+__device__ __forceinline__ void sincos_small(double z, double& s, double& c) {
+    const double z2 = z * z;
+    double ps = fma(z2, -1.0 / 39916800.0, 1.0 / 362880.0);
+    ps = fma(z2, ps, -1.0 / 5040.0);
+    ps = fma(z2, ps, 1.0 / 120.0);
+    ps = fma(z2, ps, -1.0 / 6.0);
+    s = fma(z * z2, ps, z);
+    double pc = fma(z2, 1.0 / 479001600.0, -1.0 / 3628800.0);
+    pc = fma(z2, pc, 1.0 / 40320.0);
+    pc = fma(z2, pc, -1.0 / 720.0);
+    pc = fma(z2, pc, 1.0 / 24.0);
+    pc = fma(z2, pc, -0.5);
+    c = fma(z2, pc, 1.0);
+}
+// sin(pi x_q), cos(pi x_q) with x_q = x0 + l1 d1 + l2 d2 + l3 d3
+__device__ __forceinline__ void axis_sincos(const AxisTrig& a, double l1, double l2, double l3, double& s,
+                                            double& c) {
+    const double delta = fma(l3, a.d3, fma(l2, a.d2, l1 * a.d1));
+    double sz, cz;
+    sincos_small(kPi * delta, sz, cz);
+    s = fma(a.s0, cz, a.c0 * sz);
+    c = fma(a.c0, cz, -(a.s0 * sz));
+}
+
+// exp(d) for |d| <= 0.08 (through d^10: < 3e-20 relative)
+__device__ __forceinline__ double exp_small(double d) {
+    double p = fma(d, 1.0 / 3628800.0, 1.0 / 362880.0);
+    p = fma(d, p, 1.0 / 40320.0);
+    p = fma(d, p, 1.0 / 5040.0);
+    p = fma(d, p, 1.0 / 720.0);
+    p = fma(d, p, 1.0 / 120.0);
+    p = fma(d, p, 1.0 / 24.0);
+    p = fma(d, p, 1.0 / 6.0);
+    p = fma(d, p, 0.5);
+    p = fma(d, p, 1.0);
+    return fma(d, p, 1.0);
+}
+
 // loop-invariant factor of prob_f_fast
 template <int KIND>
 __device__ __forceinline__ double prob_f_pre(const Coef& k) {
