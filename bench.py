@@ -287,6 +287,10 @@ def main():
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
     hc, ht, hd, hn = pin(coords), pin(tets), pin(db), pin(nb)
     h2d = hc.nbytes + ht.nbytes + hd.nbytes + hn.nbytes
+    for _ in range(args.warmup):  # untimed: lets the device pool reach steady state
+        m2 = ph.Mesh.from_arrays(hc, ht, hd, hn)
+        m2.pipeline(cfg.problem, True)
+        del m2
     barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
