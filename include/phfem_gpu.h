@@ -164,15 +164,17 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * sell_val's diagonal slots and rhs_neg must be zeroed first.  Optional
  * debug outputs (may be NULL): a_blocks [16 nE], slot_coef [4 nE],
  * slot_mrow [4 nE].  rhs [4 nE] (= b + LN) is always written (recovery).
- * norms [2] (device) receive sum(rhs^2), sum(bd^2) partials, reduced
- * deterministically through partials[grid]. */
-int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
+ * norms [2] (device) receive sum(rhs^2), sum(bd^2) over the l face rows,
+ * reduced deterministically through partials[2 * grid].  redo [ne + 1] is
+ * scratch: the count and list of elements whose operands leave the
+ * reciprocal-division window and are recomputed with IEEE division. */
+int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
                                 const double* face_area, int32_t* sell_col, double* sell_val,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, double* norms,
-                                double* partials, unsigned long long* err, void* stream);
+                                double* partials, int32_t* redo, unsigned long long* err, void* stream);
 int phfem_gpu_assemble_grid(int64_t ne);
 
 /* --------------------------------------------------------------- solver */

@@ -176,158 +176,258 @@ __global__ void __launch_bounds__(kLoadThreads)
     }
 }
 
+// Everything one element contributes, computed before any scatter so that a
+// FastDiv pass whose operands left the exact window can be redone with
+// ExactDiv without double-counting atomics.
+struct ElemOut {
+    double s[4][4];   // S_T[r][q] (rows/cols of non-Neumann faces only)
+    double rb[4];     // r_T
+    double rhs[4];    // B_T = b + LN
+    double bdv[4];    // b_D of Dirichlet faces
+    double coef[4];   // C_T entries sigma*|F|/3
+    bool singular;
+};
+
+template <int KIND, class Dv>
+__device__ __forceinline__ void condense_compute(int64_t t, const V3 p[4], const Coef& k, const Slots& sl,
+                                                 const double area[4], const double b[4],
+                                                 double* __restrict__ a_blocks, ElemOut& o, Dv& dv) {
+    // boundary data first, while only the coordinates are live: Neumann
+    // terms (assembly.cpp:81-94; this element's Neumann faces in face order
+    // == local slot order) and Dirichlet traces b_D = |F| u_D(centroid)
+    // (assembly.cpp:96-104; stored tuple = owner slot's)
+    double ln[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        o.bdv[q] = 0.0;
+        if (!sl.bnd[q]) continue;
+        const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+        const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
+        const V3 s3 = vadd(vadd(q0, q1), q2);
+        const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
+        if (sl.row[q] >= 0) {
+            o.bdv[q] = mul(area[q], prob_u<KIND>(cen.x, cen.y, cen.z));
+            continue;
+        }
+        const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+        const double len = __dsqrt_rn(vdot(n, n));
+        const double ar = mul(0.5, len);
+        const Div dl = dv.make(len);
+        const V3 un = {dv.div(n.x, dl), dv.div(n.y, dl), dv.div(n.z, dl)};
+        const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+        const double contrib = dv.div(mul(ar, gc), kDiv3);
+        ln[i0] = add(ln[i0], contrib);
+        ln[i1] = add(ln[i1], contrib);
+        ln[i2] = add(ln[i2], contrib);
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o.rhs[v] = add(b[v], ln[v]);  // assembly.cpp:135
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
+        const double sg = sl.owner[q] ? 1.0 : -1.0;
+        o.coef[q] = dv.div(mul(sg, area[q]), kDiv3);
+    }
+    Local L;
+    local_matrices(p, k, L, dv);  // local_stiffness_mass (assembly.cpp:7-33)
+    if (a_blocks) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a_blocks[16 * t + 4 * i + j] = L.a[i][j];
+    }
+    // local Schur complement (solver.cpp:101-127)
+    Lu4 lu;
+    lu_factor(L.a, lu, dv);
+    o.singular = lu.singular;
+    if (lu.singular) return;
+    // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
+    // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
+    auto cr = [&](int r, int v) -> double {
+        const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
+        return on ? o.coef[r] : 0.0;
+    };
+    // one solved column x = A^-1 c_q at a time; S_T[r][q] accumulated over
+    // p = 0..3 exactly as solver.cpp:121-125
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (sl.row[q] < 0) continue;
+        const double cq[4] = {cr(q, 0), cr(q, 1), cr(q, 2), cr(q, 3)};
+        double x[4];
+        lu_solve(lu, cq, x, dv);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
+            o.s[r][q] = s;
+        }
+    }
+    double ainv_b[4];
+    lu_solve(lu, o.rhs, ainv_b, dv);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        double rb = 0.0;
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
+        o.rb[r] = rb;
+    }
+}
+
+// Scatter of one element's S_T, b_D - r_T and B_T (assembly.cpp:135,
+// solver.cpp:131-145): row R of face r, owner slot -> positions 0 (atomic
+// diagonal) and 1-3, second slot -> 0 and 4-6; padding col = R, val = 0.
+__device__ __forceinline__ void scatter_elem(int64_t t, const Slots& sl, const ElemOut& o,
+                                             int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+                                             double* __restrict__ rhs_neg, double* __restrict__ bd,
+                                             double* __restrict__ rhs, double* __restrict__ slot_coef,
+                                             int32_t* __restrict__ slot_mrow) {
+    if (slot_coef) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) slot_coef[4 * t + q] = o.coef[q];
+    }
+    if (slot_mrow) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = sl.row[q];
+    }
+    reinterpret_cast<double2*>(rhs)[2 * t] = make_double2(o.rhs[0], o.rhs[1]);
+    reinterpret_cast<double2*>(rhs)[2 * t + 1] = make_double2(o.rhs[2], o.rhs[3]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if (sl.row[r] < 0) continue;
+        const int64_t R = sl.row[r];
+        const int base = sl.owner[r] ? 0 : 3;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q == r) {
+                atomicAdd(sell_val + sell_idx(R, 0), o.s[r][r]);
+                sell_col[sell_idx(R, 0)] = (int32_t)R;
+                continue;
+            }
+            const int64_t ix = sell_idx(R, base + 1 + (q < r ? q : q - 1));
+            const bool real = sl.row[q] >= 0;
+            sell_col[ix] = real ? sl.row[q] : (int32_t)R;
+            sell_val[ix] = real ? o.s[r][q] : 0.0;
+        }
+        if (sl.bnd[r]) {
+#pragma unroll
+            for (int pos = 4; pos < 7; ++pos) {
+                sell_col[sell_idx(R, pos)] = (int32_t)R;
+                sell_val[sell_idx(R, pos)] = 0.0;
+            }
+            rhs_neg[R] = sub(o.bdv[r], o.rb[r]);  // b_D - r_T, single contributor
+            bd[R] = o.bdv[r];
+        } else {
+            atomicAdd(rhs_neg + R, -o.rb[r]);
+        }
+    }
+}
+
+struct ElemIn {
+    V3 p[4];
+    Coef k;
+    Slots sl;
+    double area[4], b[4];
+};
+
+__device__ __forceinline__ void load_elem(int64_t t, const double* __restrict__ coords,
+                                          const int32_t* __restrict__ tets, const phg_problem& prob,
+                                          const int32_t* __restrict__ face_of_slot,
+                                          const int32_t* __restrict__ slot_mate, const int32_t* __restrict__ face_mrow,
+                                          const double* __restrict__ face_area, const double* __restrict__ b_in,
+                                          ElemIn& in) {
+    const int4 e = ldtet(tets, t);
+    in.p[0] = ldnode(coords, e.x);
+    in.p[1] = ldnode(coords, e.y);
+    in.p[2] = ldnode(coords, e.z);
+    in.p[3] = ldnode(coords, e.w);
+    in.k = load_coef(prob, t);
+    load_slots(t, face_of_slot, slot_mate, face_mrow, in.sl);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) in.area[q] = __ldg(face_area + in.sl.face[q]);
+    const double2 r01 = reinterpret_cast<const double2*>(b_in)[2 * t];
+    const double2 r23 = reinterpret_cast<const double2*>(b_in)[2 * t + 1];
+    in.b[0] = r01.x;
+    in.b[1] = r01.y;
+    in.b[2] = r23.x;
+    in.b[3] = r23.y;
+}
+
+__device__ __forceinline__ bool elem_degenerate(const ElemIn& in) {
+    return vdot(vcross(vsub(in.p[1], in.p[0]), vsub(in.p[2], in.p[0])), vsub(in.p[3], in.p[0])) == 0.0;
+}
+
+// Fast pass: straight-line division (FastDiv).  An element whose operands
+// left the exact window is appended to redo_list and not scattered.
+// b_in holds the Gauss load vector from load_k and is overwritten by
+// B_T = b + LN (the input is read before the write, per element).
 template <int KIND>
 __global__ void __launch_bounds__(kCondThreads, 4)
     condense_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
-               double* __restrict__ rhs_in, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+               double* __restrict__ rhs, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
                double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
-               double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, double* __restrict__ partials,
-               unsigned long long* err) {
-    __shared__ double sh[kCondThreads / 32];
-    double acc_bd = 0.0, acc_rhs = 0.0;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
-        const int4 e = ldtet(tets, t);
-        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
-        const Coef k = load_coef(prob, t);
-        Slots sl;
-        load_slots(t, face_of_slot, slot_mate, face_mrow, sl);
-        // boundary data first, while only the coordinates are live:
-        // Neumann terms (assembly.cpp:81-94; this element's Neumann faces in
-        // face order == local slot order) and Dirichlet traces b_D = |F|
-        // u_D(centroid) (assembly.cpp:96-104; stored tuple = owner slot)
-        double ln[4] = {0.0, 0.0, 0.0, 0.0};
-        double bdv[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!sl.bnd[q]) continue;
-            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
-            const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
-            const V3 cen = vdivq(vadd(vadd(q0, q1), q2), kDiv3);
-            if (sl.row[q] >= 0) {
-                bdv[q] = mul(__ldg(face_area + sl.face[q]), prob_u<KIND>(cen.x, cen.y, cen.z));
-                continue;
-            }
-            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
-            const double len = __dsqrt_rn(vdot(n, n));
-            const double ar = mul(0.5, len);
-            const V3 un = vdivq(n, make_div(len));
-            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-            const double contrib = dq(mul(ar, gc), kDiv3);
-            ln[i0] = add(ln[i0], contrib);
-            ln[i1] = add(ln[i1], contrib);
-            ln[i2] = add(ln[i2], contrib);
-        }
-        Local L;
-        local_matrices(p, k, L);  // local_stiffness_mass (assembly.cpp:7-33)
-        if (L.degenerate) continue;  // reported by load_k
-        double coef[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
-            const double sg = sl.owner[q] ? 1.0 : -1.0;
-            coef[q] = dq(mul(sg, __ldg(face_area + sl.face[q])), kDiv3);
-        }
-        if (a_blocks) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) a_blocks[16 * t + 4 * i + j] = L.a[i][j];
-        }
-        if (slot_coef) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) slot_coef[4 * t + q] = coef[q];
-        }
-        if (slot_mrow) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = sl.row[q];
-        }
-        const double2 r01 = reinterpret_cast<const double2*>(rhs_in)[2 * t];
-        const double2 r23 = reinterpret_cast<const double2*>(rhs_in)[2 * t + 1];
-        const double rhs[4] = {add(r01.x, ln[0]), add(r01.y, ln[1]), add(r23.x, ln[2]), add(r23.y, ln[3])};
-        reinterpret_cast<double2*>(const_cast<double*>(rhs_in))[2 * t] = make_double2(rhs[0], rhs[1]);
-        reinterpret_cast<double2*>(const_cast<double*>(rhs_in))[2 * t + 1] = make_double2(rhs[2], rhs[3]);
-        acc_rhs = add(acc_rhs, add(add(add(mul(rhs[0], rhs[0]), mul(rhs[1], rhs[1])), mul(rhs[2], rhs[2])),
-                                   mul(rhs[3], rhs[3])));
+               double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, int32_t* __restrict__ redo_list,
+               int32_t* __restrict__ redo_count, unsigned long long* err) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= ne) return;
+    ElemIn in;
+    load_elem(t, coords, tets, prob, face_of_slot, slot_mate, face_mrow, face_area, rhs, in);
+    if (elem_degenerate(in)) return;  // reported by load_k (assembly.cpp:13-14)
+    ElemOut o;
+    FastDiv fd;
+    condense_compute<KIND>(t, in.p, in.k, in.sl, in.area, in.b, a_blocks, o, fd);
+    if (!fd.ok) {
+        redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
+        return;
+    }
+    if (o.singular) {  // "degenerate element block" (solver.cpp:103-109)
+        report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
+        return;
+    }
+    scatter_elem(t, in.sl, o, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow);
+}
 
-        // local Schur complement (solver.cpp:101-127)
-        Lu4 lu;
-        lu_factor(L.a, lu);
-        if (lu.singular) {
+// Exact pass over the listed elements (IEEE division throughout).
+template <int KIND>
+__global__ void __launch_bounds__(kCondThreads)
+    condense_redo_k(const int32_t* __restrict__ redo_list, const int32_t* __restrict__ redo_count,
+                    const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
+                    const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
+                    const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
+                    double* __restrict__ rhs, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+                    double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
+                    double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, unsigned long long* err) {
+    const int32_t n = *redo_count;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int64_t t = redo_list[i];
+        ElemIn in;
+        load_elem(t, coords, tets, prob, face_of_slot, slot_mate, face_mrow, face_area, rhs, in);
+        ElemOut o;
+        ExactDiv ed;
+        condense_compute<KIND>(t, in.p, in.k, in.sl, in.area, in.b, a_blocks, o, ed);
+        if (o.singular) {
             report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
             continue;
         }
-        // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
-        // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
-        auto cr = [&](int r, int v) -> double {
-            const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
-            return on ? coef[r] : 0.0;
-        };
-        // one solved column x = A^-1 c_q at a time: S_T[r][q] for all r,
-        // accumulated over p = 0..3 exactly as solver.cpp:121-125
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (sl.row[q] < 0) {
-                // Neumann column: padding in the rows of the other faces
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    if (r == q || sl.row[r] < 0) continue;
-                    const int64_t R = sl.row[r];
-                    const int64_t ix = sell_idx(R, (sl.owner[r] ? 0 : 3) + 1 + (q < r ? q : q - 1));
-                    sell_col[ix] = (int32_t)R;
-                    sell_val[ix] = 0.0;
-                }
-                continue;
-            }
-            const double cq[4] = {cr(q, 0), cr(q, 1), cr(q, 2), cr(q, 3)};
-            double x[4];
-            lu_solve(lu, cq, x);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (sl.row[r] < 0) continue;
-                double s = 0.0;
-#pragma unroll
-                for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
-                const int64_t R = sl.row[r];
-                if (q == r) {
-                    atomicAdd(sell_val + sell_idx(R, 0), s);
-                    sell_col[sell_idx(R, 0)] = (int32_t)R;
-                } else {
-                    const int64_t ix = sell_idx(R, (sl.owner[r] ? 0 : 3) + 1 + (q < r ? q : q - 1));
-                    sell_col[ix] = sl.row[q];
-                    sell_val[ix] = s;
-                }
-            }
-        }
-        double ainv_b[4];
-        lu_solve(lu, rhs, ainv_b);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            if (sl.row[r] < 0) continue;
-            double rb = 0.0;
-#pragma unroll
-            for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
-            const int64_t R = sl.row[r];
-            if (sl.bnd[r]) {
-#pragma unroll
-                for (int pos = 4; pos < 7; ++pos) {
-                    sell_col[sell_idx(R, pos)] = (int32_t)R;
-                    sell_val[sell_idx(R, pos)] = 0.0;
-                }
-                // rhs_neg = b_D - r_T (solver.cpp:131-138), single contributor
-                rhs_neg[R] = sub(bdv[r], rb);
-                bd[R] = bdv[r];
-                acc_bd = add(acc_bd, mul(bdv[r], bdv[r]));
-            } else {
-                atomicAdd(rhs_neg + R, -rb);
-            }
-        }
+        scatter_elem(t, in.sl, o, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow);
     }
-    const double s0 = block_sum(acc_rhs, sh);
-    const double s1 = block_sum(acc_bd, sh);
+}
+
+// deterministic sums of squares of B_T and b_D (fixed grid, fixed order)
+__global__ void __launch_bounds__(256) sumsq2_k(const double* __restrict__ a, int64_t na, const double* __restrict__ b,
+                                                int64_t nb, double* __restrict__ partials) {
+    __shared__ double sh[8];
+    double sa = 0.0, sb = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < na; i += (int64_t)gridDim.x * blockDim.x)
+        sa = fma(a[i], a[i], sa);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb; i += (int64_t)gridDim.x * blockDim.x)
+        sb = fma(b[i], b[i], sb);
+    sa = block_sum(sa, sh);
+    sb = block_sum(sb, sh);
     if (threadIdx.x == 0) {
-        partials[2 * blockIdx.x] = s0;
-        partials[2 * blockIdx.x + 1] = s1;
+        partials[2 * blockIdx.x] = sa;
+        partials[2 * blockIdx.x + 1] = sb;
     }
 }
 
@@ -377,26 +477,36 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
 // (and so the S rows they scatter into) stay within an L2-resident window;
 // a grid-stride loop spread them over ~600k elements and turned the
 // scattered SELL writes into DRAM read-modify-writes (ncu, profiles/).
+// partial-sum slots used by the deterministic norm reduction
+constexpr int kNormGrid = kSMs * 8;
 extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
-    return grid_for(ne, kLoadThreads);
+    (void)ne;
+    return kNormGrid;
 }
 
-extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, const int32_t* tets,
+extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                            const phg_problem* prob, const int32_t* face_of_slot,
                                            const int32_t* slot_mate, const int32_t* face_mrow,
                                            const double* face_area, int32_t* sell_col, double* sell_val,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
-                                           unsigned long long* err, void* stream) {
+                                           int32_t* redo, unsigned long long* err, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    const int grid = phfem_gpu_assemble_grid(ne);
+    if (ne == 0) return 0;
+    // one element per thread, blocks in element order: the elements in flight
+    // (and the S rows they scatter into) stay in an L2-resident window
+    const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
     const phg_problem p = *prob;
-#define PHG_ASM(K)                                                                                                  \
-    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, partials,  \
-                                            err);                                                                   \
-    condense_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area, \
-                                                rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,         \
-                                                slot_mrow, partials, err)
+    cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
+#define PHG_ASM(K)                                                                                                   \
+    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, partials,   \
+                                            err);                                                                    \
+    condense_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
+                                                rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,          \
+                                                slot_mrow, redo + 1, redo, err);                                    \
+    condense_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
+                                                     face_mrow, face_area, rhs, sell_col, sell_val, rhs_neg, bd,    \
+                                                     a_blocks, slot_coef, slot_mrow, err)
     switch (p.kind) {
         case 0: PHG_ASM(0); break;
         case 1: PHG_ASM(1); break;
@@ -407,7 +517,8 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, const double* coords, con
         default: return (int)cudaErrorInvalidValue;
     }
 #undef PHG_ASM
-    reduce_pairs<<<1, 1024, 0, s>>>(partials, grid, norms);
-    phg::count_launches(3);
+    sumsq2_k<<<kNormGrid, 256, 0, s>>>(rhs, 4 * ne, bd, l, partials);
+    reduce_pairs<<<1, 1024, 0, s>>>(partials, kNormGrid, norms);
+    phg::count_launches(5);
     return (int)cudaGetLastError();
 }

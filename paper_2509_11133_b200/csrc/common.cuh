@@ -51,6 +51,26 @@ __device__ __forceinline__ double dq(double a, const Div& d) {
     return div_slow(a, d.b);
 }
 
+// Branch-free variant for straight-line element code: always takes the
+// reciprocal path and clears `ok` when an operand is outside the window
+// (zero numerators are fine); callers recompute the element with exact
+// division when ok ends up false.
+__device__ __forceinline__ bool dq_in_range(double a) {
+    const unsigned hi = (unsigned)(__double_as_longlong(a) >> 32);
+    const unsigned e = (hi >> 20) & 0x7FFu;  // biased exponent
+    return (e - (1023u - 499u)) < 998u || a == 0.0;
+}
+__device__ __forceinline__ double dq_fast(double a, const Div& d, bool& ok) {
+    ok = ok && dq_in_range(a);
+    const double q0 = __dmul_rn(a, d.r);
+    const double rem = __fma_rn(-d.b, q0, a);
+    return __fma_rn(rem, d.r, q0);
+}
+__device__ __forceinline__ Div make_div_fast(double b, bool& ok) {
+    ok = ok && dq_in_range(b) && b != 0.0;
+    return {b, __drcp_rn(b), true};
+}
+
 struct V3 {
     double x, y, z;
 };

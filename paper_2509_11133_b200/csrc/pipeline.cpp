@@ -286,13 +286,14 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     Work& w = sys.w;
     w.partials.alloc(2 * (int64_t)grid);
     w.norms.alloc(2);
+    w.redo.alloc(m.ne + 1);
     reset_err(w);
     const phg_problem p = device_problem(k, problem);
-    check(phfem_gpu_assemble_condense(m.ne, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
+    check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
                                       c.face_mrow.p, c.face_area.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,
-                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.err.p, SV()),
+                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p, w.err.p, SV()),
           "assemble");
     const double ms = tm.stop_ms();
     if (st) st->assemble += ms;

@@ -201,6 +201,21 @@ __device__ __forceinline__ Coef load_coef(const phg_problem& p, int64_t t) {
 
 // -------------------------------------------------------------- element core
 
+// Division policies of the element core.  ExactDiv gives IEEE quotients
+// (dq: shared reciprocal + Markstein, IEEE fallback).  FastDiv is
+// straight-line (no branches) and records in `ok` whether every operand was
+// inside the window where that equals IEEE division; when it is not, the
+// caller recomputes the element with ExactDiv.
+struct ExactDiv {
+    __device__ __forceinline__ double div(double a, const Div& d) { return dq(a, d); }
+    __device__ __forceinline__ Div make(double b) { return make_div(b); }
+};
+struct FastDiv {
+    bool ok = true;
+    __device__ __forceinline__ double div(double a, const Div& d) { return dq_fast(a, d, ok); }
+    __device__ __forceinline__ Div make(double b) { return make_div_fast(b, ok); }
+};
+
 // local_stiffness_mass (assembly.cpp:7-33) with A_T = K(A) + c M
 struct Local {
     double a[4][4];
@@ -209,18 +224,19 @@ struct Local {
     bool degenerate;
 };
 
-__device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Local& L) {
+template <class Dv>
+__device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Local& L, Dv& dv) {
     const V3 d1 = vsub(p[1], p[0]), d2 = vsub(p[2], p[0]), d3 = vsub(p[3], p[0]);
     const double det = vdot(vcross(d1, d2), d3);
     L.degenerate = det == 0.0;
-    L.vol = dq(fabs(det), kDiv6);
-    const Div ddet = make_div(det);
+    L.vol = dv.div(fabs(det), kDiv6);
+    const Div ddet = dv.make(det);
     const V3 c1 = vcross(d2, d3), c2 = vcross(d3, d1), c3 = vcross(d1, d2);
-    L.g[1] = {dq(c1.x, ddet), dq(c1.y, ddet), dq(c1.z, ddet)};
-    L.g[2] = {dq(c2.x, ddet), dq(c2.y, ddet), dq(c2.z, ddet)};
-    L.g[3] = {dq(c3.x, ddet), dq(c3.y, ddet), dq(c3.z, ddet)};
+    L.g[1] = {dv.div(c1.x, ddet), dv.div(c1.y, ddet), dv.div(c1.z, ddet)};
+    L.g[2] = {dv.div(c2.x, ddet), dv.div(c2.y, ddet), dv.div(c2.z, ddet)};
+    L.g[3] = {dv.div(c3.x, ddet), dv.div(c3.y, ddet), dv.div(c3.z, ddet)};
     L.g[0] = vmul(vadd(vadd(L.g[1], L.g[2]), L.g[3]), -1.0);
-    const double m20 = dq(L.vol, kDiv20);
+    const double m20 = dv.div(L.vol, kDiv20);
     const double mdiag = mul(k.c, mul(m20, 2.0)), moff = mul(k.c, mul(m20, 1.0));
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -231,6 +247,10 @@ __device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Loc
             L.a[i][j] = add(mul(L.vol, d), i == j ? mdiag : moff);
         }
 }
+__device__ __forceinline__ void local_matrices(const V3 p[4], const Coef& k, Local& L) {
+    ExactDiv dv;
+    local_matrices(p, k, L, dv);
+}
 
 // Mat4Lu::factor / solve (geom.hpp:48-87)
 struct Lu4 {
@@ -240,7 +260,8 @@ struct Lu4 {
     Div piv[4];  // shared reciprocals of the pivots lu[i][i]
 };
 
-__device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
+template <class Dv>
+__device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f, Dv& dv) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         f.perm[i] = i;
@@ -276,22 +297,27 @@ __device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
                 }
             }
         }
-        f.piv[col] = make_div(f.lu[col][col]);
+        f.piv[col] = dv.make(f.lu[col][col]);
 #pragma unroll
         for (int r = col + 1; r < 4; ++r) {
-            const double m = dq(f.lu[r][col], f.piv[col]);
+            const double m = dv.div(f.lu[r][col], f.piv[col]);
             f.lu[r][col] = m;
 #pragma unroll
             for (int c = col + 1; c < 4; ++c) f.lu[r][c] = sub(f.lu[r][c], mul(m, f.lu[col][c]));
         }
     }
 }
+__device__ __forceinline__ void lu_factor(const double a[4][4], Lu4& f) {
+    ExactDiv dv;
+    lu_factor(a, f, dv);
+}
 
 __device__ __forceinline__ double sel4(const double b[4], int i) {
     return i == 0 ? b[0] : (i == 1 ? b[1] : (i == 2 ? b[2] : b[3]));
 }
 
-__device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double x[4]) {
+template <class Dv>
+__device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double x[4], Dv& dv) {
     double y[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -305,8 +331,12 @@ __device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double
         double s = y[i];
 #pragma unroll
         for (int j = i + 1; j < 4; ++j) s = sub(s, mul(f.lu[i][j], x[j]));
-        x[i] = dq(s, f.piv[i]);
+        x[i] = dv.div(s, f.piv[i]);
     }
+}
+__device__ __forceinline__ void lu_solve(const Lu4& f, const double b[4], double x[4]) {
+    ExactDiv dv;
+    lu_solve(f, b, x, dv);
 }
 
 }  // namespace phg
