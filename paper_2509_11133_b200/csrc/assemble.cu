@@ -73,11 +73,49 @@ __device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict_
     }
 }
 
+// Gauss-64 load vector of the transcendental kinds with the trig / exp
+// factors as order-N Taylor series around vertex 0 (problems.cuh)
+template <int KIND, int N>
+__device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Coef& k, double vol, double b[4]) {
+    const int GX = KIND == 3 ? kTaySin : kTayExp;
+    const int GY = KIND == 4 ? kTayCos : kTaySin;
+    const AxisTaylor<N> tx = axis_taylor<N, GX>(p[0].x, p[1].x, p[2].x, p[3].x);
+    const AxisTaylor<N> ty = axis_taylor<N, GY>(p[0].y, p[1].y, p[2].y, p[3].y);
+    const AxisTaylor<N> tz = axis_taylor<N, kTaySin>(p[0].z, p[1].z, p[2].z, p[3].z);
+    (void)tz;
+    (void)tx;
+#pragma unroll 2
+    for (int qp = 0; qp < 64; ++qp) {
+        const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2], l3 = c_lam5[4 * qp + 3];
+        double f;
+        if constexpr (KIND == 3) {
+            // the constant factor cpre is applied once after the loop
+            f = taylor_eval(tx, l1, l2, l3) * taylor_eval(ty, l1, l2, l3) * taylor_eval(tz, l1, l2, l3);
+        } else if constexpr (KIND == 4) {
+            const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
+            const double ec = taylor_eval(tx, l1, l2, l3) * taylor_eval(ty, l1, l2, l3);
+            f = fma(cpre, ec * (z * z), -(k.a2 * 2.0) * ec);
+        } else {
+            const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
+            const double s = taylor_eval(ty, l1, l2, l3) * taylor_eval(tz, l1, l2, l3);
+            f = fma(cpre, x * (8.0 - x) * s, 2.0 * k.a0 * s);
+        }
+        const double fw = c_w5[qp] * f;
+        b[0] = fma(fw, l0, b[0]);
+        b[1] = fma(fw, l1, b[1]);
+        b[2] = fma(fw, l2, b[2]);
+        b[3] = fma(fw, l3, b[3]);
+    }
+    const double sc = KIND == 3 ? vol * cpre : vol;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] *= sc;
+}
+
 // B_T: Gauss-64 load vector (assembly.cpp:64-78) + Neumann terms
 // (assembly.cpp:81-94, face order == local slot order for one element),
 // rhs = b + LN (assembly.cpp:135).
 template <int KIND>
-__global__ void __launch_bounds__(kLoadThreads)
+__global__ void __launch_bounds__(kLoadThreads, 4)
     load_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
            const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
            const int32_t* __restrict__ face_mrow, double* __restrict__ rhs_out, double* __restrict__ partials,
@@ -114,60 +152,30 @@ __global__ void __launch_bounds__(kLoadThreads)
             }
         } else {
             const double cpre = prob_f_pre<KIND>(k);
-            // trig factors by angle addition from vertex 0 when the element
-            // is small enough (problems.cuh: axis_sincos), else sinpi/cospi
-            const AxisTrig ax = axis_trig(p[0].x, p[1].x, p[2].x, p[3].x);
-            const AxisTrig ay = axis_trig(p[0].y, p[1].y, p[2].y, p[3].y);
-            const AxisTrig az = axis_trig(p[0].z, p[1].z, p[2].z, p[3].z);
-            const double zmax = fmax(axis_zmax(ax), fmax(axis_zmax(ay), axis_zmax(az)));
-            if (zmax <= 0.25) {
-                const double e0 = KIND == 4 ? exp(p[0].x) : 0.0;
+            // Taylor expansion around vertex 0 when the element is small
+            // enough (problems.cuh: axis_taylor), else sinpi/cospi/exp
+            const double zmax = fmax(axis_zmax(p[0].x, p[1].x, p[2].x, p[3].x),
+                                     fmax(axis_zmax(p[0].y, p[1].y, p[2].y, p[3].y),
+                                          axis_zmax(p[0].z, p[1].z, p[2].z, p[3].z)));
+            switch (taylor_order(zmax)) {
+                case 7: load_taylor<KIND, 7>(p, cpre, k, vol, b); break;
+                case 8: load_taylor<KIND, 8>(p, cpre, k, vol, b); break;
+                case 10: load_taylor<KIND, 10>(p, cpre, k, vol, b); break;
+                case 13: load_taylor<KIND, 13>(p, cpre, k, vol, b); break;
+                default:
 #pragma unroll 2
-                for (int qp = 0; qp < 64; ++qp) {
-                    const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
-                                 l3 = c_lam5[4 * qp + 3];
-                    double f;
-                    if constexpr (KIND == 3) {
-                        double sx, cx, sy, cy, sz, cz;
-                        axis_sincos(ax, l1, l2, l3, sx, cx);
-                        axis_sincos(ay, l1, l2, l3, sy, cy);
-                        axis_sincos(az, l1, l2, l3, sz, cz);
-                        f = cpre * (sx * sy * sz);
-                    } else if constexpr (KIND == 4) {
-                        const double dx = fma(l3, ax.d3, fma(l2, ax.d2, l1 * ax.d1));
-                        const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
-                        double sy, cy;
-                        axis_sincos(ay, l1, l2, l3, sy, cy);
-                        const double ec = (e0 * exp_small(dx)) * cy;
-                        f = fma(cpre, ec * (z * z), -(k.a2 * 2.0) * ec);
-                    } else {
+                    for (int qp = 0; qp < 64; ++qp) {
+                        const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                                     l3 = c_lam5[4 * qp + 3];
                         const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
-                        double sy, cy, sz, cz;
-                        axis_sincos(ay, l1, l2, l3, sy, cy);
-                        axis_sincos(az, l1, l2, l3, sz, cz);
-                        const double s = sy * sz;
-                        f = fma(cpre, x * (8.0 - x) * s, 2.0 * k.a0 * s);
+                        const double y = fma(p[3].y, l3, fma(p[2].y, l2, fma(p[1].y, l1, p[0].y * l0)));
+                        const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
+                        const double fw = (vol * c_w5[qp]) * prob_f_fast<KIND>(x, y, z, cpre, k);
+                        b[0] = fma(fw, l0, b[0]);
+                        b[1] = fma(fw, l1, b[1]);
+                        b[2] = fma(fw, l2, b[2]);
+                        b[3] = fma(fw, l3, b[3]);
                     }
-                    const double fw = (vol * c_w5[qp]) * f;
-                    b[0] = fma(fw, l0, b[0]);
-                    b[1] = fma(fw, l1, b[1]);
-                    b[2] = fma(fw, l2, b[2]);
-                    b[3] = fma(fw, l3, b[3]);
-                }
-            } else {
-#pragma unroll 2
-            for (int qp = 0; qp < 64; ++qp) {
-                const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
-                             l3 = c_lam5[4 * qp + 3];
-                const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
-                const double y = fma(p[3].y, l3, fma(p[2].y, l2, fma(p[1].y, l1, p[0].y * l0)));
-                const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
-                const double fw = (vol * c_w5[qp]) * prob_f_fast<KIND>(x, y, z, cpre, k);
-                b[0] = fma(fw, l0, b[0]);
-                b[1] = fma(fw, l1, b[1]);
-                b[2] = fma(fw, l2, b[2]);
-                b[3] = fma(fw, l3, b[3]);
-            }
             }
         }
         // b only; condense_k adds the Neumann terms (rhs = b + LN)

@@ -57,6 +57,10 @@ struct FaceTab {
 };
 
 __device__ __forceinline__ unsigned hash32(uint32_t k) { return k * 0x9E3779B1u; }
+// table slot from the HIGH bits of a multiplicative hash: the low bits of
+// k * odd depend only on the low bits of k, and structured meshes have
+// neighbour ids that agree there (v + 1, v + (n+1), v + (n+1)^2, ...)
+__device__ __forceinline__ unsigned bucket(unsigned h, unsigned mask) { return __umulhi(h, mask + 1); }
 __device__ __forceinline__ unsigned hash64(unsigned long long k) {
     k ^= k >> 29;
     k *= 0xBF58476D1CE4E5B9ull;
@@ -64,7 +68,7 @@ __device__ __forceinline__ unsigned hash64(unsigned long long k) {
 }
 
 __device__ __forceinline__ int edge_slot_insert(int32_t* key, unsigned mask, int32_t b) {
-    unsigned h = hash32((uint32_t)b) & mask;
+    unsigned h = bucket(hash32((uint32_t)b), mask);
     for (;;) {
         const int32_t old = atomicCAS(key + h, -1, b);
         if (old == -1 || old == b) return (int)h;
@@ -72,12 +76,12 @@ __device__ __forceinline__ int edge_slot_insert(int32_t* key, unsigned mask, int
     }
 }
 __device__ __forceinline__ int edge_slot_find(const int32_t* key, unsigned mask, int32_t b) {
-    unsigned h = hash32((uint32_t)b) & mask;
+    unsigned h = bucket(hash32((uint32_t)b), mask);
     while (key[h] != b) h = (h + 1) & mask;
     return (int)h;
 }
 __device__ __forceinline__ int face_slot_insert(unsigned long long* key, unsigned mask, unsigned long long k) {
-    unsigned h = hash64(k) & mask;
+    unsigned h = bucket(hash64(k), mask);
     for (;;) {
         const unsigned long long old = atomicCAS(key + h, ~0ull, k);
         if (old == ~0ull || old == k) return (int)h;
@@ -85,7 +89,7 @@ __device__ __forceinline__ int face_slot_insert(unsigned long long* key, unsigne
     }
 }
 __device__ __forceinline__ int face_slot_find(const unsigned long long* key, unsigned mask, unsigned long long k) {
-    unsigned h = hash64(k) & mask;
+    unsigned h = bucket(hash64(k), mask);
     while (key[h] != k) h = (h + 1) & mask;
     return (int)h;
 }
@@ -209,10 +213,12 @@ constexpr int kFastWarps = 4;
 // face's oriented cycle [abc],[acd],[adb],[dcb].  Packed 4-bit fields.
 __device__ __forceinline__ int nbr_of(int lv, int i) { return i + (i >= lv); }
 __device__ __forceinline__ void face_of(int lv, int i, int& k, int& xi, int& yi) {
-    // rows: lv; entries (k, x, y) for i = 0, 1, 2
-    constexpr unsigned tab[4][3] = {{0x012, 0x123, 0x231}, {0x020, 0x203, 0x332},
-                                    {0x001, 0x130, 0x313}, {0x102, 0x210, 0x321}};
-    const unsigned e = tab[lv][i];
+    // rows: lv; entries (k, x, y) for i = 0, 1, 2, 12 bits each
+    const unsigned long long row = lv == 0   ? 0x231123012ull
+                                   : lv == 1 ? 0x332203020ull
+                                   : lv == 2 ? 0x313130001ull
+                                             : 0x321210102ull;
+    const unsigned e = (unsigned)(row >> (12 * i)) & 0xfffu;
     k = (int)(e >> 8);
     xi = (int)((e >> 4) & 0xf);
     yi = (int)(e & 0xf);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                 const int32_t b = tv(tet, w);
                 if (b <= v) continue;
                 eslot[u][i] = (int32_t)(6 * t + edge_index(lv, w));
-                unsigned h = hash32((uint32_t)b) & mask;
+                unsigned h = bucket(hash32((uint32_t)b), mask);
                 for (;;) {
                     const int32_t old = atomicCAS(ekey + h, -1, b);
                     if (old == -1 || old == b) break;
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     if (x <= v || y <= v) continue;
                     const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
                                                          : ((unsigned long long)y << 32 | (uint32_t)x);
-                    unsigned h = hash64(key) & mask;
+                    unsigned h = bucket(hash64(key), mask);
                     for (;;) {
                         const unsigned long long old = atomicCAS(fkey + h, ~0ull, key);
                         if (old == ~0ull || old == key) break;

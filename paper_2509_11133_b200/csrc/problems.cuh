@@ -108,63 +108,78 @@ __device__ __forceinline__ double prob_f_fast(double x, double y, double z, doub
         return prob_f<KIND>(x, y, z, k);
     }
 }
-// sin(pi x), cos(pi x) at the quadrature points of one element by angle
-// addition from the element's vertex 0: x = x0 + delta with
-// delta = l1 d1 + l2 d2 + l3 d3 and z = pi delta, |z| <= pi max_i |d_i| <= zmax.
-// For zmax <= 0.25 the Taylor polynomials below (through z^11 / z^12) are
-// accurate to < 1e-17 relative, i.e. to the last bit before rounding; larger
-// elements keep the direct sinpi/cospi evaluation.
-struct AxisTrig {
-    double s0, c0;    // sinpi(x0), cospi(x0)
-    double d1, d2, d3;
+// sin(pi x), cos(pi x) and e^x at the quadrature points of one element as a
+// Taylor series around the element's vertex 0: x = x0 + delta with
+// delta = l1 d1 + l2 d2 + l3 d3.  With z = pi delta (trig) or z = delta (exp),
+//   g(x0 + delta) = sum_{n<=N} g^(n)(x0)/n! * z^n,
+// whose coefficients are formed once per element from sinpi/cospi/exp at x0;
+// one quadrature point then costs 3 + N FMA per axis.  All derivatives of
+// these g are bounded by 1 (trig) or e^x0 e^|delta| (exp), so the truncation
+// error is below zmax^(N+1)/(N+1)! relative; taylor_order() picks N with that
+// bound under 1e-17 (< ulp(1)/20).  Elements with zmax > 0.25 keep the
+// direct sinpi/cospi/exp evaluation.
+enum { kTaySin = 0, kTayCos = 1, kTayExp = 2 };
+template <int N>
+struct AxisTaylor {
+    double k[N + 1];
+    double e1, e2, e3;
 };
-__device__ __forceinline__ AxisTrig axis_trig(double x0, double x1, double x2, double x3) {
-    AxisTrig a;
-    sincospi(x0, &a.s0, &a.c0);
-    a.d1 = x1 - x0;
-    a.d2 = x2 - x0;
-    a.d3 = x3 - x0;
+__device__ __forceinline__ double inv_fact(int n) {
+    constexpr double f[14] = {1.0,
+                              1.0,
+                              1.0 / 2.0,
+                              1.0 / 6.0,
+                              1.0 / 24.0,
+                              1.0 / 120.0,
+                              1.0 / 720.0,
+                              1.0 / 5040.0,
+                              1.0 / 40320.0,
+                              1.0 / 362880.0,
+                              1.0 / 3628800.0,
+                              1.0 / 39916800.0,
+                              1.0 / 479001600.0,
+                              1.0 / 6227020800.0};
+    return f[n];
+}
+// |z| bound of one axis (pi-scaled; also bounds the exp axis' |delta|)
+__device__ __forceinline__ double axis_zmax(double x0, double x1, double x2, double x3) {
+    return kPi * fmax(fabs(x1 - x0), fmax(fabs(x2 - x0), fabs(x3 - x0)));
+}
+// 0 = out of range (direct evaluation)
+__device__ __forceinline__ int taylor_order(double zmax) {
+    // 0.028^8/8! = 9.4e-18, 0.05^9/9! = 5.4e-18, 0.12^11/11! = 1.9e-18,
+    // 0.25^14/14! = 4.3e-20
+    return zmax <= 0.028 ? 7 : (zmax <= 0.05 ? 8 : (zmax <= 0.12 ? 10 : (zmax <= 0.25 ? 13 : 0)));
+}
+template <int N, int G>
+__device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, double x2, double x3) {
+    AxisTaylor<N> a;
+    const double sc = G == kTayExp ? 1.0 : kPi;
+    a.e1 = sc * (x1 - x0);
+    a.e2 = sc * (x2 - x0);
+    a.e3 = sc * (x3 - x0);
+    if constexpr (G == kTayExp) {
+        const double e0 = exp(x0);
+#pragma unroll
+        for (int n = 0; n <= N; ++n) a.k[n] = e0 * inv_fact(n);
+    } else {
+        double s0, c0;
+        sincospi(x0, &s0, &c0);
+        // derivative cycle of sin: s c -s -c; of cos: c -s -c s
+        const double d[4] = {G == kTaySin ? s0 : c0, G == kTaySin ? c0 : -s0, G == kTaySin ? -s0 : -c0,
+                             G == kTaySin ? -c0 : s0};
+#pragma unroll
+        for (int n = 0; n <= N; ++n) a.k[n] = d[n & 3] * inv_fact(n);
+    }
     return a;
 }
-__device__ __forceinline__ double axis_zmax(const AxisTrig& a) {
-    return kPi * fmax(fabs(a.d1), fmax(fabs(a.d2), fabs(a.d3)));
-}
-__device__ __forceinline__ void sincos_small(double z, double& s, double& c) {
-    const double z2 = z * z;
-    double ps = fma(z2, -1.0 / 39916800.0, 1.0 / 362880.0);
-    ps = fma(z2, ps, -1.0 / 5040.0);
-    ps = fma(z2, ps, 1.0 / 120.0);
-    ps = fma(z2, ps, -1.0 / 6.0);
-    s = fma(z * z2, ps, z);
-    double pc = fma(z2, 1.0 / 479001600.0, -1.0 / 3628800.0);
-    pc = fma(z2, pc, 1.0 / 40320.0);
-    pc = fma(z2, pc, -1.0 / 720.0);
-    pc = fma(z2, pc, 1.0 / 24.0);
-    pc = fma(z2, pc, -0.5);
-    c = fma(z2, pc, 1.0);
-}
-// sin(pi x_q), cos(pi x_q) with x_q = x0 + l1 d1 + l2 d2 + l3 d3
-__device__ __forceinline__ void axis_sincos(const AxisTrig& a, double l1, double l2, double l3, double& s,
-                                            double& c) {
-    const double delta = fma(l3, a.d3, fma(l2, a.d2, l1 * a.d1));
-    double sz, cz;
-    sincos_small(kPi * delta, sz, cz);
-    s = fma(a.s0, cz, a.c0 * sz);
-    c = fma(a.c0, cz, -(a.s0 * sz));
-}
-
-// exp(d) for |d| <= 0.08 (through d^10: < 3e-20 relative)
-__device__ __forceinline__ double exp_small(double d) {
-    double p = fma(d, 1.0 / 3628800.0, 1.0 / 362880.0);
-    p = fma(d, p, 1.0 / 40320.0);
-    p = fma(d, p, 1.0 / 5040.0);
-    p = fma(d, p, 1.0 / 720.0);
-    p = fma(d, p, 1.0 / 120.0);
-    p = fma(d, p, 1.0 / 24.0);
-    p = fma(d, p, 1.0 / 6.0);
-    p = fma(d, p, 0.5);
-    p = fma(d, p, 1.0);
-    return fma(d, p, 1.0);
+template <int N>
+__device__ __forceinline__ double taylor_eval(const AxisTaylor<N>& a, double l1, double l2, double l3) {
+    const double z = fma(l3, a.e3, fma(l2, a.e2, l1 * a.e1));
+    double r = a.k[N];
+#pragma unroll
+    for (int n = N - 1; n >= 0; --n) r = fma(r, z, a.k[n]);
+    return r;
 }
 
 // loop-invariant factor of prob_f_fast
