@@ -236,21 +236,24 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                      int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
                      int32_t* __restrict__ defer_count, unsigned long long* err) {
     constexpr int CAP = E == 1 ? 128 : 256;  // > 3 * 32 E candidates
+    constexpr int LOG = E == 1 ? 7 : 8;
     constexpr unsigned mask = CAP - 1;
+    // Faces are keyed by the edge-table slots of their two upper vertices
+    // (both > v, so both are keys of v's edge table): a 2 LOG-bit key.
     __shared__ int32_t s_ekey[kFastWarps][CAP], s_eval[kFastWarps][CAP];
-    __shared__ unsigned long long s_fkey[kFastWarps][CAP];
+    __shared__ int32_t s_fkey[kFastWarps][CAP];
     __shared__ int32_t s_flo[kFastWarps][CAP], s_fhi[kFastWarps][CAP], s_fcnt[kFastWarps][CAP];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int32_t* ekey = s_ekey[warp];
     int32_t* eval = s_eval[warp];
-    unsigned long long* fkey = s_fkey[warp];
+    int32_t* fkey = s_fkey[warp];
     int32_t* flo = s_flo[warp];
     int32_t* fhi = s_fhi[warp];
     int32_t* fcnt = s_fcnt[warp];
     for (int i = lane; i < CAP; i += 32) {
         ekey[i] = -1;
         eval[i] = INT_MAX;
-        fkey[i] = ~0ull;
+        fkey[i] = -1;
         flo[i] = INT_MAX;
         fhi[i] = -1;
         fcnt[i] = 0;
@@ -279,6 +282,9 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             const int64_t t = inc >> 2;
             const int lv = inc & 3;
             const int4 tet = ldtet(tets, t);
+            // table slot + 1 of each local vertex above v (0 otherwise),
+            // 16-bit fields (no local-memory array)
+            unsigned long long hv = 0;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int w = nbr_of(lv, i);
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     h = (h + 1) & mask;
                 }
                 eh[u][i] = (int)h;
+                hv |= (unsigned long long)(h + 1) << (16 * w);
                 atomicMin(eval + h, eslot[u][i]);
             }
             if (do_faces) {
@@ -299,14 +306,13 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                 for (int i = 0; i < 3; ++i) {
                     int k, xi, yi;
                     face_of(lv, i, k, xi, yi);
-                    const int32_t x = tv(tet, xi), y = tv(tet, yi);
-                    if (x <= v || y <= v) continue;
-                    const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
-                                                         : ((unsigned long long)y << 32 | (uint32_t)x);
-                    unsigned h = bucket(hash64(key), mask);
+                    const int hx = (int)((hv >> (16 * xi)) & 0xffff) - 1, hy = (int)((hv >> (16 * yi)) & 0xffff) - 1;
+                    if ((hx | hy) < 0) continue;  // x or y <= v
+                    const int32_t key = hx < hy ? (hx << LOG | hy) : (hy << LOG | hx);
+                    unsigned h = bucket(hash32((uint32_t)key), mask);
                     for (;;) {
-                        const unsigned long long old = atomicCAS(fkey + h, ~0ull, key);
-                        if (old == ~0ull || old == key) break;
+                        const int32_t old = atomicCAS(fkey + h, -1, key);
+                        if (old == -1 || old == key) break;
                         h = (h + 1) & mask;
                     }
                     fh[u][i] = (int)h;
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     atomicMax(fhi + h, fslot[u][i]);
                     // count in bits 2+, orientation (x < y: 1, else 2) below:
                     // exactly one slot of each orientation sums to 11
-                    atomicAdd(fcnt + h, x < y ? 5 : 6);
+                    atomicAdd(fcnt + h, tv(tet, xi) < tv(tet, yi) ? 5 : 6);
                 }
             }
         }
@@ -348,7 +354,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     eval[eh[u][i]] = INT_MAX;
                 }
                 if (fh[u][i] >= 0) {
-                    fkey[fh[u][i]] = ~0ull;
+                    fkey[fh[u][i]] = -1;
                     flo[fh[u][i]] = INT_MAX;
                     fhi[fh[u][i]] = -1;
                     fcnt[fh[u][i]] = 0;
@@ -633,8 +639,15 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     // pass 3: anything larger (block per vertex); counts stay on the device
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(defer_count, 0, 2 * sizeof(int32_t), s);
+    // one full wave of resident blocks (grid-stride over the vertices)
+    static int resident = 0;
+    if (resident == 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, star_groups_warp<1>, 32 * kFastWarps, 0);
+        resident = (per_sm > 0 ? per_sm : 8) * kSMs;
+    }
     const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
-    const int grid = (int)(blocks < kSMs * 8 ? blocks : kSMs * 8);
+    const int grid = (int)(blocks < resident ? blocks : resident);
     star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
                                                          slot_mate, defer_list, defer_count, err);
     star_groups_warp<2><<<kSMs * 4, 32 * kFastWarps, 0, s>>>(0, defer_list, defer_count, star_ptr, star, tets,
