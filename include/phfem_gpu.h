@@ -161,7 +161,9 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
 
 /* Fused assemble_system + build_schur local part (assembly.cpp:7-138,
  * solver.cpp:90-127) with the direct scatter into SELL S and rhs_neg.
- * sell_val's diagonal slots and rhs_neg must be zeroed first.  Optional
+ * Rows 0..l-1 of the SELL arrays, rhs_neg and bd are fully written (the
+ * row owners clear the accumulated entries first); padding rows of the
+ * last slice are left untouched.  Optional
  * debug outputs (may be NULL): a_blocks [16 nE], slot_coef [4 nE],
  * slot_mrow [4 nE].  rhs [4 nE] (= b + LN) is always written (recovery).
  * norms [2] (device) receive sum(rhs^2), sum(bd^2) over the l face rows,

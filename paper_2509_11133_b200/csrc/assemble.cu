@@ -118,13 +118,26 @@ template <int KIND>
 __global__ void __launch_bounds__(kLoadThreads, 4)
     load_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
            const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
-           const int32_t* __restrict__ face_mrow, double* __restrict__ rhs_out, double* __restrict__ partials,
-           unsigned long long* err) {
-    (void)face_of_slot;
-    (void)slot_mate;
-    (void)face_mrow;
-    (void)partials;
+           const int32_t* __restrict__ face_mrow, double* __restrict__ rhs_out, double* __restrict__ sell_val,
+           double* __restrict__ rhs_neg, double* __restrict__ bd, unsigned long long* err) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        // clear the accumulated entries of the rows this element owns (each
+        // row has exactly one owner slot) for condense_k's atomics: the S
+        // diagonal, rhs_neg and b_D.  Free here: this kernel is fp64-bound.
+        {
+            const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+            const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int32_t mate = tv(mate4, q);
+                if (mate >= 0 && mate < (int32_t)(4 * t + q)) continue;
+                const int32_t R = __ldg(face_mrow + tv(fos4, q));
+                if (R < 0) continue;
+                sell_val[sell_idx(R, 0)] = 0.0;
+                rhs_neg[R] = 0.0;
+                bd[R] = 0.0;
+            }
+        }
         const int4 e = ldtet(tets, t);
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
         const Coef k = load_coef(prob, t);
@@ -507,8 +520,8 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     const phg_problem p = *prob;
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
 #define PHG_ASM(K)                                                                                                   \
-    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, partials,   \
-                                            err);                                                                    \
+    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, sell_val,   \
+                                            rhs_neg, bd, err);                                                       \
     condense_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
                                                 rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,          \
                                                 slot_mrow, redo + 1, redo, err);                                    \

@@ -264,14 +264,10 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     const int64_t width = PHG_SELL_C * PHG_SELL_W;
     sys.sell_col.alloc(sys.nchunks * width);
     sys.sell_val.alloc(sys.nchunks * width);
-    if (sys.nchunks)
-        check(cudaMemset2DAsync(sys.sell_val.p, width * sizeof(double), 0, PHG_SELL_C * sizeof(double),
-                                (size_t)sys.nchunks, S()),
-              "memset diag");
+    // the S diagonal, rhs_neg and b_D are cleared by the assembly kernel
+    // itself (row owners), every other SELL slot is written exactly once
     sys.rhs_neg.alloc(c.l);
-    sys.rhs_neg.zero();
     sys.bd.alloc(c.l);
-    sys.bd.zero();
     sys.rhs.alloc(4 * m.ne);
     if (debug_views) {
         sys.a_blocks.alloc(16 * m.ne);
