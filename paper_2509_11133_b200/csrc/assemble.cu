@@ -2,12 +2,12 @@
 // (assemble_system, assembly.cpp:7-138, and the local part of build_schur,
 // solver.cpp:90-127), scattering straight into the SELL-32 Schur matrix.
 //
-// Two element-parallel kernels, split by register footprint:
-//   load     B_T = Gauss-64 load vector + Neumann terms (assembly.cpp:46-94),
-//            the fp64-heavy part, at high occupancy (few live registers);
-//   condense A_T = K_T(A) + c M_T, C_T rows sigma*|F|/3, Dirichlet data,
-//            partial-pivot LU of A_T, S_T = C A^-1 C', r_T = C A^-1 B, and the
-//            scatter of S_T and b_D - r_T into the face system.
+// One fused element-parallel kernel per problem kind: the fp64-heavy
+// Gauss-64 load vector (assembly.cpp:46-78) and the latency-bound gathers /
+// scatter of the condensation overlap across the warps of an SM.  Per
+// element: B_T = b + Neumann terms, A_T = K_T(A) + c M_T, C_T rows
+// sigma*|F|/3, Dirichlet data, partial-pivot LU of A_T, S_T = C A^-1 C',
+// r_T = C A^-1 B, streamed into the face system as they are formed.
 // Everything the reference computes in these loops is replayed in its
 // operation order without FMA, so A_T, C_T and S_T are bit-identical; the
 // transcendental load data differ only by libm-vs-libdevice ulps.
@@ -32,7 +32,6 @@ namespace {
 
 using namespace phg;
 
-constexpr int kLoadThreads = 128;
 constexpr int kCondThreads = 128;
 
 __device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
@@ -111,123 +110,119 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
     for (int i = 0; i < 4; ++i) b[i] *= sc;
 }
 
-// B_T: Gauss-64 load vector (assembly.cpp:64-78) + Neumann terms
-// (assembly.cpp:81-94, face order == local slot order for one element),
-// rhs = b + LN (assembly.cpp:135).
+// Gauss-64 load vector b_T (assembly.cpp:64-78) of one element with
+// volume vol.
 template <int KIND>
-__global__ void __launch_bounds__(kLoadThreads, 4)
-    load_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
-           const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
-           const int32_t* __restrict__ face_mrow, double* __restrict__ rhs_out, double* __restrict__ sell_val,
-           double* __restrict__ rhs_neg, double* __restrict__ bd, unsigned long long* err) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
-        // clear the accumulated entries of the rows this element owns (each
-        // row has exactly one owner slot) for condense_k's atomics: the S
-        // diagonal, rhs_neg and b_D.  Free here: this kernel is fp64-bound.
-        {
-            const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-            const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
+__device__ __forceinline__ void load_vector(const V3 p[4], const Coef& k, double vol, double b[4]) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int32_t mate = tv(mate4, q);
-                if (mate >= 0 && mate < (int32_t)(4 * t + q)) continue;
-                const int32_t R = __ldg(face_mrow + tv(fos4, q));
-                if (R < 0) continue;
-                sell_val[sell_idx(R, 0)] = 0.0;
-                rhs_neg[R] = 0.0;
-                bd[R] = 0.0;
-            }
-        }
-        const int4 e = ldtet(tets, t);
-        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
-        const Coef k = load_coef(prob, t);
-        // elem_volume == local.volume (assembly.cpp:18, 47)
-        const V3 d1 = vsub(p[1], p[0]), d2 = vsub(p[2], p[0]), d3 = vsub(p[3], p[0]);
-        const double det = vdot(vcross(d1, d2), d3);
-        if (det == 0.0) {
-            report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
-            continue;
-        }
-        const double vol = dq(fabs(det), kDiv6);
-        double b[4] = {0.0, 0.0, 0.0, 0.0};
-        if constexpr (KIND <= 2) {
-            // polynomial data: the reference's exact operation order
+    for (int i = 0; i < 4; ++i) b[i] = 0.0;
+    if constexpr (KIND <= 2) {
+        // polynomial data: the reference's exact operation order
 #pragma unroll 2
-            for (int qp = 0; qp < 64; ++qp) {
-                const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
-                             l3 = c_lam5[4 * qp + 3];
-                const V3 x = vadd(vadd(vadd(vmul(p[0], l0), vmul(p[1], l1)), vmul(p[2], l2)), vmul(p[3], l3));
-                const double fw = mul(mul(vol, c_w5[qp]), prob_f<KIND>(x.x, x.y, x.z, k));
-                b[0] = add(b[0], mul(fw, l0));
-                b[1] = add(b[1], mul(fw, l1));
-                b[2] = add(b[2], mul(fw, l2));
-                b[3] = add(b[3], mul(fw, l3));
-            }
-        } else {
-            const double cpre = prob_f_pre<KIND>(k);
-            // Taylor expansion around vertex 0 when the element is small
-            // enough (problems.cuh: axis_taylor), else sinpi/cospi/exp
-            const double zmax = fmax(axis_zmax(p[0].x, p[1].x, p[2].x, p[3].x),
-                                     fmax(axis_zmax(p[0].y, p[1].y, p[2].y, p[3].y),
-                                          axis_zmax(p[0].z, p[1].z, p[2].z, p[3].z)));
-            switch (taylor_order(zmax)) {
-                case 7: load_taylor<KIND, 7>(p, cpre, k, vol, b); break;
-                case 8: load_taylor<KIND, 8>(p, cpre, k, vol, b); break;
-                case 10: load_taylor<KIND, 10>(p, cpre, k, vol, b); break;
-                case 13: load_taylor<KIND, 13>(p, cpre, k, vol, b); break;
-                default:
-#pragma unroll 2
-                    for (int qp = 0; qp < 64; ++qp) {
-                        const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
-                                     l3 = c_lam5[4 * qp + 3];
-                        const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
-                        const double y = fma(p[3].y, l3, fma(p[2].y, l2, fma(p[1].y, l1, p[0].y * l0)));
-                        const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
-                        const double fw = (vol * c_w5[qp]) * prob_f_fast<KIND>(x, y, z, cpre, k);
-                        b[0] = fma(fw, l0, b[0]);
-                        b[1] = fma(fw, l1, b[1]);
-                        b[2] = fma(fw, l2, b[2]);
-                        b[3] = fma(fw, l3, b[3]);
-                    }
-            }
+        for (int qp = 0; qp < 64; ++qp) {
+            const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                         l3 = c_lam5[4 * qp + 3];
+            const V3 x = vadd(vadd(vadd(vmul(p[0], l0), vmul(p[1], l1)), vmul(p[2], l2)), vmul(p[3], l3));
+            const double fw = mul(mul(vol, c_w5[qp]), prob_f<KIND>(x.x, x.y, x.z, k));
+            b[0] = add(b[0], mul(fw, l0));
+            b[1] = add(b[1], mul(fw, l1));
+            b[2] = add(b[2], mul(fw, l2));
+            b[3] = add(b[3], mul(fw, l3));
         }
-        // b only; condense_k adds the Neumann terms (rhs = b + LN)
-        reinterpret_cast<double2*>(rhs_out)[2 * t] = make_double2(b[0], b[1]);
-        reinterpret_cast<double2*>(rhs_out)[2 * t + 1] = make_double2(b[2], b[3]);
+    } else {
+        const double cpre = prob_f_pre<KIND>(k);
+        // Taylor expansion around vertex 0 when the element is small
+        // enough (problems.cuh: axis_taylor), else sinpi/cospi/exp
+        const double zmax = fmax(axis_zmax(p[0].x, p[1].x, p[2].x, p[3].x),
+                                 fmax(axis_zmax(p[0].y, p[1].y, p[2].y, p[3].y),
+                                      axis_zmax(p[0].z, p[1].z, p[2].z, p[3].z)));
+        switch (taylor_order(zmax)) {
+            case 7: load_taylor<KIND, 7>(p, cpre, k, vol, b); break;
+            case 8: load_taylor<KIND, 8>(p, cpre, k, vol, b); break;
+            case 10: load_taylor<KIND, 10>(p, cpre, k, vol, b); break;
+            default:
+#pragma unroll 2
+                for (int qp = 0; qp < 64; ++qp) {
+                    const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2],
+                                 l3 = c_lam5[4 * qp + 3];
+                    const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
+                    const double y = fma(p[3].y, l3, fma(p[2].y, l2, fma(p[1].y, l1, p[0].y * l0)));
+                    const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
+                    const double fw = (vol * c_w5[qp]) * prob_f_fast<KIND>(x, y, z, cpre, k);
+                    b[0] = fma(fw, l0, b[0]);
+                    b[1] = fma(fw, l1, b[1]);
+                    b[2] = fma(fw, l2, b[2]);
+                    b[3] = fma(fw, l3, b[3]);
+                }
+        }
     }
 }
 
-// Everything one element contributes, computed before any scatter so that a
-// FastDiv pass whose operands left the exact window can be redone with
-// ExactDiv without double-counting atomics.
-struct ElemOut {
-    double s[4][4];   // S_T[r][q] (rows/cols of non-Neumann faces only)
-    double rb[4];     // r_T
-    double rhs[4];    // B_T = b + LN
-    double bdv[4];    // b_D of Dirichlet faces
-    double coef[4];   // C_T entries sigma*|F|/3
-    bool singular;
+// face-side inputs of one element
+struct FaceIn {
+    const int32_t* __restrict__ face_of_slot;
+    const int32_t* __restrict__ slot_mate;
+    const int32_t* __restrict__ face_mrow;
+    const double* __restrict__ face_area;
 };
 
+// One element's assembly and condensation, streamed straight into the face
+// system (assembly.cpp:7-138, solver.cpp:101-145).  Every output except the
+// two-contributor sums (S diagonal and rhs_neg of interior rows) has a
+// single writer and is a plain store made as soon as it is known; those
+// atomics are issued only at the end, once dv.good() is known.  An element
+// whose FastDiv operands left the exact window returns 1 without any atomic:
+// its plain stores are garbage that the ExactDiv redo pass overwrites.
+// Returns 0 done, 1 redo, 2 singular block, 3 zero volume.
+//
+// Row R of face r: owner slot -> positions 0 (atomic diagonal) and 1-3,
+// second slot -> 0 and 4-6; padding col = R, val = 0.
 template <int KIND, class Dv>
-__device__ __forceinline__ void condense_compute(int64_t t, const V3 p[4], const Coef& k, const Slots& sl,
-                                                 const double area[4], const double b[4],
-                                                 double* __restrict__ a_blocks, ElemOut& o, Dv& dv) {
-    // boundary data first, while only the coordinates are live: Neumann
-    // terms (assembly.cpp:81-94; this element's Neumann faces in face order
-    // == local slot order) and Dirichlet traces b_D = |F| u_D(centroid)
-    // (assembly.cpp:96-104; stored tuple = owner slot's)
+__device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict__ coords,
+                                             const int32_t* __restrict__ tets, const phg_problem& prob,
+                                             const FaceIn& fin, double* __restrict__ a_blocks,
+                                             int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+                                             double* __restrict__ rhs_neg, double* __restrict__ bd,
+                                             double* __restrict__ rhs, double* __restrict__ slot_coef,
+                                             int32_t* __restrict__ slot_mrow, Dv& dv) {
+    V3 p[4];
+    {
+        const int4 e = ldtet(tets, t);
+        p[0] = ldnode(coords, e.x);
+        p[1] = ldnode(coords, e.y);
+        p[2] = ldnode(coords, e.z);
+        p[3] = ldnode(coords, e.w);
+    }
+    const Coef k = load_coef(prob, t);
+    // elem_volume == local.volume (assembly.cpp:18, 47)
+    double bt[4];
+    {
+        const double det = vdot(vcross(vsub(p[1], p[0]), vsub(p[2], p[0])), vsub(p[3], p[0]));
+        if (det == 0.0) return 3;
+        load_vector<KIND>(p, k, dq(fabs(det), kDiv6), bt);
+    }
+    // the face-side gathers only now, after the fp64-heavy load vector (the
+    // other warps of the SM cover their latency)
+    Slots sl;
+    load_slots(t, fin.face_of_slot, fin.slot_mate, fin.face_mrow, sl);
+    double area[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) area[q] = __ldg(fin.face_area + sl.face[q]);
+    // boundary data: Neumann terms (assembly.cpp:81-94; this element's
+    // Neumann faces in face order == local slot order) and Dirichlet traces
+    // b_D = |F| u_D(centroid) (assembly.cpp:96-104; stored tuple = owner's)
     double ln[4] = {0.0, 0.0, 0.0, 0.0};
+    double bdv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        o.bdv[q] = 0.0;
+        bdv[q] = 0.0;
         if (!sl.bnd[q]) continue;
         const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
         const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
         const V3 s3 = vadd(vadd(q0, q1), q2);
         const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
         if (sl.row[q] >= 0) {
-            o.bdv[q] = mul(area[q], prob_u<KIND>(cen.x, cen.y, cen.z));
+            bdv[q] = mul(area[q], prob_u<KIND>(cen.x, cen.y, cen.z));
             continue;
         }
         const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
@@ -242,148 +237,117 @@ __device__ __forceinline__ void condense_compute(int64_t t, const V3 p[4], const
         ln[i2] = add(ln[i2], contrib);
     }
 #pragma unroll
-    for (int v = 0; v < 4; ++v) o.rhs[v] = add(b[v], ln[v]);  // assembly.cpp:135
+    for (int v = 0; v < 4; ++v) bt[v] = add(bt[v], ln[v]);  // B_T = b + LN (assembly.cpp:135)
+    reinterpret_cast<double2*>(rhs)[2 * t] = make_double2(bt[0], bt[1]);
+    reinterpret_cast<double2*>(rhs)[2 * t + 1] = make_double2(bt[2], bt[3]);
+    double coef[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // slot_coef = sigma*|F|/3 (assembly.cpp:125)
         const double sg = sl.owner[q] ? 1.0 : -1.0;
-        o.coef[q] = dv.div(mul(sg, area[q]), kDiv3);
+        coef[q] = dv.div(mul(sg, area[q]), kDiv3);
     }
-    Local L;
-    local_matrices(p, k, L, dv);  // local_stiffness_mass (assembly.cpp:7-33)
-    if (a_blocks) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) a_blocks[16 * t + 4 * i + j] = L.a[i][j];
-    }
-    // local Schur complement (solver.cpp:101-127)
-    Lu4 lu;
-    lu_factor(L.a, lu, dv);
-    o.singular = lu.singular;
-    if (lu.singular) return;
-    // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
-    // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
-    auto cr = [&](int r, int v) -> double {
-        const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
-        return on ? o.coef[r] : 0.0;
-    };
-    // one solved column x = A^-1 c_q at a time; S_T[r][q] accumulated over
-    // p = 0..3 exactly as solver.cpp:121-125
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        if (sl.row[q] < 0) continue;
-        const double cq[4] = {cr(q, 0), cr(q, 1), cr(q, 2), cr(q, 3)};
-        double x[4];
-        lu_solve(lu, cq, x, dv);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            double s = 0.0;
-#pragma unroll
-            for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
-            o.s[r][q] = s;
-        }
-    }
-    double ainv_b[4];
-    lu_solve(lu, o.rhs, ainv_b, dv);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        double rb = 0.0;
-#pragma unroll
-        for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
-        o.rb[r] = rb;
-    }
-}
-
-// Scatter of one element's S_T, b_D - r_T and B_T (assembly.cpp:135,
-// solver.cpp:131-145): row R of face r, owner slot -> positions 0 (atomic
-// diagonal) and 1-3, second slot -> 0 and 4-6; padding col = R, val = 0.
-__device__ __forceinline__ void scatter_elem(int64_t t, const Slots& sl, const ElemOut& o,
-                                             int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
-                                             double* __restrict__ rhs_neg, double* __restrict__ bd,
-                                             double* __restrict__ rhs, double* __restrict__ slot_coef,
-                                             int32_t* __restrict__ slot_mrow) {
     if (slot_coef) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) slot_coef[4 * t + q] = o.coef[q];
+        for (int q = 0; q < 4; ++q) slot_coef[4 * t + q] = coef[q];
     }
     if (slot_mrow) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) slot_mrow[4 * t + q] = sl.row[q];
     }
-    reinterpret_cast<double2*>(rhs)[2 * t] = make_double2(o.rhs[0], o.rhs[1]);
-    reinterpret_cast<double2*>(rhs)[2 * t + 1] = make_double2(o.rhs[2], o.rhs[3]);
+    Lu4 lu;
+    {
+        Local L;
+        local_matrices(p, k, L, dv);  // local_stiffness_mass (assembly.cpp:7-33)
+        if (a_blocks) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) a_blocks[16 * t + 4 * i + j] = L.a[i][j];
+        }
+        lu_factor(L.a, lu, dv);  // local Schur complement (solver.cpp:101-127)
+    }
+    if (lu.singular) return 2;
+    // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
+    // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
+    auto cr = [&](int r, int v) -> double {
+        const bool on = sl.row[r] >= 0 && v != (r == 0 ? 3 : (r == 3 ? 0 : r));
+        return on ? coef[r] : 0.0;
+    };
+    // r_T = C A^-1 B_T; Dirichlet rows get b_D - r_T and b_D (single
+    // contributor), interior rows keep -r_T for the final atomic
+    double nrb[4];
+    {
+        double ainv_b[4];
+        lu_solve(lu, bt, ainv_b, dv);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            nrb[r] = 0.0;
+            if (sl.row[r] < 0) continue;
+            double rb = 0.0;
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
+            const int64_t R = sl.row[r];
+            sell_col[sell_idx(R, 0)] = (int32_t)R;
+            if (sl.bnd[r]) {
+                rhs_neg[R] = sub(bdv[r], rb);
+                bd[R] = bdv[r];
+#pragma unroll
+                for (int pos = 4; pos < 7; ++pos) {
+                    sell_col[sell_idx(R, pos)] = (int32_t)R;
+                    sell_val[sell_idx(R, pos)] = 0.0;
+                }
+            } else {
+                bd[R] = 0.0;
+                nrb[r] = -rb;
+            }
+        }
+    }
+    // one solved column x = A^-1 c_q at a time; S_T[r][q] accumulated over
+    // p = 0..3 exactly as solver.cpp:121-125, stored at once (r != q)
+    double sdiag[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double x[4] = {0.0, 0.0, 0.0, 0.0};
+        const bool real = sl.row[q] >= 0;
+        if (real) {
+            const double cq[4] = {cr(q, 0), cr(q, 1), cr(q, 2), cr(q, 3)};
+            lu_solve(lu, cq, x, dv);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (sl.row[r] < 0) continue;
+            double s = 0.0;
+            if (real) {
+#pragma unroll
+                for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
+            }
+            if (r == q) {
+                sdiag[r] = s;
+                continue;
+            }
+            const int64_t ix = sell_idx(sl.row[r], (sl.owner[r] ? 1 : 4) + (q < r ? q : q - 1));
+            sell_col[ix] = real ? sl.row[q] : sl.row[r];
+            sell_val[ix] = real ? s : 0.0;
+        }
+    }
+    if (!dv.good()) return 1;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         if (sl.row[r] < 0) continue;
         const int64_t R = sl.row[r];
-        const int base = sl.owner[r] ? 0 : 3;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (q == r) {
-                atomicAdd(sell_val + sell_idx(R, 0), o.s[r][r]);
-                sell_col[sell_idx(R, 0)] = (int32_t)R;
-                continue;
-            }
-            const int64_t ix = sell_idx(R, base + 1 + (q < r ? q : q - 1));
-            const bool real = sl.row[q] >= 0;
-            sell_col[ix] = real ? sl.row[q] : (int32_t)R;
-            sell_val[ix] = real ? o.s[r][q] : 0.0;
-        }
-        if (sl.bnd[r]) {
-#pragma unroll
-            for (int pos = 4; pos < 7; ++pos) {
-                sell_col[sell_idx(R, pos)] = (int32_t)R;
-                sell_val[sell_idx(R, pos)] = 0.0;
-            }
-            rhs_neg[R] = sub(o.bdv[r], o.rb[r]);  // b_D - r_T, single contributor
-            bd[R] = o.bdv[r];
-        } else {
-            atomicAdd(rhs_neg + R, -o.rb[r]);
-        }
+        atomicAdd(sell_val + sell_idx(R, 0), sdiag[r]);
+        if (!sl.bnd[r]) atomicAdd(rhs_neg + R, nrb[r]);
     }
+    return 0;
 }
 
-struct ElemIn {
-    V3 p[4];
-    Coef k;
-    Slots sl;
-    double area[4], b[4];
-};
-
-__device__ __forceinline__ void load_elem(int64_t t, const double* __restrict__ coords,
-                                          const int32_t* __restrict__ tets, const phg_problem& prob,
-                                          const int32_t* __restrict__ face_of_slot,
-                                          const int32_t* __restrict__ slot_mate, const int32_t* __restrict__ face_mrow,
-                                          const double* __restrict__ face_area, const double* __restrict__ b_in,
-                                          ElemIn& in) {
-    const int4 e = ldtet(tets, t);
-    in.p[0] = ldnode(coords, e.x);
-    in.p[1] = ldnode(coords, e.y);
-    in.p[2] = ldnode(coords, e.z);
-    in.p[3] = ldnode(coords, e.w);
-    in.k = load_coef(prob, t);
-    load_slots(t, face_of_slot, slot_mate, face_mrow, in.sl);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) in.area[q] = __ldg(face_area + in.sl.face[q]);
-    const double2 r01 = reinterpret_cast<const double2*>(b_in)[2 * t];
-    const double2 r23 = reinterpret_cast<const double2*>(b_in)[2 * t + 1];
-    in.b[0] = r01.x;
-    in.b[1] = r01.y;
-    in.b[2] = r23.x;
-    in.b[3] = r23.y;
-}
-
-__device__ __forceinline__ bool elem_degenerate(const ElemIn& in) {
-    return vdot(vcross(vsub(in.p[1], in.p[0]), vsub(in.p[2], in.p[0])), vsub(in.p[3], in.p[0])) == 0.0;
-}
-
-// Fast pass: straight-line division (FastDiv).  An element whose operands
-// left the exact window is appended to redo_list and not scattered.
-// b_in holds the Gauss load vector from load_k and is overwritten by
-// B_T = b + LN (the input is read before the write, per element).
+// Fast pass: one element per thread, blocks in element order (the elements
+// in flight and the S rows they scatter into stay in an L2-resident window),
+// FastDiv division.  Elements whose operands left the exact window are
+// appended to redo_list.
 template <int KIND>
 __global__ void __launch_bounds__(kCondThreads, 4)
-    condense_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
+    assemble_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
                double* __restrict__ rhs, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
@@ -392,27 +356,20 @@ __global__ void __launch_bounds__(kCondThreads, 4)
                int32_t* __restrict__ redo_count, unsigned long long* err) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= ne) return;
-    ElemIn in;
-    load_elem(t, coords, tets, prob, face_of_slot, slot_mate, face_mrow, face_area, rhs, in);
-    if (elem_degenerate(in)) return;  // reported by load_k (assembly.cpp:13-14)
-    ElemOut o;
     FastDiv fd;
-    condense_compute<KIND>(t, in.p, in.k, in.sl, in.area, in.b, a_blocks, o, fd);
-    if (!fd.ok) {
-        redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
-        return;
-    }
-    if (o.singular) {  // "degenerate element block" (solver.cpp:103-109)
-        report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
-        return;
-    }
-    scatter_elem(t, in.sl, o, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow);
+    const int st = assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area},
+                                       a_blocks, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, fd);
+    if (st == 1) redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
+    // "degenerate element block" (solver.cpp:103-109)
+    if (st == 2) report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
+    // "degenerate element (zero volume)" (assembly.cpp:13-14)
+    if (st == 3) report(err, PHG_ERR_ZERO_VOLUME, (unsigned long long)t);
 }
 
 // Exact pass over the listed elements (IEEE division throughout).
 template <int KIND>
 __global__ void __launch_bounds__(kCondThreads)
-    condense_redo_k(const int32_t* __restrict__ redo_list, const int32_t* __restrict__ redo_count,
+    assemble_redo_k(const int32_t* __restrict__ redo_list, const int32_t* __restrict__ redo_count,
                     const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                     const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                     const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
@@ -422,16 +379,19 @@ __global__ void __launch_bounds__(kCondThreads)
     const int32_t n = *redo_count;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int64_t t = redo_list[i];
-        ElemIn in;
-        load_elem(t, coords, tets, prob, face_of_slot, slot_mate, face_mrow, face_area, rhs, in);
-        ElemOut o;
         ExactDiv ed;
-        condense_compute<KIND>(t, in.p, in.k, in.sl, in.area, in.b, a_blocks, o, ed);
-        if (o.singular) {
+        if (assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area}, a_blocks,
+                                sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, ed) == 2)
             report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
-            continue;
-        }
-        scatter_elem(t, in.sl, o, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow);
+    }
+}
+
+// clear the two-contributor accumulators (S diagonal, rhs_neg) of rows 0..l-1
+__global__ void __launch_bounds__(256) zero_rows_k(int64_t l, double* __restrict__ sell_val,
+                                                   double* __restrict__ rhs_neg) {
+    for (int64_t R = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; R < l; R += (int64_t)gridDim.x * blockDim.x) {
+        sell_val[sell_idx(R, 0)] = 0.0;
+        rhs_neg[R] = 0.0;
     }
 }
 
@@ -514,18 +474,15 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            int32_t* redo, unsigned long long* err, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne == 0) return 0;
-    // one element per thread, blocks in element order: the elements in flight
-    // (and the S rows they scatter into) stay in an L2-resident window
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
     const phg_problem p = *prob;
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
+    zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, sell_val, rhs_neg);
 #define PHG_ASM(K)                                                                                                   \
-    load_k<K><<<grid, kLoadThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, rhs, sell_val,   \
-                                            rhs_neg, bd, err);                                                       \
-    condense_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
+    assemble_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
                                                 rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,          \
                                                 slot_mrow, redo + 1, redo, err);                                    \
-    condense_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
+    assemble_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
                                                      face_mrow, face_area, rhs, sell_col, sell_val, rhs_neg, bd,    \
                                                      a_blocks, slot_coef, slot_mrow, err)
     switch (p.kind) {

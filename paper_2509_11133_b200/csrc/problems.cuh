@@ -116,7 +116,7 @@ __device__ __forceinline__ double prob_f_fast(double x, double y, double z, doub
 // one quadrature point then costs 3 + N FMA per axis.  All derivatives of
 // these g are bounded by 1 (trig) or e^x0 e^|delta| (exp), so the truncation
 // error is below zmax^(N+1)/(N+1)! relative; taylor_order() picks N with that
-// bound under 1e-17 (< ulp(1)/20).  Elements with zmax > 0.25 keep the
+// bound under 1e-17 (< ulp(1)/20).  Elements with zmax > 0.12 keep the
 // direct sinpi/cospi/exp evaluation.
 enum { kTaySin = 0, kTayCos = 1, kTayExp = 2 };
 template <int N>
@@ -125,7 +125,7 @@ struct AxisTaylor {
     double e1, e2, e3;
 };
 __device__ __forceinline__ double inv_fact(int n) {
-    constexpr double f[14] = {1.0,
+    constexpr double f[11] = {1.0,
                               1.0,
                               1.0 / 2.0,
                               1.0 / 6.0,
@@ -135,10 +135,7 @@ __device__ __forceinline__ double inv_fact(int n) {
                               1.0 / 5040.0,
                               1.0 / 40320.0,
                               1.0 / 362880.0,
-                              1.0 / 3628800.0,
-                              1.0 / 39916800.0,
-                              1.0 / 479001600.0,
-                              1.0 / 6227020800.0};
+                              1.0 / 3628800.0};
     return f[n];
 }
 // |z| bound of one axis (pi-scaled; also bounds the exp axis' |delta|)
@@ -147,9 +144,9 @@ __device__ __forceinline__ double axis_zmax(double x0, double x1, double x2, dou
 }
 // 0 = out of range (direct evaluation)
 __device__ __forceinline__ int taylor_order(double zmax) {
-    // 0.028^8/8! = 9.4e-18, 0.05^9/9! = 5.4e-18, 0.12^11/11! = 1.9e-18,
-    // 0.25^14/14! = 4.3e-20
-    return zmax <= 0.028 ? 7 : (zmax <= 0.05 ? 8 : (zmax <= 0.12 ? 10 : (zmax <= 0.25 ? 13 : 0)));
+    // 0.028^8/8! = 9.4e-18, 0.05^9/9! = 5.4e-18, 0.12^11/11! = 1.9e-18;
+    // coarser elements (small meshes) take the direct evaluation
+    return zmax <= 0.028 ? 7 : (zmax <= 0.05 ? 8 : (zmax <= 0.12 ? 10 : 0));
 }
 template <int N, int G>
 __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, double x2, double x3) {
@@ -222,11 +219,13 @@ __device__ __forceinline__ Coef load_coef(const phg_problem& p, int64_t t) {
 // inside the window where that equals IEEE division; when it is not, the
 // caller recomputes the element with ExactDiv.
 struct ExactDiv {
+    __device__ __forceinline__ bool good() const { return true; }
     __device__ __forceinline__ double div(double a, const Div& d) { return dq(a, d); }
     __device__ __forceinline__ Div make(double b) { return make_div(b); }
 };
 struct FastDiv {
     bool ok = true;
+    __device__ __forceinline__ bool good() const { return ok; }
     __device__ __forceinline__ double div(double a, const Div& d) { return dq_fast(a, d, ok); }
     __device__ __forceinline__ Div make(double b) { return make_div_fast(b, ok); }
 };

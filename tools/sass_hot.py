@@ -52,3 +52,13 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def stall_lines(path, name=None, n=25):
+    """Hottest lines with their dominant stall reasons."""
+    k, rows = load(path, name)
+    reasons = [c for c in rows[0] if c.startswith("stall_") and "Not Issued" not in c]
+    for i, r in sorted(enumerate(rows), key=lambda p: -int(p[1]["Warp Stall Sampling (All Samples)"] or 0))[:n]:
+        top = sorted(((int(r[c] or 0), c[6:]) for c in reasons), reverse=True)[:3]
+        print(f"  {i:5d} {r['Source'].strip()[:50]:50s} {r['Warp Stall Sampling (All Samples)']:>6s} "
+              + " ".join(f"{c}={v}" for v, c in top if v))
