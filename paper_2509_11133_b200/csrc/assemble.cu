@@ -185,22 +185,26 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
                                              double* __restrict__ rhs_neg, double* __restrict__ bd,
                                              double* __restrict__ rhs, double* __restrict__ slot_coef,
                                              int32_t* __restrict__ slot_mrow, Dv& dv) {
-    V3 p[4];
-    {
-        const int4 e = ldtet(tets, t);
-        p[0] = ldnode(coords, e.x);
-        p[1] = ldnode(coords, e.y);
-        p[2] = ldnode(coords, e.z);
-        p[3] = ldnode(coords, e.w);
-    }
-    const Coef k = load_coef(prob, t);
     // elem_volume == local.volume (assembly.cpp:18, 47)
     double bt[4];
     {
-        const double det = vdot(vcross(vsub(p[1], p[0]), vsub(p[2], p[0])), vsub(p[3], p[0]));
+        const int4 e = ldtet(tets, t);
+        const V3 p0[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+        const double det = vdot(vcross(vsub(p0[1], p0[0]), vsub(p0[2], p0[0])), vsub(p0[3], p0[0]));
         if (det == 0.0) return 3;
-        load_vector<KIND>(p, k, dq(fabs(det), kDiv6), bt);
+        load_vector<KIND>(p0, load_coef(prob, t), dq(fabs(det), kDiv6), bt);
     }
+    // coordinates and coefficients again (L1/L2 hits) rather than keeping
+    // them live through the load vector's Taylor coefficients
+    V3 p[4];
+    {
+        const int4 e = ld_fresh(reinterpret_cast<const int4*>(tets) + t);
+        p[0] = ldnode_fresh(coords, e.x);
+        p[1] = ldnode_fresh(coords, e.y);
+        p[2] = ldnode_fresh(coords, e.z);
+        p[3] = ldnode_fresh(coords, e.w);
+    }
+    const Coef k = load_coef_fresh(prob, t);
     // the face-side gathers only now, after the fp64-heavy load vector (the
     // other warps of the SM cover their latency)
     Slots sl;

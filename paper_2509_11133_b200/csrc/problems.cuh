@@ -211,6 +211,22 @@ __device__ __forceinline__ Coef load_coef(const phg_problem& p, int64_t t) {
     return k;
 }
 
+// load_coef with loads that are not merged with earlier ones (ld_fresh)
+__device__ __forceinline__ Coef load_coef_fresh(const phg_problem& p, int64_t t) {
+    Coef k;
+    if (p.a_diag) {
+        k.a0 = ld_fresh(p.a_diag + 3 * t);
+        k.a1 = ld_fresh(p.a_diag + 3 * t + 1);
+        k.a2 = ld_fresh(p.a_diag + 3 * t + 2);
+    } else if (p.a_elem) {
+        k.a0 = k.a1 = k.a2 = ld_fresh(p.a_elem + t);
+    } else {
+        k.a0 = k.a1 = k.a2 = 1.0;
+    }
+    k.c = p.c;
+    return k;
+}
+
 // -------------------------------------------------------------- element core
 
 // Division policies of the element core.  ExactDiv gives IEEE quotients
