@@ -100,10 +100,13 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
                           int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
                           void* stream);
 
-/* Per element counts of first-occurrence edges (low 8 bits) and owned faces
- * (next 8 bits): packed[t]. */
-int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
-                             int32_t* edge_count, int32_t* face_count, void* stream);
+/* Exclusive offsets [ne + 1] of the per-element counts of first-occurrence
+ * edges (edge_off) and owned faces (face_off; skipped when slot_mate is
+ * NULL), counted and scanned in one pass.  scratch needs
+ * phfem_gpu_element_offsets_scratch(ne) bytes. */
+size_t phfem_gpu_element_offsets_scratch(int64_t ne);
+int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate, int64_t* edge_off,
+                              int64_t* face_off, void* scratch, void* stream);
 
 /* Numbering from the exclusive offsets: edge ids = rank of the first slot,
  * face ids = rank of the owner slot (the faces_up order).  One thread per

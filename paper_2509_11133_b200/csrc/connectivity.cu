@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace {
 
@@ -405,22 +406,128 @@ __global__ void __launch_bounds__(256)
 
 __device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mate < 0 || mate > s; }
 
-__global__ void element_counts(int64_t ne, const int32_t* __restrict__ edge_first,
-                               const int32_t* __restrict__ slot_mate, int32_t* __restrict__ edge_count,
-                               int32_t* __restrict__ face_count) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
-        if (edge_first) {
-            int c = 0;
-            for (int k = 0; k < 6; ++k) c += edge_first[6 * t + k] == (int32_t)(6 * t + k);
-            edge_count[t] = c;
+// Per-element counts of first-occurrence edges and owned faces and their
+// exclusive offsets edge_off / face_off [ne + 1], reduce-then-scan (scan.cuh):
+//   offsets_count_k  one byte per element (edges | faces << 4) + tile sums,
+//                    both counts packed in one int64 (edges << 31 | faces;
+//                    6 nE < 2^31 is enforced at upload, so no carry)
+//   scan_sums        the tile sums
+//   offsets_scan_k   16 elements per thread from 16 B of count bytes
+__global__ void __launch_bounds__(kScanThreads)
+    offsets_count_k(int64_t ne, const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
+                    uint8_t* __restrict__ cnt8, long long* __restrict__ sums) {
+    const int64_t first = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    long long se = 0, sf = 0;
+    uint32_t packed[kScanItems / 4];
+#pragma unroll
+    for (int c = 0; c < kScanItems / 4; ++c) {
+        // 4 elements: 24 edge slots (6 x int4) and 16 face slots (4 x int4)
+        const int64_t t0 = first + 4 * c;
+        uint32_t word = 0;
+        if (t0 + 4 <= ne) {
+            const int4* ef = reinterpret_cast<const int4*>(edge_first + 6 * t0);
+            int32_t e[24];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const int4 q = __ldg(ef + i);
+                e[4 * i] = q.x;
+                e[4 * i + 1] = q.y;
+                e[4 * i + 2] = q.z;
+                e[4 * i + 3] = q.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                int ce = 0, cf = 0;
+#pragma unroll
+                for (int k = 0; k < 6; ++k) ce += e[6 * j + k] == (int32_t)(6 * (t0 + j) + k);
+                if (slot_mate) {
+                    const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t0 + j);
+                    const int32_t sl = (int32_t)(4 * (t0 + j));
+                    cf = face_owner(sl, m.x) + face_owner(sl + 1, m.y) + face_owner(sl + 2, m.z) +
+                         face_owner(sl + 3, m.w);
+                }
+                se += ce;
+                sf += cf;
+                word |= (uint32_t)(ce | cf << 4) << (8 * j);
+            }
+        } else {
+            for (int j = 0; j < 4; ++j) {
+                const int64_t t = t0 + j;
+                if (t >= ne) continue;
+                int ce = 0, cf = 0;
+                for (int k = 0; k < 6; ++k) ce += edge_first[6 * t + k] == (int32_t)(6 * t + k);
+                if (slot_mate) {
+                    const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+                    const int32_t sl = (int32_t)(4 * t);
+                    cf = face_owner(sl, m.x) + face_owner(sl + 1, m.y) + face_owner(sl + 2, m.z) +
+                         face_owner(sl + 3, m.w);
+                }
+                se += ce;
+                sf += cf;
+                word |= (uint32_t)(ce | cf << 4) << (8 * j);
+            }
         }
-        if (slot_mate) {
-            const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-            const int32_t s = (int32_t)(4 * t);
-            face_count[t] = face_owner(s, m.x) + face_owner(s + 1, m.y) + face_owner(s + 2, m.z) +
-                            face_owner(s + 3, m.w);
-        }
+        packed[c] = word;
     }
+    if (first + kScanItems <= ne) {
+        reinterpret_cast<uint4*>(cnt8 + first)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    } else {
+        for (int i = 0; i < kScanItems; ++i)
+            if (first + i < ne) cnt8[first + i] = (uint8_t)(packed[i / 4] >> (8 * (i % 4)));
+    }
+    const long long s = block_sum_ll<kScanThreads>(se << 31 | sf);
+    if (threadIdx.x == 0) sums[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    offsets_scan_k(int64_t ne, const uint8_t* __restrict__ cnt8, const long long* __restrict__ tile_off,
+                   int64_t* __restrict__ edge_off, int64_t* __restrict__ face_off) {
+    __shared__ long long stage[kScanTile + kScanTile / 16];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    const int64_t first = base + (int64_t)threadIdx.x * kScanItems;
+    uint8_t c[kScanItems];
+    if (first + kScanItems <= ne) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(cnt8 + first));
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) c[i] = (uint8_t)(w[i / 4] >> (8 * (i % 4)));
+    } else {
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) c[i] = first + i < ne ? cnt8[first + i] : 0;
+    }
+    long long se = 0, sf = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        se += c[i] & 15;
+        sf += c[i] >> 4;
+    }
+    const long long packed = block_excl_scan_ll<kScanThreads>(se << 31 | sf) + tile_off[blockIdx.x];
+    long long run = packed >> 31;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
+        run += c[i] & 15;
+    }
+    __syncthreads();
+    store_tile_i64(stage, edge_off, base, ne);
+    if (!face_off) return;
+    __syncthreads();
+    run = packed & 0x7fffffffll;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
+        run += c[i] >> 4;
+    }
+    __syncthreads();
+    store_tile_i64(stage, face_off, base, ne);
+}
+
+// grand totals edge_off[ne], face_off[ne] from the packed total
+__global__ void offsets_total_k(const int64_t* __restrict__ packed_total, int64_t ne, int64_t* __restrict__ edge_off,
+                                int64_t* __restrict__ face_off) {
+    const long long p = *packed_total;
+    edge_off[ne] = p >> 31;
+    if (face_off) face_off[ne] = p & 0x7fffffffll;
 }
 
 // Ids of all slots of one element (one thread per element, blocks in element
@@ -576,28 +683,50 @@ __global__ void face_class_k(int64_t nf, int64_t nd, const uint32_t* __restrict_
                              int32_t* __restrict__ is_row, unsigned long long* __restrict__ counts,
                              unsigned long long* err) {
     int c0 = 0, c1 = 0, c2 = 0;
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t cl = claim[f];
-        const bool boundary = face_slots[2 * f + 1] < 0;
+    auto one = [&](int64_t f, uint32_t cl, int32_t mate) -> uint8_t {
         uint8_t cls = 0;
         if (cl != 0xffffffffu) cls = (int64_t)cl < nd ? 1 : 2;
-        else if (boundary) report(err, PHG_ERR_FACE, (unsigned long long)f << 2 | 1);
-        face_class[f] = cls;
-        is_row[f] = cls != 2;
+        else if (mate < 0) report(err, PHG_ERR_FACE, (unsigned long long)f << 2 | 1);
         c0 += cls == 0;
         c1 += cls == 1;
         c2 += cls == 2;
+        return cls;
+    };
+    // four faces per thread and step: 16 B loads keep enough bytes in flight
+    const int64_t nq = nf / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 cl = __ldg(reinterpret_cast<const uint4*>(claim) + i);
+        const int4 s01 = __ldg(reinterpret_cast<const int4*>(face_slots) + 2 * i);
+        const int4 s23 = __ldg(reinterpret_cast<const int4*>(face_slots) + 2 * i + 1);
+        const int64_t f = 4 * i;
+        const uint8_t a = one(f, cl.x, s01.y), b = one(f + 1, cl.y, s01.w), c = one(f + 2, cl.z, s23.y),
+                      d = one(f + 3, cl.w, s23.w);
+        reinterpret_cast<uchar4*>(face_class)[i] = make_uchar4(a, b, c, d);
+        reinterpret_cast<int4*>(is_row)[i] = make_int4(a != 2, b != 2, c != 2, d != 2);
+    }
+    for (int64_t f = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf;
+         f += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t cls = one(f, claim[f], face_slots[2 * f + 1]);
+        face_class[f] = cls;
+        is_row[f] = cls != 2;
     }
     for (int o = 16; o > 0; o >>= 1) {
         c0 += __shfl_xor_sync(0xffffffffu, c0, o);
         c1 += __shfl_xor_sync(0xffffffffu, c1, o);
         c2 += __shfl_xor_sync(0xffffffffu, c2, o);
     }
+    // one atomic triple per block: per-warp atomics on the same three words
+    // serialise in L2 (~170 us at 25M faces)
+    __shared__ int sc[3];
+    if (threadIdx.x < 3) sc[threadIdx.x] = 0;
+    __syncthreads();
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(counts + 0, (unsigned long long)c0);
-        atomicAdd(counts + 1, (unsigned long long)c1);
-        atomicAdd(counts + 2, (unsigned long long)c2);
+        atomicAdd(sc + 0, c0);
+        atomicAdd(sc + 1, c1);
+        atomicAdd(sc + 2, c2);
     }
+    __syncthreads();
+    if (threadIdx.x < 3) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
 }
 
 __global__ void face_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, const int64_t* __restrict__ row_off,
@@ -662,10 +791,28 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     return (int)cudaGetLastError();
 }
 
-extern "C" int phfem_gpu_element_counts(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
-                                        int32_t* edge_count, int32_t* face_count, void* stream) {
-    element_counts<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, edge_first, slot_mate, edge_count,
-                                                                        face_count); phg::count_launches(1);
+extern "C" size_t phfem_gpu_element_offsets_scratch(int64_t ne) {
+    // tile sums + packed total, then one count byte per element
+    return (size_t)((scan_tiles(ne) + 3) / 2 * 2) * sizeof(long long) + (size_t)((ne + 15) / 16 * 16);
+}
+
+extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
+                                         int64_t* edge_off, int64_t* face_off, void* scratch, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ne <= 0) {
+        cudaMemsetAsync(edge_off, 0, sizeof(int64_t), s);
+        if (slot_mate) cudaMemsetAsync(face_off, 0, sizeof(int64_t), s);
+        return (int)cudaGetLastError();
+    }
+    const int64_t ntiles = scan_tiles(ne);
+    long long* sums = static_cast<long long*>(scratch);
+    int64_t* total = reinterpret_cast<int64_t*>(sums + ntiles);
+    uint8_t* cnt8 = reinterpret_cast<uint8_t*>(sums + (ntiles + 3) / 2 * 2);  // 16 B aligned
+    offsets_count_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, edge_first, slot_mate, cnt8, sums);
+    scan_sums(sums, ntiles, total, s);
+    offsets_scan_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, cnt8, sums, edge_off, slot_mate ? face_off : nullptr);
+    offsets_total_k<<<1, 1, 0, s>>>(total, ne, edge_off, slot_mate ? face_off : nullptr);
+    phg::count_launches(4);
     return (int)cudaGetLastError();
 }
 

@@ -85,7 +85,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     Timer tm;
     const auto w0 = std::chrono::steady_clock::now();
     reset_err(w);
-    w.scratch.alloc((int64_t)phfem_gpu_scan_scratch(std::max<int64_t>({nc, ne, 4 * ne})));
+    w.scratch.alloc((int64_t)std::max(phfem_gpu_scan_scratch(std::max<int64_t>({nc, ne, 4 * ne})),
+                                      phfem_gpu_element_offsets_scratch(ne)));
     // 1. vertex star (CSR by vertex)
     tm.start();
     w.cnt.alloc(nc);
@@ -109,17 +110,13 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
           "star groups");
     if (st) st->groups += tm.stop_ms();
     // 3. numbering: per-element counts, scans, ids, remaining slots
-    w.ecount.alloc(ne);
-    if (faces) w.fcount.alloc(ne);
     tm.start();
     c.edge_off.alloc(ne + 1);
     if (faces) w.face_off.alloc(ne + 1);
-    check(phfem_gpu_element_counts(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.ecount.p,
-                                   faces ? w.fcount.p : nullptr, SV()),
-          "element counts");
-    check(phfem_gpu_scan_i32(w.ecount.p, c.edge_off.p, ne, w.scratch.p, SV()), "edge scan");
+    check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, c.edge_off.p,
+                                    faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
+          "element offsets");
     if (faces) {
-        check(phfem_gpu_scan_i32(w.fcount.p, w.face_off.p, ne, w.scratch.p, SV()), "face scan");
         const auto tot = read_many<int64_t, 2>({c.edge_off.p + ne, w.face_off.p + ne});
         c.ned = tot[0];
         c.nf = tot[1];

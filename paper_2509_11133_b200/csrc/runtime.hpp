@@ -143,7 +143,7 @@ struct Coefs {
 // transient device buffers of one connectivity / refinement / assembly pass,
 // kept with their owner so repeated passes reuse them
 struct Work {
-    DBuf<int32_t> cnt, ecount, fcount, is_row, big_list, big_count, packed, redo;
+    DBuf<int32_t> cnt, is_row, big_list, big_count, packed, redo;
     DBuf<int64_t> cursor, face_off, row_off;
     DBuf<unsigned char> scratch;
     DBuf<uint32_t> claim;
