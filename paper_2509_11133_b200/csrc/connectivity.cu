@@ -406,24 +406,40 @@ __global__ void __launch_bounds__(256)
 
 __device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mate < 0 || mate > s; }
 
-// Per-element counts of first-occurrence edges and owned faces and their
-// exclusive offsets edge_off / face_off [ne + 1], reduce-then-scan (scan.cuh):
-//   offsets_count_k  one byte per element (edges | faces << 4) + tile sums,
-//                    both counts packed in one int64 (edges << 31 | faces;
-//                    6 nE < 2^31 is enforced at upload, so no carry)
+// Per-element masks of first-occurrence edge slots (bits 0-5) and owned face
+// slots (bits 6-9) and the exclusive offsets edge_off / face_off [ne + 1] of
+// their popcounts, reduce-then-scan (scan.cuh):
+//   offsets_count_k  masks + tile sums, both counts packed in one int64
+//                    (edges << 31 | faces; 6 nE < 2^31 is enforced at
+//                    upload, so no carry)
 //   scan_sums        the tile sums
-//   offsets_scan_k   16 elements per thread from 16 B of count bytes
+//   offsets_scan_k   16 elements per thread from 32 B of masks
+// number() ranks non-first slots in their group's first element with the
+// same masks (one 2-byte gather instead of re-reading edge_first).
+__device__ __forceinline__ uint32_t elem_mask(int64_t t, const int32_t* e6, const int4* mate) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m |= (uint32_t)(e6[k] == (int32_t)(6 * t + k)) << k;
+    if (mate) {
+        const int4 q = *mate;
+        const int32_t sl = (int32_t)(4 * t);
+        m |= (uint32_t)face_owner(sl, q.x) << 6 | (uint32_t)face_owner(sl + 1, q.y) << 7 |
+             (uint32_t)face_owner(sl + 2, q.z) << 8 | (uint32_t)face_owner(sl + 3, q.w) << 9;
+    }
+    return m;
+}
+
 __global__ void __launch_bounds__(kScanThreads)
     offsets_count_k(int64_t ne, const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
-                    uint8_t* __restrict__ cnt8, long long* __restrict__ sums) {
+                    uint16_t* __restrict__ masks, long long* __restrict__ sums) {
     const int64_t first = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
     long long se = 0, sf = 0;
-    uint32_t packed[kScanItems / 4];
+    uint32_t packed[kScanItems / 2];
 #pragma unroll
     for (int c = 0; c < kScanItems / 4; ++c) {
         // 4 elements: 24 edge slots (6 x int4) and 16 face slots (4 x int4)
         const int64_t t0 = first + 4 * c;
-        uint32_t word = 0;
+        uint32_t m[4] = {0, 0, 0, 0};
         if (t0 + 4 <= ne) {
             const int4* ef = reinterpret_cast<const int4*>(edge_first + 6 * t0);
             int32_t e[24];
@@ -437,76 +453,78 @@ __global__ void __launch_bounds__(kScanThreads)
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                int ce = 0, cf = 0;
-#pragma unroll
-                for (int k = 0; k < 6; ++k) ce += e[6 * j + k] == (int32_t)(6 * (t0 + j) + k);
-                if (slot_mate) {
-                    const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t0 + j);
-                    const int32_t sl = (int32_t)(4 * (t0 + j));
-                    cf = face_owner(sl, m.x) + face_owner(sl + 1, m.y) + face_owner(sl + 2, m.z) +
-                         face_owner(sl + 3, m.w);
-                }
-                se += ce;
-                sf += cf;
-                word |= (uint32_t)(ce | cf << 4) << (8 * j);
+                int4 q;
+                if (slot_mate) q = __ldg(reinterpret_cast<const int4*>(slot_mate) + t0 + j);
+                m[j] = elem_mask(t0 + j, e + 6 * j, slot_mate ? &q : nullptr);
             }
         } else {
             for (int j = 0; j < 4; ++j) {
                 const int64_t t = t0 + j;
                 if (t >= ne) continue;
-                int ce = 0, cf = 0;
-                for (int k = 0; k < 6; ++k) ce += edge_first[6 * t + k] == (int32_t)(6 * t + k);
-                if (slot_mate) {
-                    const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-                    const int32_t sl = (int32_t)(4 * t);
-                    cf = face_owner(sl, m.x) + face_owner(sl + 1, m.y) + face_owner(sl + 2, m.z) +
-                         face_owner(sl + 3, m.w);
-                }
-                se += ce;
-                sf += cf;
-                word |= (uint32_t)(ce | cf << 4) << (8 * j);
+                int32_t e[6];
+                for (int k = 0; k < 6; ++k) e[k] = edge_first[6 * t + k];
+                int4 q;
+                if (slot_mate) q = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+                m[j] = elem_mask(t, e, slot_mate ? &q : nullptr);
             }
         }
-        packed[c] = word;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            se += __popc(m[j] & 63u);
+            sf += __popc(m[j] >> 6);
+        }
+        packed[2 * c] = m[0] | m[1] << 16;
+        packed[2 * c + 1] = m[2] | m[3] << 16;
     }
     if (first + kScanItems <= ne) {
-        reinterpret_cast<uint4*>(cnt8 + first)[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        uint4* o = reinterpret_cast<uint4*>(masks + first);
+        o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
     } else {
         for (int i = 0; i < kScanItems; ++i)
-            if (first + i < ne) cnt8[first + i] = (uint8_t)(packed[i / 4] >> (8 * (i % 4)));
+            if (first + i < ne) masks[first + i] = (uint16_t)(packed[i / 2] >> (16 * (i % 2)));
     }
     const long long s = block_sum_ll<kScanThreads>(se << 31 | sf);
     if (threadIdx.x == 0) sums[blockIdx.x] = s;
 }
 
 __global__ void __launch_bounds__(kScanThreads)
-    offsets_scan_k(int64_t ne, const uint8_t* __restrict__ cnt8, const long long* __restrict__ tile_off,
+    offsets_scan_k(int64_t ne, const uint16_t* __restrict__ masks, const long long* __restrict__ tile_off,
                    int64_t* __restrict__ edge_off, int64_t* __restrict__ face_off) {
     __shared__ long long stage[kScanTile + kScanTile / 16];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     const int64_t first = base + (int64_t)threadIdx.x * kScanItems;
-    uint8_t c[kScanItems];
+    uint8_t ce[kScanItems], cf[kScanItems];
     if (first + kScanItems <= ne) {
-        const uint4 q = __ldg(reinterpret_cast<const uint4*>(cnt8 + first));
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        const uint4* p = reinterpret_cast<const uint4*>(masks + first);
+        const uint4 q0 = __ldg(p), q1 = __ldg(p + 1);
+        const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-        for (int i = 0; i < kScanItems; ++i) c[i] = (uint8_t)(w[i / 4] >> (8 * (i % 4)));
+        for (int i = 0; i < kScanItems; ++i) {
+            const uint32_t m = (w[i / 2] >> (16 * (i % 2))) & 0xffffu;
+            ce[i] = (uint8_t)__popc(m & 63u);
+            cf[i] = (uint8_t)__popc(m >> 6);
+        }
     } else {
 #pragma unroll
-        for (int i = 0; i < kScanItems; ++i) c[i] = first + i < ne ? cnt8[first + i] : 0;
+        for (int i = 0; i < kScanItems; ++i) {
+            const uint32_t m = first + i < ne ? masks[first + i] : 0u;
+            ce[i] = (uint8_t)__popc(m & 63u);
+            cf[i] = (uint8_t)__popc(m >> 6);
+        }
     }
     long long se = 0, sf = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        se += c[i] & 15;
-        sf += c[i] >> 4;
+        se += ce[i];
+        sf += cf[i];
     }
     const long long packed = block_excl_scan_ll<kScanThreads>(se << 31 | sf) + tile_off[blockIdx.x];
     long long run = packed >> 31;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
-        run += c[i] & 15;
+        run += ce[i];
     }
     __syncthreads();
     store_tile_i64(stage, edge_off, base, ne);
@@ -516,7 +534,7 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
-        run += c[i] >> 4;
+        run += cf[i];
     }
     __syncthreads();
     store_tile_i64(stage, face_off, base, ne);
@@ -538,7 +556,7 @@ __global__ void offsets_total_k(const int64_t* __restrict__ packed_total, int64_
 __global__ void __launch_bounds__(256)
     number(int64_t ne, const int32_t* __restrict__ tets, const double* __restrict__ coords,
            const int32_t* __restrict__ edge_first, const int64_t* __restrict__ edge_off,
-           int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
+           const uint16_t* __restrict__ masks, int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
            const int32_t* __restrict__ slot_mate, const int64_t* __restrict__ face_off,
            int32_t* __restrict__ face_of_slot, int8_t* __restrict__ sigma, int32_t* __restrict__ faces,
            int32_t* __restrict__ face_slots, double* __restrict__ face_area, unsigned long long* err) {
@@ -565,9 +583,8 @@ __global__ void __launch_bounds__(256)
             } else {
                 // rank of slot f among the first-occurrence slots of its element
                 const int64_t g = f / 6;
-                int r = 0;
-                for (int j = 0; j < f - 6 * g; ++j) r += __ldg(edge_first + 6 * g + j) == (int32_t)(6 * g + j);
-                ids[k] = (int32_t)(__ldg(edge_off + g) + r);
+                const uint32_t below = (1u << (f - 6 * g)) - 1u;
+                ids[k] = (int32_t)(__ldg(edge_off + g) + __popc(__ldg(masks + g) & below));
             }
         }
         int2* eo = reinterpret_cast<int2*>(edge_of_slot) + 3 * t;
@@ -604,12 +621,8 @@ __global__ void __launch_bounds__(256)
                 // among g's owned slots (sigma = -1: opposite orientation,
                 // checked in star_groups)
                 const int64_t g = mate >> 2;
-                const int4 mg = __ldg(reinterpret_cast<const int4*>(slot_mate) + g);
-                int r = 0;
-#pragma unroll
-                for (int j = 0; j < 3; ++j)
-                    if (j < (mate & 3)) r += face_owner((int32_t)(4 * g + j), tv(mg, j));
-                fid[k] = (int32_t)(__ldg(face_off + g) + r);
+                const uint32_t below = (1u << (mate & 3)) - 1u;
+                fid[k] = (int32_t)(__ldg(face_off + g) + __popc((__ldg(masks + g) >> 6) & below));
                 sg[k] = -1;
             }
         }
@@ -792,12 +805,13 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
 }
 
 extern "C" size_t phfem_gpu_element_offsets_scratch(int64_t ne) {
-    // tile sums + packed total, then one count byte per element
-    return (size_t)((scan_tiles(ne) + 3) / 2 * 2) * sizeof(long long) + (size_t)((ne + 15) / 16 * 16);
+    // tile sums + packed total
+    return (size_t)(scan_tiles(ne) + 2) * sizeof(long long);
 }
 
 extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate,
-                                         int64_t* edge_off, int64_t* face_off, void* scratch, void* stream) {
+                                         uint16_t* masks, int64_t* edge_off, int64_t* face_off, void* scratch,
+                                         void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne <= 0) {
         cudaMemsetAsync(edge_off, 0, sizeof(int64_t), s);
@@ -807,23 +821,23 @@ extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, 
     const int64_t ntiles = scan_tiles(ne);
     long long* sums = static_cast<long long*>(scratch);
     int64_t* total = reinterpret_cast<int64_t*>(sums + ntiles);
-    uint8_t* cnt8 = reinterpret_cast<uint8_t*>(sums + (ntiles + 3) / 2 * 2);  // 16 B aligned
-    offsets_count_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, edge_first, slot_mate, cnt8, sums);
+    offsets_count_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, edge_first, slot_mate, masks, sums);
     scan_sums(sums, ntiles, total, s);
-    offsets_scan_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, cnt8, sums, edge_off, slot_mate ? face_off : nullptr);
+    offsets_scan_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, masks, sums, edge_off, slot_mate ? face_off : nullptr);
     offsets_total_k<<<1, 1, 0, s>>>(total, ne, edge_off, slot_mate ? face_off : nullptr);
     phg::count_launches(4);
     return (int)cudaGetLastError();
 }
 
 extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords, const int32_t* edge_first,
-                                const int64_t* edge_off, int32_t* edge_of_slot, int32_t* edge_nodes,
+                                const int64_t* edge_off, const uint16_t* masks, int32_t* edge_of_slot,
+                                int32_t* edge_nodes,
                                 const int32_t* slot_mate, const int64_t* face_off, int32_t* face_of_slot,
                                 int8_t* sigma, int32_t* faces, int32_t* face_slots, double* face_area,
                                 unsigned long long* err, void* stream) {
     if (ne == 0) return 0;
     number<<<(unsigned)((ne + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        ne, tets, coords, edge_first, edge_off, edge_of_slot, edge_nodes, slot_mate, face_off, face_of_slot, sigma,
+        ne, tets, coords, edge_first, edge_off, masks, edge_of_slot, edge_nodes, slot_mate, face_off, face_of_slot, sigma,
         faces, face_slots, face_area, err);
     phg::count_launches(1);
     return (int)cudaGetLastError();

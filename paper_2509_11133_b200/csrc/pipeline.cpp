@@ -113,7 +113,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     tm.start();
     c.edge_off.alloc(ne + 1);
     if (faces) w.face_off.alloc(ne + 1);
-    check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, c.edge_off.p,
+    w.masks.alloc(ne + 8);
+    check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p, c.edge_off.p,
                                     faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
           "element offsets");
     if (faces) {
@@ -132,7 +133,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
         c.face_slots.alloc(2 * c.nf);
         c.face_area.alloc(c.nf);
     }
-    check(phfem_gpu_number(ne, m.tets.p, m.coords.p, c.edge_first.p, c.edge_off.p, c.edge_of_slot.p, c.edge_nodes.p,
+    check(phfem_gpu_number(ne, m.tets.p, m.coords.p, c.edge_first.p, c.edge_off.p, w.masks.p, c.edge_of_slot.p,
+                           c.edge_nodes.p,
                            faces ? c.slot_mate.p : nullptr, faces ? w.face_off.p : nullptr,
                            faces ? c.face_of_slot.p : nullptr, faces ? c.sigma.p : nullptr,
                            faces ? c.faces.p : nullptr, faces ? c.face_slots.p : nullptr,

@@ -148,6 +148,7 @@ struct Work {
     DBuf<unsigned char> scratch;
     DBuf<uint32_t> claim;
     DBuf<unsigned long long> counts, err;
+    DBuf<uint16_t> masks;
     DBuf<double> partials, norms;
 };
 
