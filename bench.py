@@ -26,7 +26,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -51,56 +50,86 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clocks + throttle reasons during the timed region: NVML polled
+    every 2 ms from a thread (a sample on entry and one on exit, so even a
+    short region is covered), nvidia-smi as the fallback."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.rows = []  # (sm_mhz, max_mhz, reason_bits)
+        self.stop = threading.Event()
+        self.nv = None
+        self.h = None
+
+    def _handle(self):
+        import pynvml as nv
+        import torch
+
+        nv.nvmlInit()
+        self.nv = nv
+        try:
+            p = torch.cuda.get_device_properties(self.index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _sample(self):
+        nv = self.nv
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                          nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM), int(r)))
+
+    def _loop(self):
+        while not self.stop.wait(0.002):
+            self._sample()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self._handle()
+            self._sample()
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self.nv is not None:
+            self.stop.set()
+            self.t.join(timeout=2)
             try:
-                self.proc.wait(timeout=5)
+                self._sample()
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        reasons = sorted({n for _, _, r in self.rows for n, bit in self.BITS.items() if r & bit})
+        return {"sm_mhz": statistics.median(x[0] for x in self.rows), "sm_max_mhz": max(x[1] for x in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml"}
 
 
 # ---------------------------------------------------- algorithmic bytes
+
+
+def ncu_facts():
+    """Per-kernel facts extracted from the committed ncu --set full captures
+    (tools/ncu_to_json.py -> profiles/ncu_kernels.json)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_kernels.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
 def algorithmic_bytes(nc, ne, ned, nf, nb, nnz_s, l, k_coef=0):
@@ -280,6 +309,23 @@ def main():
     roofline = {"bound": "hbm", "achieved": dom["gbs"], "peak": hbm, "unit": "GB/s", "frac": dom["gbs"] / hbm,
                 "traffic": None, "kernel": dom_name, "peak_kind": hbm_kind,
                 "step_achieved": total_bytes / (ms / 1e3) / 1e9, "step_frac": total_bytes / (ms / 1e3) / 1e9 / hbm}
+    kern_ms = stage_ms.get("assemble_kernel", 0.0)
+    if dom_name == "assemble_condense" and kern_ms > 0:
+        # the fused assembly kernel alone, timed live with CUDA events on the
+        # library stream; its algorithmic bytes are the assembly stage's
+        # (the zero / norm kernels around it move no algorithmic data)
+        kname = f"assemble_k<{cfg.problem}>"
+        achieved = B["assemble"] / (kern_ms / 1e3) / 1e9
+        roofline.update({"kernel": kname, "achieved": achieved, "frac": achieved / hbm, "kernel_ms": kern_ms,
+                         "algorithmic_bytes": B["assemble"]})
+        prof = ncu_facts().get(kname)
+        if prof:
+            # per-launch DRAM bytes and the real limiter from the committed
+            # ncu --set full capture of the same command (profiles/)
+            roofline["traffic"] = prof["dram_bytes"]
+            roofline["limiter"] = (f"fp64 pipe {prof['fp64_pipe_frac']:.0%} busy (ncu "
+                                   f"sm__pipe_fp64_cycles_active); HBM is not the bound")
+            roofline["profile"] = prof["source"]
 
     # e2e through the public C ABI: pinned host arrays -> device mesh ->
     # pipeline -> counts back

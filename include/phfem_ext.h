@@ -108,6 +108,7 @@ typedef struct phfem_stage_ms {
     double assemble;  /* fused assembly + condensation */
     double refine;    /* red refinement (children + nodes + boundary) */
     double total;
+    double assemble_kernel; /* the fused assembly kernel alone (roofline) */
 } phfem_stage_ms;
 
 /* One full pass on a device-resident mesh: connectivity (edges + faces),

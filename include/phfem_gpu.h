@@ -174,14 +174,16 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * norms [2] (device) receive sum(rhs^2), sum(bd^2) over the l face rows,
  * reduced deterministically through partials[2 * grid].  redo [ne + 1] is
  * scratch: the count and list of elements whose operands leave the
- * reciprocal-division window and are recomputed with IEEE division. */
+ * reciprocal-division window and are recomputed with IEEE division.
+ * ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the main kernel. */
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
                                 const double* face_area, int32_t* sell_col, double* sell_val,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, double* norms,
-                                double* partials, int32_t* redo, unsigned long long* err, void* stream);
+                                double* partials, int32_t* redo, unsigned long long* err, void* ev_begin,
+                                void* ev_end, void* stream);
 int phfem_gpu_assemble_grid(int64_t ne);
 
 /* --------------------------------------------------------------- solver */

@@ -475,7 +475,8 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            const double* face_area, int32_t* sell_col, double* sell_val,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
-                                           int32_t* redo, unsigned long long* err, void* stream) {
+                                           int32_t* redo, unsigned long long* err, void* ev_begin, void* ev_end,
+                                           void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne == 0) return 0;
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
@@ -483,9 +484,11 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
     zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, sell_val, rhs_neg);
 #define PHG_ASM(K)                                                                                                   \
+    if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);                                                         \
     assemble_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
                                                 rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,          \
                                                 slot_mrow, redo + 1, redo, err);                                    \
+    if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);                                                             \
     assemble_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
                                                      face_mrow, face_area, rhs, sell_col, sell_val, rhs_neg, bd,    \
                                                      a_blocks, slot_coef, slot_mrow, err)

@@ -837,6 +837,7 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
             ms->assemble = st.assemble;
             ms->refine = st.refine;
             ms->total = tot;
+            ms->assemble_kernel = st.assemble_kernel;
         }
         if (counts) {
             counts[0] = c->ned;

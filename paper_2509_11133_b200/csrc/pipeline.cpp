@@ -284,14 +284,21 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     w.redo.alloc(m.ne + 1);
     reset_err(w);
     const phg_problem p = device_problem(k, problem);
+    Timer tk;  // the main kernel alone
     check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
                                       c.face_mrow.p, c.face_area.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,
-                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p, w.err.p, SV()),
+                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p,
+                                      w.err.p, st ? tk.a : nullptr, st ? tk.b : nullptr, SV()),
           "assemble");
     const double ms = tm.stop_ms();
-    if (st) st->assemble += ms;
+    if (st) {
+        st->assemble += ms;
+        float kms = 0.f;
+        check(cudaEventElapsedTime(&kms, tk.a, tk.b), "event time");
+        st->assemble_kernel += kms;
+    }
     const auto nv = read_many<double, 2>({w.norms.p, w.norms.p + 1});
     sys.sum_rhs2 = nv[0];
     sys.sum_bd2 = nv[1];

@@ -192,6 +192,7 @@ struct RefineMap {
 
 struct Stages {
     double star = 0, groups = 0, number = 0, classify = 0, assemble = 0, refine = 0;
+    double assemble_kernel = 0;  // assemble_k alone
 };
 
 // --------------------------------------------------------------- pipeline

@@ -61,7 +61,8 @@ class RefineTimes(C.Structure):
 
 
 class StageMs(C.Structure):
-    _fields_ = [(n, C.c_double) for n in ("star", "groups", "number", "classify", "assemble", "refine", "total")]
+    _fields_ = [(n, C.c_double) for n in ("star", "groups", "number", "classify", "assemble", "refine", "total",
+                                          "assemble_kernel")]
 
 
 _lib = None

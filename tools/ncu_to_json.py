@@ -1,0 +1,80 @@
+"""Extract per-kernel facts from ncu --set full captures into
+profiles/ncu_kernels.json (read by bench.py for roofline.traffic).
+
+usage: python tools/ncu_to_json.py OUT.json REP.ncu-rep[=profiles/summary.txt] ...
+Each kernel keeps its first launch in the capture; names are shortened to
+`name<T>` (namespace and argument list dropped).
+"""
+import csv
+import json
+import re
+import subprocess
+import sys
+
+METRICS = {
+    "gpu__time_duration.sum": "time",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active",
+    "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput",
+    "launch__registers_per_thread": "registers",
+}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
+         "s": 1, "%": 0.01}
+
+
+def short(name):
+    name = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "")
+    name = re.sub(r"\(int\)", "", name)
+    return name.split("(")[0]
+
+
+def facts(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True)
+    rows = list(csv.reader(out.stdout.splitlines()))
+    head, units = rows[0], rows[1]
+    res = {}
+    for r in rows[2:]:
+        d = dict(zip(head, r))
+        k = short(d["Kernel Name"])
+        if k in res:
+            continue
+        v = {}
+        for m, key in METRICS.items():
+            if m in d and d[m] not in ("", "n/a"):
+                u = units[head.index(m)]
+                v[key] = float(d[m].replace(",", "")) * SCALE.get(u, 1)
+        res[k] = {
+            "dram_bytes": v.get("dram_read", 0) + v.get("dram_write", 0),
+            "dram_read": v.get("dram_read"),
+            "dram_write": v.get("dram_write"),
+            "time_s": v.get("time"),
+            "fp64_pipe_frac": v.get("fp64_pipe"),
+            "warps_active_frac": v.get("warps_active"),
+            "mem_throughput_frac": v.get("mem_throughput"),
+            "registers": v.get("registers"),
+        }
+    return res
+
+
+def main():
+    out = sys.argv[1]
+    try:
+        with open(out) as f:
+            data = json.load(f)
+    except (OSError, ValueError):
+        data = {}
+    for arg in sys.argv[2:]:
+        rep, _, src = arg.partition("=")
+        for k, v in facts(rep).items():
+            v["source"] = src or rep
+            data[k] = v
+    with open(out, "w") as f:
+        json.dump(data, f, indent=1, sort_keys=True)
+        f.write("\n")
+
+
+if __name__ == "__main__":
+    main()
