@@ -209,26 +209,27 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
 
 constexpr int kFastWarps = 4;
 
-// For local vertex lv: its i-th neighbour w (i < 3, ascending) and the
-// i-th face k containing lv with the local vertices x, y following lv in the
-// face's oriented cycle [abc],[acd],[adb],[dcb].  Packed 4-bit fields.
-__device__ __forceinline__ int nbr_of(int lv, int i) { return i + (i >= lv); }
-__device__ __forceinline__ void face_of(int lv, int i, int& k, int& xi, int& yi) {
-    // rows: lv; entries (k, x, y) for i = 0, 1, 2, 12 bits each
-    const unsigned long long row = lv == 0   ? 0x231123012ull
-                                   : lv == 1 ? 0x332203020ull
-                                   : lv == 2 ? 0x313130001ull
-                                             : 0x321210102ull;
-    const unsigned e = (unsigned)(row >> (12 * i)) & 0xfffu;
-    k = (int)(e >> 8);
-    xi = (int)((e >> 4) & 0xf);
-    yi = (int)(e & 0xf);
-}
+// Local tables of the candidate generation in star_groups_warp, per local
+// vertex lv of an incidence (faces [abc],[acd],[adb],[dcb]):
+//   neighbour i (i < 3) = the i-th other local vertex in ascending order;
+//   edge ids  0xb15663088 >> 9 lv, 3 bits per i: local edge (lv, neighbour i)
+//             in the (0,1)(0,2)(0,3)(1,2)(1,3)(2,3) order;
+//   faces     6 bits per i: local face k (bits 0-1) containing lv and the
+//             neighbour positions of x (bits 2-3) and y (bits 4-5), the
+//             vertices following lv in that face's oriented cycle:
+//             lv 0: 0xa950, 1: 0x1b884, 2: 0x27250, 3: 0x1b1a1.
 
-// E entries per lane: E = 1 handles stars of <= 32 incidences (all Kuhn
+// E incidences per lane: E = 1 handles stars of <= 32 incidences (all Kuhn
 // vertices), E = 2 those of <= 64 (refined meshes reach 36).  Vertices come
 // from `list` (or 0..n-1) with n = *count (or nv); larger stars are appended
 // to defer_list for the next pass.  No host round trip between passes.
+//
+// Work compaction: of the 6 candidates per incidence (3 edges, 3 faces) only
+// those whose other vertices are all above v belong to v (about 60 of 144
+// for a Kuhn vertex).  They are first appended to per-warp lists in shared
+// memory (ballot + popc positions), and the hash inserts / read-backs /
+// resets then run over the lists with all 32 lanes busy: 2-3 rounds per
+// vertex instead of 6 mostly idle ones.
 template <int E>
 __global__ void __launch_bounds__(32 * kFastWarps)
     star_groups_warp(int64_t nv, const int32_t* __restrict__ list, const int32_t* __restrict__ count,
@@ -236,25 +237,29 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                      const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
                      int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
                      int32_t* __restrict__ defer_count, unsigned long long* err) {
-    constexpr int CAP = E == 1 ? 128 : 256;  // > 3 * 32 E candidates
-    constexpr int LOG = E == 1 ? 7 : 8;
+    constexpr int CAP = 128 * E;  // > 3 * 32 E keys (load factor < 3/4)
     constexpr unsigned mask = CAP - 1;
-    // Faces are keyed by the edge-table slots of their two upper vertices
-    // (both > v, so both are keys of v's edge table): a 2 LOG-bit key.
+    constexpr int LCAP = 96 * E;  // list entries: 3 candidates per incidence
+    constexpr int R = 3 * E;      // rounds of 32 over a full list
     __shared__ int32_t s_ekey[kFastWarps][CAP], s_eval[kFastWarps][CAP];
-    __shared__ int32_t s_fkey[kFastWarps][CAP];
+    __shared__ unsigned long long s_fkey[kFastWarps][CAP];
     __shared__ int32_t s_flo[kFastWarps][CAP], s_fhi[kFastWarps][CAP], s_fcnt[kFastWarps][CAP];
+    __shared__ int2 s_el[kFastWarps][LCAP];  // (b, edge slot)
+    __shared__ int4 s_fl[kFastWarps][LCAP];  // (lo, hi, face slot, count increment)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
     int32_t* ekey = s_ekey[warp];
     int32_t* eval = s_eval[warp];
-    int32_t* fkey = s_fkey[warp];
+    unsigned long long* fkey = s_fkey[warp];
     int32_t* flo = s_flo[warp];
     int32_t* fhi = s_fhi[warp];
     int32_t* fcnt = s_fcnt[warp];
+    int2* el = s_el[warp];
+    int4* fl = s_fl[warp];
     for (int i = lane; i < CAP; i += 32) {
         ekey[i] = -1;
         eval[i] = INT_MAX;
-        fkey[i] = -1;
+        fkey[i] = ~0ull;
         flo[i] = INT_MAX;
         fhi[i] = -1;
         fcnt[i] = 0;
@@ -271,96 +276,119 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             if (lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
             continue;
         }
-        int eh[E][3], fh[E][3];
-        int32_t eslot[E][3], fslot[E][3];
+        // 1. candidates of v -> lists
+        int ne_l = 0, nf_l = 0;
 #pragma unroll
         for (int u = 0; u < E; ++u) {
-#pragma unroll
-            for (int i = 0; i < 3; ++i) eh[u][i] = fh[u][i] = -1;
             const int e = lane + 32 * u;
-            if (e >= m) continue;
-            const int32_t inc = __ldg(star + beg + e);
-            const int64_t t = inc >> 2;
-            const int lv = inc & 3;
-            const int4 tet = ldtet(tets, t);
-            // table slot + 1 of each local vertex above v (0 otherwise),
-            // 16-bit fields (no local-memory array)
-            unsigned long long hv = 0;
+            const bool valid = e < m;
+            int32_t t = 0;
+            int lv = 0;
+            int4 tet = make_int4(0, 0, 0, 0);
+            if (valid) {
+                const int32_t inc = __ldg(star + beg + e);
+                t = inc >> 2;
+                lv = inc & 3;
+                tet = ldtet(tets, t);
+            }
+            // the other three vertices in local order (= nbr_of(lv, i)), their
+            // local edge ids and, for face i containing lv, its local face k
+            // and the positions of x, y (the vertices following lv in the
+            // oriented cycle) among them; 3-bit / 6-bit packed per lv
+            const int32_t o[3] = {lv == 0 ? tet.y : tet.x, lv <= 1 ? tet.z : tet.y, lv <= 2 ? tet.w : tet.z};
+            const unsigned etab = (unsigned)(0xb15663088ull >> (9 * lv));
+            const unsigned ftab = lv == 0 ? 0xa950u : (lv == 1 ? 0x1b884u : (lv == 2 ? 0x27250u : 0x1b1a1u));
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
-                const int w = nbr_of(lv, i);
-                const int32_t b = tv(tet, w);
-                if (b <= v) continue;
-                eslot[u][i] = (int32_t)(6 * t + edge_index(lv, w));
-                unsigned h = bucket(hash32((uint32_t)b), mask);
-                for (;;) {
-                    const int32_t old = atomicCAS(ekey + h, -1, b);
-                    if (old == -1 || old == b) break;
-                    h = (h + 1) & mask;
-                }
-                eh[u][i] = (int)h;
-                hv |= (unsigned long long)(h + 1) << (16 * w);
-                atomicMin(eval + h, eslot[u][i]);
-            }
-            if (do_faces) {
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    int k, xi, yi;
-                    face_of(lv, i, k, xi, yi);
-                    const int hx = (int)((hv >> (16 * xi)) & 0xffff) - 1, hy = (int)((hv >> (16 * yi)) & 0xffff) - 1;
-                    if ((hx | hy) < 0) continue;  // x or y <= v
-                    const int32_t key = hx < hy ? (hx << LOG | hy) : (hy << LOG | hx);
-                    unsigned h = bucket(hash32((uint32_t)key), mask);
-                    for (;;) {
-                        const int32_t old = atomicCAS(fkey + h, -1, key);
-                        if (old == -1 || old == key) break;
-                        h = (h + 1) & mask;
-                    }
-                    fh[u][i] = (int)h;
-                    fslot[u][i] = (int32_t)(4 * t + k);
-                    atomicMin(flo + h, fslot[u][i]);
-                    atomicMax(fhi + h, fslot[u][i]);
+                const int32_t b = o[i];
+                const bool q = valid && b > v;
+                const unsigned bal = __ballot_sync(0xffffffffu, q);
+                if (q) el[ne_l + __popc(bal & lt)] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
+                ne_l += __popc(bal);
+                if (do_faces) {
+                    const unsigned f = (ftab >> (6 * i)) & 63u;
+                    const unsigned px = (f >> 2) & 3u, py = f >> 4;
+                    const int32_t x = px == 0 ? o[0] : (px == 1 ? o[1] : o[2]);
+                    const int32_t y = py == 0 ? o[0] : (py == 1 ? o[1] : o[2]);
+                    const bool qf = valid && x > v && y > v;
+                    const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     // count in bits 2+, orientation (x < y: 1, else 2) below:
                     // exactly one slot of each orientation sums to 11
-                    atomicAdd(fcnt + h, tv(tet, xi) < tv(tet, yi) ? 5 : 6);
+                    if (qf)
+                        fl[nf_l + __popc(balf & lt)] =
+                            make_int4(min(x, y), max(x, y), 4 * t + (int)(f & 3u), x < y ? 5 : 6);
+                    nf_l += __popc(balf);
                 }
             }
         }
         __syncwarp();
+        // 2. inserts over the lists, all lanes busy
+        int eh[R], fh[R];
 #pragma unroll
-        for (int u = 0; u < E; ++u)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (eh[u][i] >= 0) edge_first[eslot[u][i]] = eval[eh[u][i]];
-                if (fh[u][i] >= 0) {
-                    const int h = fh[u][i];
-                    const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
-                    const int cnt = c >> 2;
-                    if (cnt > 2 || (cnt == 2 && c != 11)) {
-                        // same orientation twice: "elements A and B claim
-                        // the same oriented face" (connectivity.cpp:62-68)
-                        const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
-                        report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
-                    }
-                    slot_mate[fslot[u][i]] = cnt >= 2 ? (fslot[u][i] == lo ? hi : lo) : -1;
+        for (int r = 0; r < R; ++r) {
+            eh[r] = fh[r] = -1;
+            const int j = lane + 32 * r;
+            if (j < ne_l) {
+                const int2 c = el[j];
+                unsigned h = bucket(hash32((uint32_t)c.x), mask);
+                for (;;) {
+                    const int32_t old = atomicCAS(ekey + h, -1, c.x);
+                    if (old == -1 || old == c.x) break;
+                    h = (h + 1) & mask;
                 }
+                eh[r] = (int)h;
+                atomicMin(eval + h, c.y);
             }
+            if (j < nf_l) {
+                const int4 c = fl[j];
+                const unsigned long long key = (unsigned long long)c.x << 32 | (uint32_t)c.y;
+                unsigned h = bucket(hash64(key), mask);
+                for (;;) {
+                    const unsigned long long old = atomicCAS(fkey + h, ~0ull, key);
+                    if (old == ~0ull || old == key) break;
+                    h = (h + 1) & mask;
+                }
+                fh[r] = (int)h;
+                atomicMin(flo + h, c.z);
+                atomicMax(fhi + h, c.z);
+                atomicAdd(fcnt + h, c.w);
+            }
+        }
         __syncwarp();
+        // 3. read-back: every listed slot gets its group's result
 #pragma unroll
-        for (int u = 0; u < E; ++u)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                if (eh[u][i] >= 0) {
-                    ekey[eh[u][i]] = -1;
-                    eval[eh[u][i]] = INT_MAX;
+        for (int r = 0; r < R; ++r) {
+            const int j = lane + 32 * r;
+            if (eh[r] >= 0) edge_first[el[j].y] = eval[eh[r]];
+            if (fh[r] >= 0) {
+                const int h = fh[r];
+                const int32_t slot = fl[j].z;
+                const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
+                const int cnt = c >> 2;
+                if (cnt > 2 || (cnt == 2 && c != 11)) {
+                    // same orientation twice: "elements A and B claim the
+                    // same oriented face" (connectivity.cpp:62-68)
+                    const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
+                    report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                 }
-                if (fh[u][i] >= 0) {
-                    fkey[fh[u][i]] = -1;
-                    flo[fh[u][i]] = INT_MAX;
-                    fhi[fh[u][i]] = -1;
-                    fcnt[fh[u][i]] = 0;
-                }
+                slot_mate[slot] = cnt >= 2 ? (slot == lo ? hi : lo) : -1;
             }
+        }
+        __syncwarp();
+        // 4. reset the touched table entries
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (eh[r] >= 0) {
+                ekey[eh[r]] = -1;
+                eval[eh[r]] = INT_MAX;
+            }
+            if (fh[r] >= 0) {
+                fkey[fh[r]] = ~0ull;
+                flo[fh[r]] = INT_MAX;
+                fhi[fh[r]] = -1;
+                fcnt[fh[r]] = 0;
+            }
+        }
         __syncwarp();
     }
 }
