@@ -268,29 +268,69 @@ __global__ void __launch_bounds__(32 * kFastWarps)
     const bool do_faces = slot_mate != nullptr;
     const int64_t n = count ? (int64_t)*count : nv;
     const int64_t nwarps = (int64_t)gridDim.x * kFastWarps;
-    for (int64_t it = (int64_t)blockIdx.x * kFastWarps + warp; it < n; it += nwarps) {
-        const int32_t v = list ? list[it] : (int32_t)it;
-        const int64_t beg = star_ptr[v];
-        const int m = (int)(star_ptr[v + 1] - beg);
-        if (m > 32 * E) {
-            if (lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
-            continue;
+    // Software pipeline over this warp's vertices: the dependent loads
+    // star_ptr -> star -> tets of the next vertices are issued one and two
+    // iterations ahead, so their latency overlaps the current vertex.
+    // (no arithmetic on a loaded value in the stage that loads it: that
+    // would wait for the load right there)
+    struct Ptr {
+        int32_t v;
+        int64_t beg, end;
+    };
+    auto load_ptr = [&](int64_t i) -> Ptr {
+        Ptr P{-1, 0, 0};
+        if (i < n) {
+            P.v = list ? list[i] : (int32_t)i;
+            P.beg = star_ptr[P.v];
+            P.end = star_ptr[P.v + 1];
         }
+        return P;
+    };
+    auto load_inc = [&](const Ptr& P, int32_t (&inc)[E]) {
+        const int64_t m = P.end - P.beg;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            const int e = lane + 32 * u;
+            inc[u] = -1;
+            if (e < m && m <= 32 * E) inc[u] = __ldg(star + P.beg + e);
+        }
+    };
+    auto load_tet = [&](const int32_t (&inc)[E], int4 (&tt)[E]) {
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            tt[u] = make_int4(0, 0, 0, 0);
+            if (inc[u] >= 0) tt[u] = ldtet(tets, inc[u] >> 2);
+        }
+    };
+    const int64_t it0 = (int64_t)blockIdx.x * kFastWarps + warp;
+    Ptr P1 = load_ptr(it0), P2 = load_ptr(it0 + nwarps);
+    int32_t I1[E], I2[E];
+    int4 T1[E];
+    load_inc(P1, I1);
+    load_tet(I1, T1);
+    load_inc(P2, I2);
+    Ptr P3 = load_ptr(it0 + 2 * nwarps);
+    for (int64_t it = it0; it < n; it += nwarps) {
+        // stages for it + nwarps (tets) and it + 2 nwarps (incidences, ptrs)
+        int4 T2[E];
+        load_tet(I2, T2);
+        int32_t I3[E];
+        load_inc(P3, I3);
+        const Ptr P4 = load_ptr(it + 3 * nwarps);
+        const int32_t v = P1.v;
+        const int m = (int)(P1.end - P1.beg);
+        const bool deferred = m > 32 * E;
+        if (deferred && lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
+        if (!deferred) {
         // 1. candidates of v -> lists
         int ne_l = 0, nf_l = 0;
 #pragma unroll
         for (int u = 0; u < E; ++u) {
             const int e = lane + 32 * u;
             const bool valid = e < m;
-            int32_t t = 0;
-            int lv = 0;
-            int4 tet = make_int4(0, 0, 0, 0);
-            if (valid) {
-                const int32_t inc = __ldg(star + beg + e);
-                t = inc >> 2;
-                lv = inc & 3;
-                tet = ldtet(tets, t);
-            }
+            const int32_t t = valid ? I1[u] >> 2 : 0;
+            const int lv = valid ? I1[u] & 3 : 0;
+            const int4 tet = T1[u];
             // the other three vertices in local order (= nbr_of(lv, i)), their
             // local edge ids and, for face i containing lv, its local face k
             // and the positions of x, y (the vertices following lv in the
@@ -390,6 +430,16 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             }
         }
         __syncwarp();
+        }
+        P1 = P2;
+        P2 = P3;
+        P3 = P4;
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+            I1[u] = I2[u];
+            I2[u] = I3[u];
+            T1[u] = T2[u];
+        }
     }
 }
 
