@@ -326,6 +326,16 @@ def main():
             roofline["limiter"] = (f"fp64 pipe {prof['fp64_pipe_frac']:.0%} busy (ncu "
                                    f"sm__pipe_fp64_cycles_active); HBM is not the bound")
             roofline["profile"] = prof["source"]
+            if prof.get("fp64_flop") and cfg.name == "cfg4_kuhn128_sin":
+                # fp64 roofline of the same kernel: flops per launch from the
+                # SASS count of the committed capture (same config), over
+                # the live kernel time; peak = 64 DFMA/clk/SM x 2 x 148 SMs
+                # x the max SM clock
+                fl = prof["fp64_flop"]
+                peak = 64 * 2 * 148 * 1.965e9 / 1e12
+                ach = fl / (kern_ms / 1e3) / 1e12
+                roofline["fp64"] = {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                                    "flop_per_tet": fl / ne}
 
     # e2e through the public C ABI: pinned host arrays -> device mesh ->
     # pipeline -> counts back

@@ -56,7 +56,36 @@ def facts(rep):
             "mem_throughput_frac": v.get("mem_throughput"),
             "registers": v.get("registers"),
         }
+    for k, flop in fp64_flops(rep).items():
+        if k in res:
+            res[k]["fp64_flop"] = flop
     return res
+
+
+def fp64_flops(rep):
+    """fp64 flops per kernel (first launch) from the SASS source page:
+    predicated-on thread instructions, DFMA = 2, DMUL / DADD = 1."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True)
+    res, cur, hdr = {}, None, None
+    for x in csv.reader(out.stdout.splitlines()):
+        if x and x[0] == "Kernel Name":
+            k = short(x[1])
+            cur = None if k in res else k
+            if cur:
+                res[cur] = 0.0
+            continue
+        if x and x[0] == "Address":
+            hdr = x
+            continue
+        if cur and hdr:
+            d = dict(zip(hdr, x))
+            w = d.get("Source", "").split()
+            if not w:
+                continue
+            op = (w[1] if w[0].startswith("@") else w[0]).split(".")[0]
+            n = float(d.get("Predicated-On Thread Instructions Executed") or 0)
+            res[cur] += 2 * n if op == "DFMA" else (n if op in ("DMUL", "DADD") else 0)
+    return {k: v for k, v in res.items() if v > 0}
 
 
 def main():
