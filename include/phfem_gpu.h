@@ -81,9 +81,13 @@ int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, do
                        double* partials, void* stream);
 
 /* -------------------------------------------------------- connectivity */
-/* vertex -> (element, local vertex) incidence ("star"), CSR by vertex */
+/* vertex -> (element, local vertex) incidence ("star"), CSR by vertex:
+ * count[v] (zeroed) += incidences; star_ptr = exclusive scan of count;
+ * star_fill places each incidence at star_ptr[v] + --count[v] (the order
+ * inside a vertex's segment is unspecified; every consumer is order free)
+ * and leaves count zeroed. */
 int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream);
-int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_t* star,
+int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr, int32_t* count, int32_t* star,
                         void* stream);
 
 /* Per vertex v, group the edges (v,b), b>v and the faces whose smallest

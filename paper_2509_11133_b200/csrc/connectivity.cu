@@ -36,15 +36,18 @@ __global__ void star_count(const int32_t* __restrict__ tets, int64_t ne, int32_t
     }
 }
 
-__global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, unsigned long long* __restrict__ cursor,
-                          int32_t* __restrict__ star) {
+// position = segment start + the count left after a 32-bit decrement
+__global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, const int64_t* __restrict__ star_ptr,
+                          int32_t* __restrict__ count, int32_t* __restrict__ star) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
         const int4 e = ldtet(tets, t);
         const int32_t base = (int32_t)(4 * t);
-        star[atomicAdd(cursor + e.x, 1ull)] = base + 0;
-        star[atomicAdd(cursor + e.y, 1ull)] = base + 1;
-        star[atomicAdd(cursor + e.z, 1ull)] = base + 2;
-        star[atomicAdd(cursor + e.w, 1ull)] = base + 3;
+        const int32_t c0 = atomicSub(count + e.x, 1), c1 = atomicSub(count + e.y, 1), c2 = atomicSub(count + e.z, 1),
+                      c3 = atomicSub(count + e.w, 1);
+        star[__ldg(star_ptr + e.x) + c0 - 1] = base + 0;
+        star[__ldg(star_ptr + e.y) + c1 - 1] = base + 1;
+        star[__ldg(star_ptr + e.z) + c2 - 1] = base + 2;
+        star[__ldg(star_ptr + e.w) + c3 - 1] = base + 3;
     }
 }
 
@@ -845,9 +848,10 @@ extern "C" int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* co
     return (int)cudaGetLastError();
 }
 
-extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, int64_t* cursor, int32_t* star, void* stream) {
-    star_fill<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(
-        tets, ne, reinterpret_cast<unsigned long long*>(cursor), star); phg::count_launches(1);
+extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr, int32_t* count,
+                                   int32_t* star, void* stream) {
+    star_fill<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, star_ptr, count, star);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

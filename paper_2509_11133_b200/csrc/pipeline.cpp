@@ -94,10 +94,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_star_count(m.tets.p, ne, w.cnt.p, SV()), "star count");
     c.star_ptr.alloc(nc + 1);
     check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, nc, w.scratch.p, SV()), "star scan");
-    w.cursor.alloc(nc);
-    if (nc) check(cudaMemcpyAsync(w.cursor.p, c.star_ptr.p, sizeof(int64_t) * nc, cudaMemcpyDeviceToDevice, S()), "D2D");
     c.star.alloc(4 * ne);
-    check(phfem_gpu_star_fill(m.tets.p, ne, w.cursor.p, c.star.p, SV()), "star fill");
+    check(phfem_gpu_star_fill(m.tets.p, ne, c.star_ptr.p, w.cnt.p, c.star.p, SV()), "star fill");
     if (st) st->star += tm.stop_ms();
     // 2. per-vertex grouping of edges and faces
     tm.start();
