@@ -24,6 +24,12 @@
 namespace phg {
 __constant__ double c_lam5[64 * 4];
 __constant__ double c_w5[64];
+// the same rule in its collapsed-product structure (quadrature.cpp:47-59):
+// point 16a + 4b + c has lambda1 = c_l1[a], lambda2 = c_l2[4a + b],
+// lambda3 = c_l3[16a + 4b + c]
+__constant__ double c_l1[4];
+__constant__ double c_l2[16];
+__constant__ double c_l3[64];
 }  // namespace phg
 
 extern "C" int phfem_gpu_set_rules_errors(const double* lam9, const double* w9);
@@ -73,7 +79,21 @@ __device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict_
 }
 
 // Gauss-64 load vector of the transcendental kinds with the trig / exp
-// factors as order-N Taylor series around vertex 0 (problems.cuh)
+// factors as order-N Taylor series around vertex 0 (problems.cuh), walking
+// the rule in its collapsed-product order (a, b, c):
+//   z = lambda1 e1 + lambda2 e2 + lambda3 e3 = A(a, b) + lambda3 e3, with
+//       A(a, b) = fma(lambda2, e2, lambda1 e1) formed once per (a, b): the
+//       same operations as the per-point fma chain, a third of the cost;
+//   b1 = sum_a lambda1(a) T_a, b2 = sum_ab lambda2(a, b) U_ab with the
+//       partial sums U_ab = sum_c w f, T_a = sum_b U_ab, b3 per point, and
+//       b0 = S - b1 - b2 - b3 (lambda0 = 1 - lambda1 - lambda2 - lambda3).
+template <int N>
+__device__ __forceinline__ double horner(const AxisTaylor<N>& t, double z) {
+    double r = t.k[N];
+#pragma unroll
+    for (int n = N - 1; n >= 0; --n) r = fma(r, z, t.k[n]);
+    return r;
+}
 template <int KIND, int N>
 __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Coef& k, double vol, double b[4]) {
     const int GX = KIND == 3 ? kTaySin : kTayExp;
@@ -83,31 +103,53 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
     const AxisTaylor<N> tz = axis_taylor<N, kTaySin>(p[0].z, p[1].z, p[2].z, p[3].z);
     (void)tz;
     (void)tx;
-#pragma unroll 2
-    for (int qp = 0; qp < 64; ++qp) {
-        const double l0 = c_lam5[4 * qp], l1 = c_lam5[4 * qp + 1], l2 = c_lam5[4 * qp + 2], l3 = c_lam5[4 * qp + 3];
-        double f;
-        if constexpr (KIND == 3) {
-            // the constant factor cpre is applied once after the loop
-            f = taylor_eval(tx, l1, l2, l3) * taylor_eval(ty, l1, l2, l3) * taylor_eval(tz, l1, l2, l3);
-        } else if constexpr (KIND == 4) {
-            const double z = fma(p[3].z, l3, fma(p[2].z, l2, fma(p[1].z, l1, p[0].z * l0)));
-            const double ec = taylor_eval(tx, l1, l2, l3) * taylor_eval(ty, l1, l2, l3);
-            f = fma(cpre, ec * (z * z), -(k.a2 * 2.0) * ec);
-        } else {
-            const double x = fma(p[3].x, l3, fma(p[2].x, l2, fma(p[1].x, l1, p[0].x * l0)));
-            const double s = taylor_eval(ty, l1, l2, l3) * taylor_eval(tz, l1, l2, l3);
-            f = fma(cpre, x * (8.0 - x) * s, 2.0 * k.a0 * s);
+    // the coordinate entering f polynomially: z (kind 4) or x (kind 5)
+    const double c0 = KIND == 4 ? p[0].z : p[0].x;
+    const double d1 = (KIND == 4 ? p[1].z : p[1].x) - c0, d2 = (KIND == 4 ? p[2].z : p[2].x) - c0,
+                 d3 = (KIND == 4 ? p[3].z : p[3].x) - c0;
+    double S = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    for (int a = 0; a < 4; ++a) {
+        const double l1 = c_l1[a];
+        double T = 0.0;
+#pragma unroll 1
+        for (int bb = 0; bb < 4; ++bb) {
+            const double l2 = c_l2[4 * a + bb];
+            const double ax = fma(l2, tx.e2, l1 * tx.e1), ay = fma(l2, ty.e2, l1 * ty.e1),
+                         az = fma(l2, tz.e2, l1 * tz.e1), al = fma(l2, d2, fma(l1, d1, c0));
+            double U = 0.0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int qp = 16 * a + 4 * bb + c;
+                const double l3 = c_l3[qp];
+                double f;
+                if constexpr (KIND == 3) {
+                    // the constant factor cpre is applied once after the loop
+                    f = horner(tx, fma(l3, tx.e3, ax)) * horner(ty, fma(l3, ty.e3, ay)) *
+                        horner(tz, fma(l3, tz.e3, az));
+                } else if constexpr (KIND == 4) {
+                    const double zc = fma(l3, d3, al);
+                    const double ec = horner(tx, fma(l3, tx.e3, ax)) * horner(ty, fma(l3, ty.e3, ay));
+                    f = fma(cpre, ec * (zc * zc), -(k.a2 * 2.0) * ec);
+                } else {
+                    const double xc = fma(l3, d3, al);
+                    const double sv = horner(ty, fma(l3, ty.e3, ay)) * horner(tz, fma(l3, tz.e3, az));
+                    f = fma(cpre, xc * (8.0 - xc) * sv, 2.0 * k.a0 * sv);
+                }
+                const double fw = c_w5[qp] * f;
+                U += fw;
+                b3 = fma(fw, l3, b3);
+            }
+            T += U;
+            b2 = fma(U, l2, b2);
         }
-        const double fw = c_w5[qp] * f;
-        b[0] = fma(fw, l0, b[0]);
-        b[1] = fma(fw, l1, b[1]);
-        b[2] = fma(fw, l2, b[2]);
-        b[3] = fma(fw, l3, b[3]);
+        S += T;
+        b1 = fma(T, l1, b1);
     }
     const double sc = KIND == 3 ? vol * cpre : vol;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) b[i] *= sc;
+    b[0] = (((S - b1) - b2) - b3) * sc;
+    b[1] = b1 * sc;
+    b[2] = b2 * sc;
+    b[3] = b3 * sc;
 }
 
 // Gauss-64 load vector b_T (assembly.cpp:64-78) of one element with
@@ -454,6 +496,22 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
     if (n5 != 64 || n9 != 216) return (int)cudaErrorInvalidValue;
     cudaMemcpyToSymbol(phg::c_lam5, lam5, sizeof(double) * 4 * 64);
     cudaMemcpyToSymbol(phg::c_w5, w5, sizeof(double) * 64);
+    // collapsed-product structure of the degree-5 rule (4 x 4 x 4 points)
+    double l1[4], l2[16], l3[64];
+    for (int a = 0; a < 4; ++a) {
+        l1[a] = lam5[4 * (16 * a) + 1];
+        for (int b = 0; b < 4; ++b) {
+            l2[4 * a + b] = lam5[4 * (16 * a + 4 * b) + 2];
+            for (int c = 0; c < 4; ++c) {
+                const int q = 16 * a + 4 * b + c;
+                l3[q] = lam5[4 * q + 3];
+                if (lam5[4 * q + 1] != l1[a] || lam5[4 * q + 2] != l2[4 * a + b]) return (int)cudaErrorInvalidValue;
+            }
+        }
+    }
+    cudaMemcpyToSymbol(phg::c_l1, l1, sizeof(l1));
+    cudaMemcpyToSymbol(phg::c_l2, l2, sizeof(l2));
+    cudaMemcpyToSymbol(phg::c_l3, l3, sizeof(l3));
     const int rc = (int)cudaGetLastError();
     return rc ? rc : phfem_gpu_set_rules_errors(lam9, w9);
 }

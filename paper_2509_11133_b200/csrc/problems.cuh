@@ -170,14 +170,6 @@ __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, doubl
     }
     return a;
 }
-template <int N>
-__device__ __forceinline__ double taylor_eval(const AxisTaylor<N>& a, double l1, double l2, double l3) {
-    const double z = fma(l3, a.e3, fma(l2, a.e2, l1 * a.e1));
-    double r = a.k[N];
-#pragma unroll
-    for (int n = N - 1; n >= 0; --n) r = fma(r, z, a.k[n]);
-    return r;
-}
 
 // loop-invariant factor of prob_f_fast
 template <int KIND>
