@@ -203,6 +203,42 @@ def cpu_baseline(n=32):
                        f"only build_schur uses more than one thread")}
 
 
+# ------------------------------------------------------- multi-process
+
+
+def dist_setup(world: int, local: int, backend: str = "nccl"):
+    """One process per GPU (torchrun env): the process group, or None at
+    world size 1.  NCCL carries only the barrier and the max-over-ranks
+    timing; the replicas exchange no data."""
+    if world <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
+def max_over_ranks(dist, x: float, device=None) -> float:
+    """The slowest rank's time (every rank gets it)."""
+    if dist is None:
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(world: int, units_per_rank: int, ms_max: float) -> float:
+    """Whole-job units/s: every rank processes the same units (weak scaling)
+    and the job takes as long as its slowest rank."""
+    return world * units_per_rank / (ms_max / 1e3)
+
+
 # ------------------------------------------------------------------ ours
 
 
@@ -230,11 +266,7 @@ def main():
     import torch
 
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = dist_setup(world, local)
 
     import numpy as np
 
@@ -280,11 +312,8 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     nlaunch = launches() - l0
     stage_ms = {k: v / args.steps for k, v in acc.items()}
-    t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * ne / (ms_max / 1e3)
+    ms_max = max_over_ranks(dist, ms, "cuda")
+    value = job_throughput(world, ne, ms_max)
 
     # nnz(S) (true, without SELL padding) from the row structure: every
     # multiplier row has 1 + the non-Neumann other faces of its 1-2 elements
@@ -360,10 +389,8 @@ def main():
     e3.synchronize()
     wall = (time.perf_counter() - t_wall) / args.steps
     e2e_ms = max(e2.elapsed_time(e3) / args.steps, wall * 1e3)
-    te = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-    if dist:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e = {"value": world * ne / (float(te.item()) / 1e3), "unit": "tets/s", "h2d_bytes_per_step": int(h2d),
+    e2e = {"value": job_throughput(world, ne, max_over_ranks(dist, e2e_ms, "cuda")), "unit": "tets/s",
+           "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(cts.nbytes + 7 * 8)}
 
     # Schur solve (Jacobi-PCG, reference stopping rule), once
