@@ -829,6 +829,7 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
             ne_child = child->ne;
         }
         const double tot = total.stop_ms();
+        st.resolve();
         if (ms) {
             ms->star = st.star;
             ms->groups = st.groups;

@@ -82,13 +82,13 @@ void replay_connectivity_errors(const std::vector<unsigned long long>& e, const 
 void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st) {
     const int64_t nc = m.nc, ne = m.ne;
     Work& w = c.w;
-    Timer tm;
+    cudaEvent_t t0 = nullptr;
     const auto w0 = std::chrono::steady_clock::now();
     reset_err(w);
     w.scratch.alloc((int64_t)std::max(phfem_gpu_scan_scratch(std::max<int64_t>({nc, ne, 4 * ne})),
                                       phfem_gpu_element_offsets_scratch(ne)));
     // 1. vertex star (CSR by vertex)
-    tm.start();
+    if (st) t0 = st->mark();
     w.cnt.alloc(nc);
     w.cnt.zero();
     check(phfem_gpu_star_count(m.tets.p, ne, w.cnt.p, SV()), "star count");
@@ -96,9 +96,9 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, nc, w.scratch.p, SV()), "star scan");
     c.star.alloc(4 * ne);
     check(phfem_gpu_star_fill(m.tets.p, ne, c.star_ptr.p, w.cnt.p, c.star.p, SV()), "star fill");
-    if (st) st->star += tm.stop_ms();
+    if (st) st->span(&st->star, t0);
     // 2. per-vertex grouping of edges and faces
-    tm.start();
+    if (st) t0 = st->mark();
     c.edge_first.alloc(6 * ne);
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(2 * (nc > 0 ? nc : 1));
@@ -106,9 +106,9 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
                                 w.big_list.p, w.big_count.p, w.err.p, SV()),
           "star groups");
-    if (st) st->groups += tm.stop_ms();
+    if (st) st->span(&st->groups, t0);
     // 3. numbering: per-element counts, scans, ids, remaining slots
-    tm.start();
+    if (st) t0 = st->mark();
     c.edge_off.alloc(ne + 1);
     if (faces) w.face_off.alloc(ne + 1);
     w.masks.alloc(ne + 8);
@@ -138,7 +138,7 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
                            faces ? c.faces.p : nullptr, faces ? c.face_slots.p : nullptr,
                            faces ? c.face_area.p : nullptr, w.err.p, SV()),
           "number");
-    if (st) st->number += tm.stop_ms();
+    if (st) st->span(&st->number, t0);
     c.has_edges = true;
     c.has_faces = false;
     c.t_edges = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
@@ -148,7 +148,7 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     }
     // 4. boundary classification and multiplier rows
     const auto w1 = std::chrono::steady_clock::now();
-    tm.start();
+    if (st) t0 = st->mark();
     const int64_t nf = c.nf;
     w.claim.alloc(nf);
     w.claim.fill_bytes(0xff);
@@ -176,7 +176,7 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     c.face_mrow.alloc(nf);
     c.row_face.alloc(c.l);
     check(phfem_gpu_face_rows(nf, c.face_class.p, w.row_off.p, c.face_mrow.p, c.row_face.p, SV()), "face rows");
-    if (st) st->classify += tm.stop_ms();
+    if (st) st->span(&st->classify, t0);
     replay_connectivity_errors(w.err.download(), m, c);
     c.has_faces = true;
     c.t_faces = std::chrono::duration<double>(std::chrono::steady_clock::now() - w1).count();
@@ -192,8 +192,7 @@ std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, Refine
     if (nc2 >= (int64_t)INT32_MAX || 6 * ne2 >= (int64_t)INT32_MAX)
         throw MeshError("out of memory while refining to level " + std::to_string(m.level + 1) +
                         ": 32-bit node/element ids exhausted");
-    Timer tm;
-    tm.start();
+    cudaEvent_t t0 = st ? st->mark() : nullptr;
     auto out = into ? into : std::make_shared<MeshData>();
     out->nc = nc2;
     out->ne = ne2;
@@ -220,8 +219,7 @@ std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, Refine
     check(phfem_gpu_refine_boundary(m.nn, m.nb.p, m.nd, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
                                     c.edge_of_slot.p, out->nb.p, w.err.p, SV()),
           "refine boundary");
-    const double ms = tm.stop_ms();
-    if (st) st->refine += ms;
+    if (st) st->span(&st->refine, t0);
     const auto e = w.err.download();
     if (e[PHG_ERR_BOUNDARY_EDGE] != kNone) {
         const int64_t i = (int64_t)(e[PHG_ERR_BOUNDARY_EDGE] >> 2);
@@ -251,8 +249,7 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
                      bool debug_views, Stages* st) {
     if (!c.has_faces) throw MeshError("assemble: face table missing");
     if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
-    Timer tm;
-    tm.start();
+    cudaEvent_t t0 = st ? st->mark() : nullptr;
     sys.problem = problem;
     sys.coef_version = k.version;
     sys.n = 4 * m.ne;
@@ -282,24 +279,19 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     w.redo.alloc(m.ne + 1);
     reset_err(w);
     const phg_problem p = device_problem(k, problem);
-    Timer tk;  // the main kernel alone
+    // the main kernel alone
+    cudaEvent_t ka = st ? st->event() : nullptr, kb = st ? st->event() : nullptr;
     check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
                                       c.face_mrow.p, c.face_area.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,
                                       debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p,
-                                      w.err.p, st ? tk.a : nullptr, st ? tk.b : nullptr, SV()),
+                                      w.err.p, ka, kb, SV()),
           "assemble");
-    const double ms = tm.stop_ms();
     if (st) {
-        st->assemble += ms;
-        float kms = 0.f;
-        check(cudaEventElapsedTime(&kms, tk.a, tk.b), "event time");
-        st->assemble_kernel += kms;
+        st->span(&st->assemble, t0);
+        st->span(&st->assemble_kernel, ka, kb);
     }
-    const auto nv = read_many<double, 2>({w.norms.p, w.norms.p + 1});
-    sys.sum_rhs2 = nv[0];
-    sys.sum_bd2 = nv[1];
     const auto e = w.err.download();
     // assembly.cpp:13-14 (first element in order), then solver.cpp:128-129
     if (e[PHG_ERR_ZERO_VOLUME] != kNone)

@@ -61,6 +61,36 @@ Timer::~Timer() {
     cudaEventDestroy(b);
 }
 void Timer::start() { check(cudaEventRecord(a, S()), "event record"); }
+
+Stages::~Stages() {
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
+}
+cudaEvent_t Stages::event() {
+    if (used_ == events_.size()) {
+        cudaEvent_t e;
+        check(cudaEventCreate(&e), "event");
+        events_.push_back(e);
+    }
+    return events_[used_++];
+}
+cudaEvent_t Stages::mark() {
+    cudaEvent_t e = event();
+    check(cudaEventRecord(e, S()), "event record");
+    return e;
+}
+void Stages::span(double* field, cudaEvent_t from) { pending_.emplace_back(field, from, mark()); }
+void Stages::span(double* field, cudaEvent_t from, cudaEvent_t to) { pending_.emplace_back(field, from, to); }
+void Stages::resolve() {
+    if (pending_.empty()) return;
+    check(cudaEventSynchronize(std::get<2>(pending_.back())), "event sync");
+    sync();
+    for (auto& [field, a, b] : pending_) {
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, a, b), "event time");
+        *field += ms;
+    }
+    pending_.clear();
+}
 double Timer::stop_ms() {
     check(cudaEventRecord(b, S()), "event record");
     check(cudaEventSynchronize(b), "event sync");
@@ -175,11 +205,21 @@ std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly
 
 // ------------------------------------------------------------------- solve
 
+void System::norms(double& sum_rhs2, double& sum_bd2) const {
+    double h[2];
+    check(cudaMemcpyAsync(h, w.norms.p, sizeof(h), cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    sum_rhs2 = h[0];
+    sum_bd2 = h[1];
+}
+
 void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const System& sys, int problem,
                  double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only) {
     const auto t0 = std::chrono::steady_clock::now();
     const int64_t l = sys.l;
-    const double nrm_rhs = std::sqrt(sys.sum_rhs2), nrm_bd = std::sqrt(sys.sum_bd2);
+    double sum_rhs2, sum_bd2;
+    sys.norms(sum_rhs2, sum_bd2);
+    const double nrm_rhs = std::sqrt(sum_rhs2), nrm_bd = std::sqrt(sum_bd2);
     // inner_cg_options, solver.cpp:78-86
     const double abs_tol = 0.2 * tol * std::hypot(nrm_rhs, nrm_bd);
     const long long mi = max_iter > 0 ? max_iter : 10 * std::max<int64_t>(l, 1);

@@ -9,6 +9,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "phfem_gpu.h"
@@ -180,7 +181,9 @@ struct System {
     int64_t n = 0, l = 0, nchunks = 0;
     DBuf<int32_t> sell_col;
     DBuf<double> sell_val, rhs_neg, bd, rhs;
-    double sum_rhs2 = 0.0, sum_bd2 = 0.0;
+    // sum(B_T^2), sum(b_D^2): reduced on the device by the assembly, read
+    // to the host only when a solve needs them
+    void norms(double& sum_rhs2, double& sum_bd2) const;
     // debug views (filled only on request)
     DBuf<double> a_blocks, slot_coef;
     DBuf<int32_t> slot_mrow;
@@ -190,9 +193,30 @@ struct RefineMap {
     DBuf<int32_t> midpoint, centroid;
 };
 
+// Stage times from events recorded on the library stream without host
+// synchronisation; resolve() (one synchronisation) turns the recorded spans
+// into milliseconds after the pass.
 struct Stages {
     double star = 0, groups = 0, number = 0, classify = 0, assemble = 0, refine = 0;
     double assemble_kernel = 0;  // assemble_k alone
+    Stages() = default;
+    Stages(const Stages&) = delete;
+    Stages& operator=(const Stages&) = delete;
+    ~Stages();
+    // records an event now; returns its handle
+    cudaEvent_t mark();
+    // an event for the caller to record
+    cudaEvent_t event();
+    // adds the time between `from` and an event recorded now to *field
+    void span(double* field, cudaEvent_t from);
+    // adds the time between two recorded events to *field
+    void span(double* field, cudaEvent_t from, cudaEvent_t to);
+    void resolve();
+
+  private:
+    std::vector<cudaEvent_t> events_;
+    size_t used_ = 0;
+    std::vector<std::tuple<double*, cudaEvent_t, cudaEvent_t>> pending_;
 };
 
 // --------------------------------------------------------------- pipeline
