@@ -135,16 +135,20 @@ int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t nn, const in
                              const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                              const int32_t* face_of_slot, const uint32_t* claim,
                              unsigned long long* err, void* stream);
-/* face classes + non-Neumann flags (connectivity.cpp:177-201); claim[f] is
- * the first list entry naming face f (all ones: none);
- * counts[3] += interior, dirichlet, neumann (device int64) */
+/* face classes (connectivity.cpp:177-201); claim[f] is the first list entry
+ * naming face f (all ones: none); counts[3] += interior, dirichlet, neumann
+ * (device int64, zeroed by the caller); *n_rows (device) = number of row
+ * (non-Neumann) faces.  scratch (phfem_gpu_face_rows_scratch(nf) bytes)
+ * carries the per-tile row offsets to phfem_gpu_face_rows. */
+size_t phfem_gpu_face_rows_scratch(int64_t nf);
 int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const int32_t* face_slots,
-                         const double* face_area, uint8_t* face_class, int32_t* is_row,
-                         unsigned long long* counts, unsigned long long* err, void* stream);
-/* multiplier rows from the exclusive scan of is_row (rank among
- * non-Neumann faces) and the inverse map row -> face */
-int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const int64_t* row_off,
-                        int32_t* face_mrow, int32_t* row_face, void* stream);
+                         uint8_t* face_class, unsigned long long* counts, void* scratch, int64_t* n_rows,
+                         unsigned long long* err, void* stream);
+/* multiplier rows = rank among the row faces (face_mrow, -1 for Neumann
+ * faces) and the inverse map row -> face, from face_class and the scratch of
+ * phfem_gpu_face_class */
+int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const void* scratch, int32_t* face_mrow,
+                        int32_t* row_face, void* stream);
 
 /* ----------------------------------------------------------- refinement */
 /* red_refine (refine.cpp:16-74): one thread per parent; child 0 at row t,

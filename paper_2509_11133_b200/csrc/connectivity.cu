@@ -772,68 +772,117 @@ __global__ void classify_check(int64_t nd, const int32_t* __restrict__ db, int64
     }
 }
 
-__global__ void face_class_k(int64_t nf, int64_t nd, const uint32_t* __restrict__ claim,
-                             const int32_t* __restrict__ face_slots, uint8_t* __restrict__ face_class,
-                             int32_t* __restrict__ is_row, unsigned long long* __restrict__ counts,
-                             unsigned long long* err) {
-    int c0 = 0, c1 = 0, c2 = 0;
-    auto one = [&](int64_t f, uint32_t cl, int32_t mate) -> uint8_t {
-        uint8_t cls = 0;
-        if (cl != 0xffffffffu) cls = (int64_t)cl < nd ? 1 : 2;
-        else if (mate < 0) report(err, PHG_ERR_FACE, (unsigned long long)f << 2 | 1);
-        c0 += cls == 0;
-        c1 += cls == 1;
-        c2 += cls == 2;
-        return cls;
-    };
-    // four faces per thread and step: 16 B loads keep enough bytes in flight
-    const int64_t nq = nf / 4;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint4 cl = __ldg(reinterpret_cast<const uint4*>(claim) + i);
-        const int4 s01 = __ldg(reinterpret_cast<const int4*>(face_slots) + 2 * i);
-        const int4 s23 = __ldg(reinterpret_cast<const int4*>(face_slots) + 2 * i + 1);
-        const int64_t f = 4 * i;
-        const uint8_t a = one(f, cl.x, s01.y), b = one(f + 1, cl.y, s01.w), c = one(f + 2, cl.z, s23.y),
-                      d = one(f + 3, cl.w, s23.w);
-        reinterpret_cast<uchar4*>(face_class)[i] = make_uchar4(a, b, c, d);
-        reinterpret_cast<int4*>(is_row)[i] = make_int4(a != 2, b != 2, c != 2, d != 2);
+// Face classes and multiplier rows, reduce-then-scan over tiles of
+// kScanTile faces (scan.cuh), thread i of a tile owning faces
+// [16 i, 16 i + 16):
+//   face_class_k  class (0 interior, 1 Dirichlet, 2 Neumann) per face, the
+//                 tile's count of row faces (non-Neumann) and the class counts
+//   scan_sums     the tile counts
+//   face_rows_k   rows = rank among the row faces, and the inverse map
+__device__ __forceinline__ uint8_t face_class_of(int64_t f, uint32_t cl, int32_t mate, int64_t nd,
+                                                 unsigned long long* err) {
+    uint8_t cls = 0;
+    if (cl != 0xffffffffu) cls = (int64_t)cl < nd ? 1 : 2;
+    else if (mate < 0) report(err, PHG_ERR_FACE, (unsigned long long)f << 2 | 1);
+    return cls;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    face_class_k(int64_t nf, int64_t nd, const uint32_t* __restrict__ claim, const int32_t* __restrict__ face_slots,
+                 uint8_t* __restrict__ face_class, long long* __restrict__ sums, unsigned long long* __restrict__ counts,
+                 unsigned long long* err) {
+    // striped groups of four faces: 16 B loads / 4 B stores, coalesced
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < kScanItems / 4; ++i) {
+        const int64_t f = base + 4 * (i * kScanThreads + (int64_t)threadIdx.x);
+        if (f + 4 <= nf) {
+            const uint4 cl = __ldg(reinterpret_cast<const uint4*>(claim + f));
+            const int4 s01 = __ldg(reinterpret_cast<const int4*>(face_slots + 2 * f));
+            const int4 s23 = __ldg(reinterpret_cast<const int4*>(face_slots + 2 * f) + 1);
+            const uint8_t k0 = face_class_of(f, cl.x, s01.y, nd, err), k1 = face_class_of(f + 1, cl.y, s01.w, nd, err),
+                          k2 = face_class_of(f + 2, cl.z, s23.y, nd, err),
+                          k3 = face_class_of(f + 3, cl.w, s23.w, nd, err);
+            reinterpret_cast<uchar4*>(face_class + f)[0] = make_uchar4(k0, k1, k2, k3);
+            ++c[k0];
+            ++c[k1];
+            ++c[k2];
+            ++c[k3];
+        } else {
+            for (int j = 0; j < 4 && f + j < nf; ++j) {
+                const uint8_t k = face_class_of(f + j, claim[f + j], face_slots[2 * (f + j) + 1], nd, err);
+                face_class[f + j] = k;
+                ++c[k];
+            }
+        }
     }
-    for (int64_t f = 4 * nq + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf;
-         f += (int64_t)gridDim.x * blockDim.x) {
-        const uint8_t cls = one(f, claim[f], face_slots[2 * f + 1]);
-        face_class[f] = cls;
-        is_row[f] = cls != 2;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-    }
-    // one atomic triple per block: per-warp atomics on the same three words
-    // serialise in L2 (~170 us at 25M faces)
+    // rows: interior + Dirichlet faces; one atomic triple per block
+    const long long rows = block_sum_ll<kScanThreads>(c[0] + c[1]);
+    if (threadIdx.x == 0) sums[blockIdx.x] = rows;
     __shared__ int sc[3];
     if (threadIdx.x < 3) sc[threadIdx.x] = 0;
     __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        c[0] += __shfl_xor_sync(0xffffffffu, c[0], o);
+        c[1] += __shfl_xor_sync(0xffffffffu, c[1], o);
+        c[2] += __shfl_xor_sync(0xffffffffu, c[2], o);
+    }
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(sc + 0, c0);
-        atomicAdd(sc + 1, c1);
-        atomicAdd(sc + 2, c2);
+        atomicAdd(sc + 0, c[0]);
+        atomicAdd(sc + 1, c[1]);
+        atomicAdd(sc + 2, c[2]);
     }
     __syncthreads();
     if (threadIdx.x < 3) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
 }
 
-__global__ void face_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, const int64_t* __restrict__ row_off,
-                            int32_t* __restrict__ face_mrow, int32_t* __restrict__ row_face) {
-    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
-        if (face_class[f] != 2) {
-            const int64_t r = row_off[f];
-            face_mrow[f] = (int32_t)r;
-            row_face[r] = (int32_t)f;
-        } else {
-            face_mrow[f] = -1;
-        }
+// classes staged in shared memory (striped in, blocked for the scan), rows
+// and the compacted row -> face list staged again and written out striped
+__global__ void __launch_bounds__(kScanThreads)
+    face_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, const long long* __restrict__ tile_off,
+                int32_t* __restrict__ face_mrow, int32_t* __restrict__ row_face) {
+    __shared__ __align__(16) uint8_t s_cls[kScanTile];
+    __shared__ int32_t s_row[kScanTile + kScanTile / 32];
+    __shared__ int32_t s_rf[kScanTile];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    const int nt = (int)(nf - base < kScanTile ? nf - base : kScanTile);
+    if (nt == kScanTile) {
+        reinterpret_cast<uint4*>(s_cls)[threadIdx.x] = __ldg(reinterpret_cast<const uint4*>(face_class + base) + threadIdx.x);
+    } else {
+        for (int i = threadIdx.x; i < kScanTile; i += kScanThreads) s_cls[i] = i < nt ? face_class[base + i] : 2;
     }
+    __syncthreads();
+    const uint4 q = reinterpret_cast<const uint4*>(s_cls)[threadIdx.x];
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    int n = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) n += ((w[i / 4] >> (8 * (i % 4))) & 0xffu) != 2;
+    long long tot;
+    int r = (int)block_excl_scan_ll<kScanThreads>(n, &tot);
+    const long long off = tile_off[blockIdx.x];
+    // local index i of the tile lives at s_row[i + i / 32] (one pad word per
+    // 32: blocked writes of 16 consecutive words stay conflict-light)
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const int li = threadIdx.x * kScanItems + i;
+        const bool row = ((w[i / 4] >> (8 * (i % 4))) & 0xffu) != 2;
+        s_row[li + (li >> 5)] = row ? (int32_t)(off + r) : -1;
+        if (row) s_rf[r++] = (int32_t)(base + li);
+    }
+    __syncthreads();
+    if (nt == kScanTile) {
+#pragma unroll
+        for (int k = 0; k < kScanItems / 4; ++k) {
+            const int i = 4 * (k * kScanThreads + threadIdx.x);  // 4 consecutive, same pad group
+            const int p = i + (i >> 5);
+            reinterpret_cast<int4*>(face_mrow + base)[k * kScanThreads + threadIdx.x] =
+                make_int4(s_row[p], s_row[p + 1], s_row[p + 2], s_row[p + 3]);
+        }
+    } else {
+        for (int i = threadIdx.x; i < nt; i += kScanThreads) face_mrow[base + i] = s_row[i + (i >> 5)];
+    }
+    for (int j = threadIdx.x; j < (int)tot; j += kScanThreads) row_face[off + j] = s_rf[j];
 }
 
 inline int grid_cap(int64_t n, int block) {
@@ -945,17 +994,31 @@ extern "C" int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t n
     return (int)cudaGetLastError();
 }
 
+extern "C" size_t phfem_gpu_face_rows_scratch(int64_t nf) {
+    return (size_t)(scan_tiles(nf) + 1) * sizeof(long long);
+}
+
 extern "C" int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const int32_t* face_slots,
-                                    const double* face_area, uint8_t* face_class, int32_t* is_row,
-                                    unsigned long long* counts, unsigned long long* err, void* stream) {
-    (void)face_area;
-    face_class_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, nd, claim, face_slots, face_class, is_row,
-                                                                      counts, err); phg::count_launches(1);
+                                    uint8_t* face_class, unsigned long long* counts, void* scratch, int64_t* n_rows,
+                                    unsigned long long* err, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nf <= 0) {
+        cudaMemsetAsync(n_rows, 0, sizeof(int64_t), s);
+        return (int)cudaGetLastError();
+    }
+    const int64_t ntiles = scan_tiles(nf);
+    long long* sums = static_cast<long long*>(scratch);
+    face_class_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(nf, nd, claim, face_slots, face_class, sums, counts, err);
+    scan_sums(sums, ntiles, n_rows, s);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }
 
-extern "C" int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const int64_t* row_off, int32_t* face_mrow,
+extern "C" int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const void* scratch, int32_t* face_mrow,
                                    int32_t* row_face, void* stream) {
-    face_rows_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_class, row_off, face_mrow, row_face); phg::count_launches(1);
+    if (nf <= 0) return 0;
+    face_rows_k<<<(unsigned)scan_tiles(nf), kScanThreads, 0, (cudaStream_t)stream>>>(
+        nf, face_class, static_cast<const long long*>(scratch), face_mrow, row_face);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -158,24 +158,21 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_classify_check(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
                                    w.claim.p, w.err.p, SV()),
           "classify check");
-    c.face_class.alloc(nf);
-    w.is_row.alloc(nf);
-    w.counts.alloc(3);
+    c.face_class.alloc(nf + 16);
+    w.counts.alloc(4);
     w.counts.zero();
-    check(phfem_gpu_face_class(nf, m.nd, w.claim.p, c.face_slots.p, c.face_area.p, c.face_class.p, w.is_row.p,
-                               w.counts.p, w.err.p, SV()),
+    w.scratch.alloc((int64_t)phfem_gpu_face_rows_scratch(nf));
+    check(phfem_gpu_face_class(nf, m.nd, w.claim.p, c.face_slots.p, c.face_class.p, w.counts.p, w.scratch.p,
+                               reinterpret_cast<int64_t*>(w.counts.p + 3), w.err.p, SV()),
           "face class");
-    w.row_off.alloc(nf + 1);
-    check(phfem_gpu_scan_i32(w.is_row.p, w.row_off.p, nf, w.scratch.p, SV()), "row scan");
-    const auto cnt = read_many<unsigned long long, 4>(
-        {w.counts.p, w.counts.p + 1, w.counts.p + 2, reinterpret_cast<const unsigned long long*>(w.row_off.p + nf)});
+    const auto cnt = read_many<unsigned long long, 4>({w.counts.p, w.counts.p + 1, w.counts.p + 2, w.counts.p + 3});
     c.n_int = (int64_t)cnt[0];
     c.n_dir = (int64_t)cnt[1];
     c.n_neu = (int64_t)cnt[2];
     c.l = (int64_t)cnt[3];
     c.face_mrow.alloc(nf);
     c.row_face.alloc(c.l);
-    check(phfem_gpu_face_rows(nf, c.face_class.p, w.row_off.p, c.face_mrow.p, c.row_face.p, SV()), "face rows");
+    check(phfem_gpu_face_rows(nf, c.face_class.p, w.scratch.p, c.face_mrow.p, c.row_face.p, SV()), "face rows");
     if (st) st->span(&st->classify, t0);
     replay_connectivity_errors(w.err.download(), m, c);
     c.has_faces = true;

@@ -144,8 +144,8 @@ struct Coefs {
 // transient device buffers of one connectivity / refinement / assembly pass,
 // kept with their owner so repeated passes reuse them
 struct Work {
-    DBuf<int32_t> cnt, is_row, big_list, big_count, packed, redo;
-    DBuf<int64_t> face_off, row_off;
+    DBuf<int32_t> cnt, big_list, big_count, packed, redo;
+    DBuf<int64_t> face_off;
     DBuf<unsigned char> scratch;
     DBuf<uint32_t> claim;
     DBuf<unsigned long long> counts, err;
