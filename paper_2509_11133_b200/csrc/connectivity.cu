@@ -240,10 +240,15 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                      const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
                      int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
                      int32_t* __restrict__ defer_count, unsigned long long* err) {
-    constexpr int CAP = 128 * E;  // > 3 * 32 E keys (load factor < 3/4)
+    // E = 1: lists of 64 candidates (a Kuhn vertex has ~36 edge and ~24 face
+    // candidates; a vertex with more is deferred to the E = 2 pass) and
+    // tables of 64 (keys <= list entries, so an insert always finds a slot);
+    // the small footprint keeps ~2x the warps resident.  E = 2: 3 candidates
+    // per incidence always fit.
+    constexpr int CAP = E == 1 ? 64 : 256;
     constexpr unsigned mask = CAP - 1;
-    constexpr int LCAP = 96 * E;  // list entries: 3 candidates per incidence
-    constexpr int R = 3 * E;      // rounds of 32 over a full list
+    constexpr int LCAP = E == 1 ? 64 : 192;
+    constexpr int R = LCAP / 32;  // rounds of 32 over a full list
     __shared__ int32_t s_ekey[kFastWarps][CAP], s_eval[kFastWarps][CAP];
     __shared__ unsigned long long s_fkey[kFastWarps][CAP];
     __shared__ int32_t s_flo[kFastWarps][CAP], s_fhi[kFastWarps][CAP], s_fcnt[kFastWarps][CAP];
@@ -346,7 +351,8 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                 const int32_t b = o[i];
                 const bool q = valid && b > v;
                 const unsigned bal = __ballot_sync(0xffffffffu, q);
-                if (q) el[ne_l + __popc(bal & lt)] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
+                const int pe = ne_l + __popc(bal & lt);
+                if (q && pe < LCAP) el[pe] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
                 ne_l += __popc(bal);
                 if (do_faces) {
                     const unsigned f = (ftab >> (6 * i)) & 63u;
@@ -357,14 +363,16 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     // count in bits 2+, orientation (x < y: 1, else 2) below:
                     // exactly one slot of each orientation sums to 11
-                    if (qf)
-                        fl[nf_l + __popc(balf & lt)] =
-                            make_int4(min(x, y), max(x, y), 4 * t + (int)(f & 3u), x < y ? 5 : 6);
+                    const int pf = nf_l + __popc(balf & lt);
+                    if (qf && pf < LCAP) fl[pf] = make_int4(min(x, y), max(x, y), 4 * t + (int)(f & 3u), x < y ? 5 : 6);
                     nf_l += __popc(balf);
                 }
             }
         }
         __syncwarp();
+        if (ne_l > LCAP || nf_l > LCAP) {  // too many candidates for this pass
+            if (lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
+        } else {
         // 2. inserts over the lists, all lanes busy
         int eh[R], fh[R];
 #pragma unroll
@@ -433,6 +441,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             }
         }
         __syncwarp();
+        }
         }
         P1 = P2;
         P2 = P3;
