@@ -189,18 +189,69 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(n=32):
-    """Reference CPU path (oracle/_ref) on a bounded sample of the workload."""
+def cpu_baseline(n=32, gpu_iterations=None, l_target=None):
+    """Reference CPU path (oracle/_ref) on a bounded sample of the workload,
+    stage by stage: connectivity, assemble_system,
+    build_schur(nproc) and build_schur(1), red_refine, and a 200-iteration
+    prefix of pcg_jacobi for the per-iteration cost."""
     try:
         m, RefCtx = reference_sample(n)
     except Exception as e:  # noqa: BLE001
         return {"value": None, "unit": "tets/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
     cores = os.cpu_count() or 1
-    sec, stages = reference_step(m, RefCtx, cores)
-    return {"value": m.ne / sec, "unit": "tets/s", "cores": cores, "kind": "reference",
-            "sample": (f"Kuhn {n}^3 x 6 = {m.ne} tets, one pass of num_edges + edge_pairs_to_elems + faces_up + "
-                       f"full_face_table + assemble_system + build_schur(workers={cores}) + red_refine in {sec:.2f} s; "
-                       f"only build_schur uses more than one thread")}
+    r = RefCtx(m)
+    t0 = time.perf_counter()
+    r.connectivity()
+    t1 = time.perf_counter()
+    r.assemble(3)
+    t2 = time.perf_counter()
+    r.build_schur(cores)
+    t3 = time.perf_counter()
+    r.refine()
+    t4 = time.perf_counter()
+    sec = t4 - t0
+    r2 = RefCtx(m)
+    r2.connectivity()
+    r2.assemble(3)
+    t5 = time.perf_counter()
+    r2.build_schur(1)
+    t6 = time.perf_counter()
+    cg_iters = 200
+    cg_s, _ = r2.cg_prefix(cg_iters)
+    l_sample = r2.counts()["l"]
+    out = {"value": m.ne / sec, "unit": "tets/s", "cores": cores, "kind": "reference",
+           "sample": (f"Kuhn {n}^3 x 6 = {m.ne} tets, one pass of num_edges + edge_pairs_to_elems + faces_up + "
+                      f"full_face_table + assemble_system + build_schur(workers={cores}) + red_refine in {sec:.2f} s; "
+                      f"only build_schur uses more than one thread"),
+           "stages_s": {"connectivity": t1 - t0, "assemble_system": t2 - t1, f"build_schur_{cores}": t3 - t2,
+                        "build_schur_1": t6 - t5, "red_refine": t4 - t3},
+           "cg_s_per_iteration": cg_s / cg_iters, "cg_sample_l": l_sample}
+    if gpu_iterations and l_target:
+        # labelled estimate (SURVEY 8(d)): per-iteration cost scaled by L,
+        # times the GPU-measured iteration count of the full problem
+        out["cg_full_estimate_s"] = cg_s / cg_iters * (l_target / l_sample) * gpu_iterations
+    return out
+
+
+def measure_fp64_peak(ph, torch, stream, iters=4096, reps=3):
+    """fp64 FMA throughput of this GPU (TFLOP/s, best of reps) from the
+    library's DFMA probe kernel, timed with CUDA events on its stream."""
+    import ctypes
+
+    fn = ph.lib().phfem_gpu_fp64_peak
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    sink = torch.zeros(1, dtype=torch.float64, device="cuda")
+    flops = ctypes.c_double()
+    best = 0.0
+    for _ in range(reps + 1):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn(iters, sink.data_ptr(), None, None, ctypes.byref(flops), stream.cuda_stream)
+        e1.record(stream)
+        e1.synchronize()
+        best = max(best, flops.value / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    return best
 
 
 # ------------------------------------------------------- multi-process
@@ -396,15 +447,27 @@ def main():
     # Schur solve (Jacobi-PCG, reference stopping rule), once
     solve = None
     if not args.no_solve:
+        # "Schur solve s" = CG + recovery + verify wall time;
+        # the CG alone is timed on the device
         r = mesh.solve_timed(cfg.problem, cfg.tol)
         b_it = B["cg_iteration"]
         gbs = b_it / (r["ms_per_iteration"] / 1e3) / 1e9 if r["ms_per_iteration"] else None
-        solve = {"seconds": r["cg_ms"] / 1e3, "iterations": r["iterations"], "converged": r["converged"],
+        solve = {"seconds": r["total_s"], "cg_seconds": r["cg_ms"] / 1e3, "iterations": r["iterations"],
+                 "converged": r["converged"], "accepted_by_verify": r["accepted"], "residual": r["residual"],
                  "ms_per_iteration": r["ms_per_iteration"], "gbs_per_iteration": gbs,
                  "hbm_frac": gbs / hbm if gbs else None, "tol": cfg.tol}
+        if not r["accepted"]:
+            solve["note"] = ("verify_solution refuses this converged solve, as the reference does "
+                             "(b_D = 0 here; SURVEY finding 8)")
+
+    fp64_peak = measure_fp64_peak(ph, torch, stream)
+    if "fp64" in roofline:
+        roofline["fp64"].update({"peak": fp64_peak, "peak_kind": "measured (DFMA probe kernel)",
+                                 "frac": roofline["fp64"]["achieved"] / fp64_peak})
 
     if rank == 0:
-        cpu = cpu_baseline() if (world == 1 and not args.no_cpu) else None
+        cpu = (cpu_baseline(gpu_iterations=solve["iterations"] if solve else None, l_target=l)
+               if (world == 1 and not args.no_cpu) else None)
         line = {
             "metric": METRIC, "value": value, "unit": "tets/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",

@@ -122,10 +122,13 @@ typedef struct phfem_stage_ms {
 int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
                    int64_t counts[5]);
 
-/* Schur solve only (assembly cached), timing the CG on the device.
- * out: [iterations, cg_ms, ms_per_iteration, converged] */
+/* Schur solve (assembly cached): Jacobi-PCG timed on the device, then
+ * recovery and verify_solution; a verify refusal (SURVEY finding 8) is
+ * reported, not raised.  out: [iterations, cg_ms, ms_per_iteration,
+ * converged, total_s (CG + recovery + verify wall time), accepted,
+ * residual, constraint_residual] */
 int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
-                      double out[4]);
+                      double out[8]);
 
 #ifdef __cplusplus
 }

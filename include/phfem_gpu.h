@@ -247,6 +247,10 @@ int phfem_gpu_sell_to_csr(int64_t l, const int32_t* sell_col, const double* sell
  * compared bit for bit with IEEE division; *mismatches (device) += count */
 int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream);
 
+/* fp64 FMA throughput probe: *flops = floating-point operations of one
+ * launch; time it between ev_begin / ev_end (cudaEvent_t, may be NULL) */
+int phfem_gpu_fp64_peak(int iters, double* sink, void* ev_begin, void* ev_end, double* flops, void* stream);
+
 /* kernels launched by this library since load (benchmark accounting) */
 long long phfem_gpu_launch_count(void);
 

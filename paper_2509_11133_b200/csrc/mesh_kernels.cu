@@ -189,7 +189,37 @@ __global__ void division_selftest(int64_t n, uint64_t seed, unsigned long long* 
     if (bad) atomicAdd(mismatches, bad);
 }
 
+// fp64 peak probe (roofline denominator of the fp64-bound assembly): 8
+// independent FMA chains per thread, a full resident grid, nothing but DFMA
+// in the loop
+__global__ void __launch_bounds__(256) fp64_peak_k(int iters, double seed, double* sink) {
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = seed + 1e-9 * (threadIdx.x + i);
+    const double b = 1.0 - 1e-12, c = 1e-15;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += a[i];
+    if (s == 123.456) sink[0] = s;  // keeps the chains alive
+}
+
 }  // namespace
+
+extern "C" int phfem_gpu_fp64_peak(int iters, double* sink, void* ev_begin, void* ev_end, double* flops,
+                                   void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int blocks = 148 * 8, threads = 256;
+    if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);
+    fp64_peak_k<<<blocks, threads, 0, s>>>(iters, 1.0, sink);
+    if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);
+    phg::count_launches(1);
+    if (flops) *flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+    return (int)cudaGetLastError();
+}
 
 extern "C" int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned long long* mismatches, void* stream) {
     division_selftest<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(n, seed, mismatches);

@@ -348,9 +348,12 @@ class Mesh:
         return {n: getattr(ms, n) for n, _ in StageMs._fields_}, counts
 
     def solve_timed(self, problem, tol=1e-10, max_iter=-1):
-        out = np.zeros(4)
+        """Schur solve with timings: CG on the device, then recovery + verify
+        (a verify refusal is reported as accepted=False, not raised)."""
+        out = np.zeros(8)
         _check(lib().phfem_solve_timed(self._h, problem, tol, max_iter, _ptr(out)))
-        return dict(iterations=int(out[0]), cg_ms=out[1], ms_per_iteration=out[2], converged=bool(out[3]))
+        return dict(iterations=int(out[0]), cg_ms=out[1], ms_per_iteration=out[2], converged=bool(out[3]),
+                    total_s=out[4], accepted=bool(out[5]), residual=out[6], constraint_residual=out[7])
 
 
 class Solution:
