@@ -128,15 +128,17 @@ __global__ void __launch_bounds__(kThreads)
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t base = (i >> 5) * (PHG_SELL_C * PHG_SELL_W) + (i & 31);
-        double s = 0.0;
+        // position 0 is the diagonal: its column is the row itself
+        const double pi = __ldg(p + i);
+        double s = __ldg(sell_val + base) * pi;
 #pragma unroll
-        for (int k = 0; k < PHG_SELL_W; ++k) {
+        for (int k = 1; k < PHG_SELL_W; ++k) {
             const int32_t c = __ldg(sell_col + base + k * PHG_SELL_C);
             const double v = __ldg(sell_val + base + k * PHG_SELL_C);
             s += v * __ldg(p + c);
         }
         q[i] = s;
-        acc[0] += p[i] * s;
+        acc[0] += pi * s;
     }
     double tot[1];
     if (!finish<1>(acc, partials, &st->counter[1], tot)) return;
@@ -157,9 +159,27 @@ __global__ void __launch_bounds__(kThreads)
     if (st->done) return;
     const double alpha = st->alpha;
     double acc[2] = {0.0, 0.0};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
-        const double pi = p[i];
-        x[i] += alpha * pi;
+    // two rows per thread and step (16 B accesses: twice the bytes in flight)
+    const int64_t l2 = l / 2;
+    const double2 *p2 = reinterpret_cast<const double2*>(p), *q2 = reinterpret_cast<const double2*>(q),
+                  *d2 = reinterpret_cast<const double2*>(d);
+    double2 *x2 = reinterpret_cast<double2*>(x), *r2 = reinterpret_cast<double2*>(r);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 pi = p2[i], qi = q2[i], di = d2[i], ri = r2[i];
+        double2 xi = x2[i];
+        xi.x += alpha * pi.x;
+        xi.y += alpha * pi.y;
+        x2[i] = xi;
+        const double ra = ri.x - alpha * qi.x, rb = ri.y - alpha * qi.y;
+        r2[i] = make_double2(ra, rb);
+        acc[0] += ra * ra;
+        acc[0] += rb * rb;
+        acc[1] += ra * (di.x * ra);
+        acc[1] += rb * (di.y * rb);
+    }
+    if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail row
+        const int64_t i = l - 1;
+        x[i] += alpha * p[i];
         const double ri = r[i] - alpha * q[i];
         r[i] = ri;
         acc[0] += ri * ri;
@@ -190,8 +210,14 @@ __global__ void __launch_bounds__(kThreads)
             const phg_cg_state* st) {
     if (st->done) return;
     const double beta = st->beta;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = d[i] * r[i] + beta * p[i];
+    const int64_t l2 = l / 2;
+    const double2 *r2 = reinterpret_cast<const double2*>(r), *d2 = reinterpret_cast<const double2*>(d);
+    double2* p2 = reinterpret_cast<double2*>(p);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 ri = r2[i], di = d2[i], pi = p2[i];
+        p2[i] = make_double2(di.x * ri.x + beta * pi.x, di.y * ri.y + beta * pi.y);
+    }
+    if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[l - 1] = d[l - 1] * r[l - 1] + beta * p[l - 1];
 }
 
 }  // namespace
