@@ -423,24 +423,32 @@ def main():
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
     hc, ht, hd, hn = pin(coords), pin(tets), pin(db), pin(nb)
     h2d = hc.nbytes + ht.nbytes + hd.nbytes + hn.nbytes
-    for _ in range(args.warmup):  # untimed: lets the device pool reach steady state
-        m2 = ph.Mesh.from_arrays(hc, ht, hd, hn)
-        m2.pipeline(cfg.problem, True)
-        del m2
+    def e2e_steps(n):
+        # double-buffered: step k+1's inputs go up on the copy engine
+        # (phfem_mesh_create_from_arrays_async) while step k's pass runs;
+        # every step still uploads its whole mesh and reads its counts back
+        nxt = ph.Mesh.from_arrays_async(hc, ht, hd, hn)
+        cts = None
+        for k in range(n):
+            cur = nxt
+            nxt = ph.Mesh.from_arrays_async(hc, ht, hd, hn) if k + 1 < n else None
+            _, cts = cur.pipeline(cfg.problem, True)
+            del cur
+        return cts
+
+    e2e_steps(args.warmup)  # untimed: lets the device pool reach steady state
     barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     t_wall = time.perf_counter()
-    for _ in range(args.steps):
-        m2 = ph.Mesh.from_arrays(hc, ht, hd, hn)
-        _, cts = m2.pipeline(cfg.problem, True)
-        del m2
+    cts = e2e_steps(args.steps)
     e3.record(stream)
     e3.synchronize()
     wall = (time.perf_counter() - t_wall) / args.steps
     e2e_ms = max(e2.elapsed_time(e3) / args.steps, wall * 1e3)
     e2e = {"value": job_throughput(world, ne, max_over_ranks(dist, e2e_ms, "cuda")), "unit": "tets/s",
+           "overlap": "double-buffered uploads on the copy engine (create_from_arrays_async)",
            "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(cts.nbytes + 7 * 8)}
 

@@ -30,6 +30,17 @@ int phfem_mesh_create_from_arrays(const double* coords, int64_t n_nodes, const i
                                   const int32_t* neumann, int64_t n_neu, int level,
                                   phfem_mesh** out);
 
+/* The same, returning before the upload completes: the copies (and the
+ * index check) run on a separate stream and copy engine, so a caller can
+ * stage the next mesh while the device still works on the previous one.
+ * The host arrays (page-locked for overlap) must stay valid and unchanged
+ * until the mesh's first use, which waits for the upload and reports an
+ * out-of-range index as PHFEM_ERR_INVALID_ARGUMENT. */
+int phfem_mesh_create_from_arrays_async(const double* coords, int64_t n_nodes, const int32_t* tetra,
+                                        int64_t n_elems, const int32_t* dirichlet, int64_t n_dir,
+                                        const int32_t* neumann, int64_t n_neu, int level,
+                                        phfem_mesh** out);
+
 /* n_x*n_y*n_z cells x 6 Kuhn tetrahedra on [0,lx]x[0,ly]x[0,lz], generated
  * on the device.  Interior nodes move by (2u-1)*jitter*h per axis with
  * u = (splitmix64(seed ^ (3n+axis)) >> 11) * 2^-53.  dirichlet_mask bit p

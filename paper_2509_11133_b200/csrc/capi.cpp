@@ -143,7 +143,12 @@ std::string stats_json(const std::string& method, int64_t n, int64_t l, int64_t 
 
 // Mesh handle: device mesh + lazily built connectivity and system caches.
 struct phfem_mesh {
-    std::shared_ptr<MeshData> data;
+    // the mesh; an asynchronous upload completes on first access
+    mutable std::shared_ptr<MeshData> data_;
+    std::shared_ptr<MeshData>& data() const {
+        if (data_ && data_->pending) finish_upload(*data_);
+        return data_;
+    }
     std::shared_ptr<Coefs> coef = std::make_shared<Coefs>();
     std::shared_ptr<Connectivity> conn;
     std::shared_ptr<System> sys;
@@ -154,7 +159,7 @@ struct phfem_mesh {
     const Connectivity& table() {
         if (!conn || !conn->has_faces) {
             auto c = std::make_shared<Connectivity>();
-            build_connectivity(*data, *c, true);
+            build_connectivity(*data(), *c, true);
             conn = c;
         }
         return *conn;
@@ -162,7 +167,7 @@ struct phfem_mesh {
     const Connectivity& edges() {
         if (!conn || !conn->has_edges) {
             auto c = std::make_shared<Connectivity>();
-            build_connectivity(*data, *c, false);
+            build_connectivity(*data(), *c, false);
             conn = c;
         }
         return *conn;
@@ -171,7 +176,7 @@ struct phfem_mesh {
         table();
         if (!sys || sys->problem != problem || sys->coef_version != coef->version || (debug && !sys->a_blocks.p)) {
             auto s = std::make_shared<System>();
-            assemble_system(*data, *coef, *conn, problem, *s, debug);
+            assemble_system(*data(), *coef, *conn, problem, *s, debug);
             sys = s;
         }
         return *sys;
@@ -210,7 +215,7 @@ phfem_solution* do_solve(phfem_mesh* m, int problem, const std::string& method, 
     auto snapshot_conn = (m->table(), m->conn);
     const System& sys = m->system(problem, false);
     auto sol = std::make_unique<phfem_solution>();
-    sol->mesh = m->data;
+    sol->mesh = m->data();
     sol->coef = m->coef;
     sol->conn = snapshot_conn;
     sol->problem = problem;
@@ -219,7 +224,7 @@ phfem_solution* do_solve(phfem_mesh* m, int problem, const std::string& method, 
     sol->n = sys.n;
     sol->l = sys.l;
     sol->peak_dim = peak_dim_override > 0 ? peak_dim_override : sys.l;
-    solve_schur(*m->data, *m->coef, *snapshot_conn, sys, problem, tol, max_iter, method, sol->res);
+    solve_schur(*m->data(), *m->coef, *snapshot_conn, sys, problem, tol, max_iter, method, sol->res);
     sol->stats = stats_json(method, sol->n, sol->l, sol->res.iterations, sol->res.residual,
                             sol->res.constraint_residual, sol->res.seconds, workers, sol->peak_dim);
     return sol.release();
@@ -235,7 +240,7 @@ int phfem_mesh_create_cube(phfem_mesh** out) {
     return guarded([&] {
         if (!out) throw InvalidArgument("null output handle");
         auto m = std::make_unique<phfem_mesh>();
-        m->data = cube_mesh();
+        m->data() = cube_mesh();
         *out = m.release();
     });
 }
@@ -246,7 +251,7 @@ int phfem_mesh_read(const char* path, phfem_mesh** out) {
         std::ifstream is(path);
         if (!is) throw IoError(std::string("cannot open '") + path + "' for reading");
         auto m = std::make_unique<phfem_mesh>();
-        m->data = read_mesh(is);
+        m->data() = read_mesh(is);
         *out = m.release();
     });
 }
@@ -256,7 +261,7 @@ int phfem_mesh_write(const phfem_mesh* mesh, const char* path) {
         if (!mesh || !path) throw InvalidArgument("null argument");
         std::ofstream os(path);
         if (!os) throw IoError(std::string("cannot open '") + path + "' for writing");
-        HostMesh h = to_host(*mesh->data);
+        HostMesh h = to_host(*mesh->data());
         write_mesh(os, h);
         if (!os) throw IoError(std::string("write failure on '") + path + "'");
     });
@@ -269,11 +274,11 @@ int phfem_mesh_refine(phfem_mesh* mesh, phfem_refine_times* times) {
         if (!mesh) throw InvalidArgument("null mesh");
         const auto t0 = std::chrono::steady_clock::now();
         Connectivity& c = const_cast<Connectivity&>(mesh->edges());
-        const int64_t ned = c.ned, ne = mesh->data->ne;
-        auto child = refine_mesh(*mesh->data, c, &mesh->last_map);
+        const int64_t ned = c.ned, ne = mesh->data()->ne;
+        auto child = refine_mesh(*mesh->data(), c, &mesh->last_map);
         mesh->map_ned = ned;
         mesh->map_ne = ne;
-        mesh->data = child;
+        mesh->data() = child;
         mesh->coef = std::make_shared<Coefs>();
         mesh->invalidate();
         if (times) {
@@ -283,15 +288,15 @@ int phfem_mesh_refine(phfem_mesh* mesh, phfem_refine_times* times) {
     });
 }
 
-int phfem_mesh_level(const phfem_mesh* mesh) { return mesh ? mesh->data->level : -1; }
+int phfem_mesh_level(const phfem_mesh* mesh) { return mesh ? mesh->data()->level : -1; }
 
 int phfem_mesh_counts(const phfem_mesh* mesh, int64_t* n_elems, int64_t* n_nodes, int64_t* n_edges,
                       int64_t* n_faces, phfem_refine_times* times) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         auto* m = const_cast<phfem_mesh*>(mesh);
-        if (n_elems) *n_elems = m->data->ne;
-        if (n_nodes) *n_nodes = m->data->nc;
+        if (n_elems) *n_elems = m->data()->ne;
+        if (n_nodes) *n_nodes = m->data()->nc;
         if (n_edges || n_faces || times) {
             const Connectivity& c = m->table();
             if (n_edges) *n_edges = c.ned;
@@ -310,7 +315,7 @@ int phfem_mesh_system_dims(const phfem_mesh* mesh, int64_t* n, int64_t* l) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         auto* m = const_cast<phfem_mesh*>(mesh);
-        if (n) *n = 4 * m->data->ne;
+        if (n) *n = 4 * m->data()->ne;
         if (l) *l = m->table().l;
     });
 }
@@ -318,7 +323,7 @@ int phfem_mesh_system_dims(const phfem_mesh* mesh, int64_t* n, int64_t* l) {
 int phfem_mesh_diameter(const phfem_mesh* mesh, double* h) {
     return guarded([&] {
         if (!mesh || !h) throw InvalidArgument("null argument");
-        *h = mesh_diameter(*mesh->data);
+        *h = mesh_diameter(*mesh->data());
     });
 }
 
@@ -366,7 +371,7 @@ int phfem_solve(const phfem_mesh* mesh, int problem, const char* solver, int wor
         int64_t peak = 0;
         if (name == "direct") {
             method = "direct";
-            peak = 4 * m->data->ne + m->table().l;
+            peak = 4 * m->data()->ne + m->table().l;
         } else if (name == "schur-parallel") {
             wk = w;
             method = w > 1 ? "schur-parallel" : "schur";
@@ -449,7 +454,7 @@ int phfem_export_vtk(const phfem_mesh* mesh, const phfem_solution* sol, const ch
         if (!mesh || !path) throw InvalidArgument("null argument");
         std::ofstream os(path);
         if (!os) throw IoError(std::string("cannot open '") + path + "' for writing");
-        const HostMesh h = to_host(*mesh->data);
+        const HostMesh h = to_host(*mesh->data());
         const size_t ne = h.tets.size() / 4;
         write_vtk_points(os, h);  // export_vtk, vtk.cpp:27-58
         os << "CELLS " << ne << ' ' << 5 * ne << "\n";
@@ -523,7 +528,7 @@ int phfem_dump_system(const phfem_mesh* mesh, int problem, const char* directory
         const std::vector<int32_t> mrow = sys.slot_mrow.download();
         const std::vector<double> rhs = sys.rhs.download();
         const std::vector<double> bd = sys.bd.download();
-        const int64_t ne = m->data->ne;
+        const int64_t ne = m->data()->ne;
         {  // system_a_csr dumped row-major (assembly.cpp:140-148, sparse.cpp:224-228)
             auto os = open(dir + "/a.txt");
             for (int64_t t = 0; t < ne; ++t)
@@ -567,9 +572,9 @@ int phfem_mesh_create_from_arrays(const double* coords, int64_t n_nodes, const i
         if (!out || (n_nodes && !coords) || (n_elems && !tetra) || (n_dir && !dirichlet) || (n_neu && !neumann))
             throw InvalidArgument("null argument");
         auto m = std::make_unique<phfem_mesh>();
-        m->data = upload_mesh(coords, n_nodes, tetra, n_elems, dirichlet, n_dir, neumann, n_neu, level);
+        m->data() = upload_mesh(coords, n_nodes, tetra, n_elems, dirichlet, n_dir, neumann, n_neu, level);
         // index range check on the device (the host copy stays untouched)
-        const MeshData& d = *m->data;
+        const MeshData& d = *m->data();
         DBuf<unsigned long long> bad(3);
         bad.fill_bytes(0xff);
         check(phfem_gpu_check_indices(d.tets.p, 4 * d.ne, d.nc, bad.p, SV()), "check indices");
@@ -585,12 +590,24 @@ int phfem_mesh_create_from_arrays(const double* coords, int64_t n_nodes, const i
     });
 }
 
+int phfem_mesh_create_from_arrays_async(const double* coords, int64_t n_nodes, const int32_t* tetra, int64_t n_elems,
+                                        const int32_t* dirichlet, int64_t n_dir, const int32_t* neumann,
+                                        int64_t n_neu, int level, phfem_mesh** out) {
+    return guarded([&] {
+        if (!out || (n_nodes && !coords) || (n_elems && !tetra) || (n_dir && !dirichlet) || (n_neu && !neumann))
+            throw InvalidArgument("null argument");
+        auto m = std::make_unique<phfem_mesh>();
+        m->data_ = upload_mesh_async(coords, n_nodes, tetra, n_elems, dirichlet, n_dir, neumann, n_neu, level);
+        *out = m.release();
+    });
+}
+
 int phfem_mesh_create_kuhn(int nx, int ny, int nz, double lx, double ly, double lz, double jitter, uint64_t seed,
                            uint32_t dirichlet_mask, phfem_mesh** out) {
     return guarded([&] {
         if (!out) throw InvalidArgument("null output handle");
         auto m = std::make_unique<phfem_mesh>();
-        m->data = kuhn_mesh(nx, ny, nz, lx, ly, lz, jitter, seed, dirichlet_mask);
+        m->data() = kuhn_mesh(nx, ny, nz, lx, ly, lz, jitter, seed, dirichlet_mask);
         *out = m.release();
     });
 }
@@ -598,10 +615,10 @@ int phfem_mesh_create_kuhn(int nx, int ny, int nz, double lx, double ly, double 
 int phfem_mesh_sizes(const phfem_mesh* mesh, int64_t out[4]) {
     return guarded([&] {
         if (!mesh || !out) throw InvalidArgument("null argument");
-        out[0] = mesh->data->nc;
-        out[1] = mesh->data->ne;
-        out[2] = mesh->data->nd;
-        out[3] = mesh->data->nn;
+        out[0] = mesh->data()->nc;
+        out[1] = mesh->data()->ne;
+        out[2] = mesh->data()->nd;
+        out[3] = mesh->data()->nn;
     });
 }
 
@@ -609,7 +626,7 @@ int phfem_mesh_get_arrays(const phfem_mesh* mesh, double* coords, int32_t* tetra
                           int32_t* neumann) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
-        const MeshData& d = *mesh->data;
+        const MeshData& d = *mesh->data();
         if (coords) d.coords.download_to(coords, 3 * d.nc);
         if (tetra) d.tets.download_to(tetra, 4 * d.ne);
         if (dirichlet) d.db.download_to(dirichlet, 3 * d.nd);
@@ -622,7 +639,7 @@ int phfem_mesh_set_coefficients(phfem_mesh* mesh, const double* a_elem, const do
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         auto k = std::make_shared<Coefs>();
-        const int64_t ne = mesh->data->ne;
+        const int64_t ne = mesh->data()->ne;
         if (a_diag) {
             k->a_diag.upload(a_diag, 3 * ne);
             k->has_diag = true;
@@ -656,7 +673,7 @@ int phfem_mesh_get_edges(const phfem_mesh* mesh, int32_t* edge_nodes, int32_t* e
         if (!mesh) throw InvalidArgument("null mesh");
         const Connectivity& c = const_cast<phfem_mesh*>(mesh)->edges();
         if (edge_nodes) c.edge_nodes.download_to(edge_nodes, 2 * c.ned);
-        if (edge_of_slot) c.edge_of_slot.download_to(edge_of_slot, 6 * mesh->data->ne);
+        if (edge_of_slot) c.edge_of_slot.download_to(edge_of_slot, 6 * mesh->data()->ne);
         phb::sync();
     });
 }
@@ -666,7 +683,7 @@ int phfem_mesh_get_faces(const phfem_mesh* mesh, int32_t* faces, int32_t* face_o
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
         const Connectivity& c = const_cast<phfem_mesh*>(mesh)->table();
-        const int64_t ne = mesh->data->ne;
+        const int64_t ne = mesh->data()->ne;
         if (faces) c.faces.download_to(faces, 3 * c.nf);
         if (face_of_slot) c.face_of_slot.download_to(face_of_slot, 4 * ne);
         if (sigma) c.sigma.download_to(sigma, 4 * ne);
@@ -722,7 +739,7 @@ int phfem_mesh_get_system(const phfem_mesh* mesh, double* a_blocks, double* slot
         if (!mesh) throw InvalidArgument("null mesh");
         if (!mesh->sys) throw InvalidArgument("phfem_mesh_assemble has not been called");
         const System& sys = *mesh->sys;
-        const int64_t ne = mesh->data->ne;
+        const int64_t ne = mesh->data()->ne;
         if ((a_blocks || slot_coef || slot_mrow) && !sys.a_blocks.p)
             throw InvalidArgument("element views were not kept");
         if (a_blocks) sys.a_blocks.download_to(a_blocks, 16 * ne);
@@ -767,7 +784,7 @@ int phfem_mesh_solve_faces(const phfem_mesh* mesh, int problem, double tol, int6
         auto* m = const_cast<phfem_mesh*>(mesh);
         const System& sys = m->system(problem, false);
         SolveResult r;
-        solve_schur(*m->data, *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r, true);
+        solve_schur(*m->data(), *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r, true);
         if (lambda) r.lambda.download_to(lambda, sys.l);
         phb::sync();
         out[0] = (double)r.iterations;
@@ -816,16 +833,16 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
         auto c = (mesh->conn && mesh->conn.use_count() == 1) ? mesh->conn : std::make_shared<Connectivity>();
         auto s = (mesh->sys && mesh->sys.use_count() == 1) ? mesh->sys : std::make_shared<System>();
         mesh->invalidate();
-        build_connectivity(*mesh->data, *c, true, &st);
+        build_connectivity(*mesh->data(), *c, true, &st);
         mesh->conn = c;
         if (do_assemble) {
-            assemble_system(*mesh->data, *mesh->coef, *c, problem, *s, false, &st);
+            assemble_system(*mesh->data(), *mesh->coef, *c, problem, *s, false, &st);
             mesh->sys = s;
         }
         int64_t ne_child = 0;
         if (do_refine) {
             if (!mesh->scratch_child) mesh->scratch_child = std::make_shared<MeshData>();
-            auto child = refine_mesh(*mesh->data, *c, nullptr, &st, mesh->scratch_child);
+            auto child = refine_mesh(*mesh->data(), *c, nullptr, &st, mesh->scratch_child);
             ne_child = child->ne;
         }
         const double tot = total.stop_ms();
@@ -858,7 +875,7 @@ int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t m
         SolveResult r;
         bool accepted = true;
         try {
-            solve_schur(*m->data, *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r,
+            solve_schur(*m->data(), *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r,
                         false);
         } catch (const SolverError& e) {
             // verify_solution's refusal of a converged solve (finding 8)

@@ -2,6 +2,8 @@
 // the device knows (nEd, nF, L) are read back once per stage; everything else
 // stays on the stream.  Device error slots are replayed in the reference's
 // check order so the same exception (and message shape) surfaces.
+#include <mutex>
+
 #include "runtime.hpp"
 
 #include <algorithm>
@@ -33,6 +35,7 @@ Runtime::Runtime() {
                         (e != cudaSuccess ? cudaGetErrorString(e) : "device count 0"));
     check(cudaGetDevice(&device), "get device");
     check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "create stream");
+    check(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking), "create stream");
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t threshold = UINT64_MAX;
@@ -158,6 +161,98 @@ std::string format_double(double v) {  // mesh.cpp:108-115
 }
 
 // ----------------------------------------------------------------- meshes
+
+// Page-locked result slots for the asynchronous index checks, allocated once:
+// cudaMallocHost / cudaFreeHost synchronise the device, which would serialise
+// an upload with the work it is meant to overlap.
+namespace {
+struct FlagSlots {
+    static constexpr int kSlots = 256;
+    std::mutex mu;
+    unsigned long long* base = nullptr;
+    std::vector<int> free_list;
+    unsigned long long* take() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!base) {
+            check(cudaMallocHost(reinterpret_cast<void**>(&base), kSlots * 4 * sizeof(unsigned long long)),
+                  "pinned alloc");
+            for (int i = kSlots - 1; i >= 0; --i) free_list.push_back(i);
+        }
+        if (free_list.empty()) throw MeshError("too many mesh uploads in flight");
+        const int i = free_list.back();
+        free_list.pop_back();
+        return base + 4 * i;
+    }
+    void give(unsigned long long* p) {
+        std::lock_guard<std::mutex> lk(mu);
+        free_list.push_back((int)((p - base) / 4));
+    }
+};
+FlagSlots& flag_slots() {
+    static FlagSlots s;
+    return s;
+}
+}  // namespace
+
+PendingUpload::~PendingUpload() {
+    if (ready) cudaEventDestroy(ready);
+    if (flags) flag_slots().give(flags);
+}
+
+std::shared_ptr<MeshData> upload_mesh_async(const double* coords, int64_t nc, const int32_t* tets, int64_t ne,
+                                            const int32_t* db, int64_t nd, const int32_t* nb, int64_t nn, int level) {
+    if (nc < 0 || ne < 0 || nd < 0 || nn < 0) throw InvalidArgument("negative mesh size");
+    if (6 * ne >= (int64_t)INT32_MAX) throw MeshError("mesh too large: 6 nE must stay below 2^31");
+    auto m = std::make_shared<MeshData>();
+    m->nc = nc;
+    m->ne = ne;
+    m->nd = nd;
+    m->nn = nn;
+    m->level = level;
+    auto pu = std::make_unique<PendingUpload>();
+    cudaStream_t s = SC();
+    m->coords.upload_on(coords, 3 * nc, s);
+    m->tets.upload_on(tets, 4 * ne, s);
+    m->db.upload_on(db, 3 * nd, s);
+    m->nb.upload_on(nb, 3 * nn, s);
+    // index range check on the copy stream, result to pinned memory
+    pu->flags = flag_slots().take();
+    pu->dflags.release();
+    pu->dflags.n = pu->dflags.cap = 3;
+    check(cudaMallocAsync(reinterpret_cast<void**>(&pu->dflags.p), 3 * sizeof(unsigned long long), s), "allocate");
+    check(cudaMemsetAsync(pu->dflags.p, 0xff, 3 * sizeof(unsigned long long), s), "memset");
+    check(phfem_gpu_check_indices(m->tets.p, 4 * ne, nc, pu->dflags.p, s), "check indices");
+    check(phfem_gpu_check_indices(m->db.p, 3 * nd, nc, pu->dflags.p + 1, s), "check indices");
+    check(phfem_gpu_check_indices(m->nb.p, 3 * nn, nc, pu->dflags.p + 2, s), "check indices");
+    check(cudaMemcpyAsync(pu->flags, pu->dflags.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaEventCreateWithFlags(&pu->ready, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(pu->ready, s), "event record");
+    pu->src[0] = tets;
+    pu->src[1] = db;
+    pu->src[2] = nb;
+    m->pending = std::move(pu);
+    return m;
+}
+
+MeshData::~MeshData() {
+    if (pending && pending->ready) {
+        cudaEventSynchronize(pending->ready);
+        cudaStreamWaitEvent(S(), pending->ready, 0);
+    }
+}
+
+void finish_upload(MeshData& m) {
+    if (!m.pending) return;
+    PendingUpload& pu = *m.pending;
+    check(cudaEventSynchronize(pu.ready), "upload");
+    // an invalid mesh stays pending: every later use fails the same way
+    for (int i = 0; i < 3; ++i)
+        if (pu.flags[i] != ~0ull)
+            throw InvalidArgument("node index " + std::to_string((long long)pu.src[i][pu.flags[i]] + 1) +
+                                  " out of range 1.." + std::to_string(m.nc));
+    check(cudaStreamWaitEvent(S(), pu.ready, 0), "wait upload");
+    m.pending.reset();
+}
 
 std::shared_ptr<MeshData> upload_mesh(const double* coords, int64_t nc, const int32_t* tets, int64_t ne,
                                       const int32_t* db, int64_t nd, const int32_t* nb, int64_t nn, int level) {

@@ -37,11 +37,13 @@ inline void check(int e, const char* what) { check(static_cast<cudaError_t>(e), 
 // One stream per process; every call synchronises on it before returning.
 struct Runtime {
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;  // asynchronous mesh uploads (copy engine)
     int device = 0;
     Runtime();
 };
 Runtime& rt();
 inline cudaStream_t S() { return rt().stream; }
+inline cudaStream_t SC() { return rt().copy; }
 inline void* SV() { return static_cast<void*>(rt().stream); }
 void sync();
 
@@ -96,6 +98,16 @@ struct DBuf {
         alloc(count);
         if (count) check(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, S()), "H2D");
     }
+    // allocation and copy ordered on another stream (the upload stream);
+    // users on the library stream wait for an event recorded after it
+    void upload_on(const T* h, int64_t count, cudaStream_t s) {
+        release();
+        n = cap = count;
+        if (count > 0) {
+            check(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * (size_t)count, s), "allocate");
+            check(cudaMemcpyAsync(p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, s), "H2D");
+        }
+    }
     std::vector<T> download() const {
         std::vector<T> h((size_t)n);
         if (n) check(cudaMemcpyAsync(h.data(), p, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, S()), "D2H");
@@ -126,13 +138,33 @@ struct Timer {
 
 // ---------------------------------------------------------------- objects
 
+// An upload still in flight on the copy stream (upload_mesh_async): the
+// event follows the copies, the index check and its D2H into `flags`.
+struct PendingUpload {
+    cudaEvent_t ready = nullptr;
+    unsigned long long* flags = nullptr;  // pinned [3]: first bad index per array
+    DBuf<unsigned long long> dflags;
+    const int32_t* src[3] = {nullptr, nullptr, nullptr};  // caller's arrays (messages)
+    ~PendingUpload();
+};
+
 struct MeshData {
     int64_t nc = 0, ne = 0, nd = 0, nn = 0;
     int level = 0;
     DBuf<double> coords;  // [3 nC]
     DBuf<int32_t> tets;   // [4 nE]
     DBuf<int32_t> db, nb; // [3 nD], [3 nN]
+    std::unique_ptr<PendingUpload> pending;
+    MeshData() = default;
+    MeshData(const MeshData&) = delete;
+    MeshData& operator=(const MeshData&) = delete;
+    ~MeshData();  // an unused pending upload is waited for before the free
 };
+
+// Completes an asynchronous upload before the mesh's first use: waits for
+// its event on the host (instant once the copy engine is done), replays the
+// index check, and orders the library stream after the upload.
+void finish_upload(MeshData& m);
 
 struct Coefs {
     DBuf<double> a_elem, a_diag;
@@ -223,6 +255,9 @@ struct Stages {
 
 std::shared_ptr<MeshData> upload_mesh(const double* coords, int64_t nc, const int32_t* tets, int64_t ne,
                                       const int32_t* db, int64_t nd, const int32_t* nb, int64_t nn, int level);
+// Host arrays must stay valid (and unchanged) until the mesh's first use.
+std::shared_ptr<MeshData> upload_mesh_async(const double* coords, int64_t nc, const int32_t* tets, int64_t ne,
+                                            const int32_t* db, int64_t nd, const int32_t* nb, int64_t nn, int level);
 std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly, double lz, double jitter,
                                     uint64_t seed, uint32_t mask);
 

@@ -95,6 +95,7 @@ def lib():
         "phfem_export_multiplier_vtk": [P, C.c_char_p],
         "phfem_dump_system": [P, C.c_int, C.c_char_p],
         "phfem_mesh_create_from_arrays": [P, I64, P, I64, P, I64, P, I64, C.c_int, PP],
+        "phfem_mesh_create_from_arrays_async": [P, I64, P, I64, P, I64, P, I64, C.c_int, PP],
         "phfem_mesh_create_kuhn": [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                    C.c_uint64, C.c_uint32, PP],
         "phfem_mesh_sizes": [P, P],
@@ -135,7 +136,7 @@ EXPORTED = [
     "phfem_mesh_dump_connectivity", "phfem_solve", "phfem_solution_destroy", "phfem_solution_values",
     "phfem_solution_stats_json", "phfem_solution_errors", "phfem_solution_write", "phfem_export_vtk",
     "phfem_export_multiplier_vtk", "phfem_dump_system",
-    "phfem_mesh_create_from_arrays", "phfem_mesh_create_kuhn", "phfem_mesh_sizes", "phfem_mesh_get_arrays",
+    "phfem_mesh_create_from_arrays", "phfem_mesh_create_from_arrays_async", "phfem_mesh_create_kuhn", "phfem_mesh_sizes", "phfem_mesh_get_arrays",
     "phfem_mesh_set_coefficients", "phfem_mesh_connectivity", "phfem_mesh_get_edges", "phfem_mesh_get_faces",
     "phfem_mesh_refinement_map", "phfem_mesh_assemble", "phfem_mesh_get_system", "phfem_solve_ex",
     "phfem_solution_stats", "phfem_solution_errors_ex", "phfem_stream", "phfem_pipeline", "phfem_solve_timed",
@@ -203,6 +204,22 @@ class Mesh:
         _check(lib().phfem_mesh_create_from_arrays(_ptr(coords), len(coords), _ptr(tets), len(tets), _ptr(db),
                                                    len(db), _ptr(nb), len(nb), level, C.byref(h)))
         return cls(h)
+
+    @classmethod
+    def from_arrays_async(cls, coords, tets, db, nb, level: int = 0) -> "Mesh":
+        """Upload on the copy engine while the device keeps working; the
+        arrays (page-locked for overlap) are kept alive by the returned mesh
+        and must not change until its first use."""
+        coords = np.ascontiguousarray(coords, dtype=np.float64).reshape(-1, 3)
+        tets = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+        db = np.ascontiguousarray(db, dtype=np.int32).reshape(-1, 3)
+        nb = np.ascontiguousarray(nb, dtype=np.int32).reshape(-1, 3)
+        h = C.c_void_p()
+        _check(lib().phfem_mesh_create_from_arrays_async(_ptr(coords), len(coords), _ptr(tets), len(tets), _ptr(db),
+                                                         len(db), _ptr(nb), len(nb), level, C.byref(h)))
+        m = cls(h)
+        m._host_arrays = (coords, tets, db, nb)
+        return m
 
     @classmethod
     def kuhn(cls, nx, ny, nz, lx=1.0, ly=1.0, lz=1.0, jitter=0.0, seed=2509, dirichlet_mask=0x3F) -> "Mesh":

@@ -342,3 +342,29 @@ def test_file_round_trip_and_exports(tmp_path):
     g.dump_system(0, str(tmp_path))
     for name in ("a.txt", "c.txt", "rhs.txt", "bd.txt"):
         assert (tmp_path / name).exists()
+
+
+def test_async_upload_matches_sync(oracle):
+    m = oracle.kuhn(3, 2, 2, jitter=0.2, dmask=0x5)
+    gs = to_gpu(m)
+    ga = ph.Mesh.from_arrays_async(m.coords, m.tets, m.db, m.nb)
+    # two uploads in flight, used in reverse order, one never used
+    gb = ph.Mesh.from_arrays_async(m.coords, m.tets, m.db, m.nb)
+    ph.Mesh.from_arrays_async(m.coords, m.tets, m.db, m.nb)
+    for g in (gb, ga):
+        for a, b in zip(g.arrays(), gs.arrays()):
+            assert np.array_equal(a, b)
+        en, eos = g.edges()
+        en_s, eos_s = gs.edges()
+        assert np.array_equal(en, en_s) and np.array_equal(eos, eos_s)
+        st, counts = g.pipeline(ph.PROBLEM_SIN3, True)
+        assert counts[4] == 12 * m.ne
+    # an out-of-range index surfaces at the first use, as in the sync path
+    bad = m.tets.copy()
+    bad[1, 2] = len(m.coords) + 5
+    gx = ph.Mesh.from_arrays_async(m.coords, bad, m.db, m.nb)
+    for _ in range(2):  # and at every later use
+        with pytest.raises(ph.ArgumentError, match="out of range"):
+            gx.edges()
+    with pytest.raises(ph.ArgumentError, match="out of range"):
+        ph.Mesh.from_arrays(m.coords, bad, m.db, m.nb)
