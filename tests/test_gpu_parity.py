@@ -368,3 +368,17 @@ def test_async_upload_matches_sync(oracle):
             gx.edges()
     with pytest.raises(ph.ArgumentError, match="out of range"):
         ph.Mesh.from_arrays(m.coords, bad, m.db, m.nb)
+
+
+@pytest.mark.parametrize("kind", [3, 4, 5])
+@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # orders 7, 8, 10, direct
+def test_small_element_load_paths(oracle, kind, h):
+    """The Taylor-series load vector (orders 7, 8, 10 by element size, see
+    problems.cuh taylor_order) against the oracle's libm evaluation: small
+    jittered Kuhn meshes with cells of size h, moved away from the origin so
+    that sin and cos are both far from zero."""
+    m = oracle.kuhn(3, 3, 2, lx=3 * h, ly=3 * h, lz=2 * h, jitter=0.2, dmask=0x15)
+    m = MeshArrays(m.coords + np.array([0.31, 0.17, 0.23]), m.tets, m.db, m.nb)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, kind=kind)
