@@ -31,7 +31,6 @@ __global__ void __launch_bounds__(kRefBlock)
                   int32_t* __restrict__ tets_out, int32_t* __restrict__ midpoint_node,
                   int32_t* __restrict__ centroid_node) {
     __shared__ int4 s_child[11 * kRefBlock];
-    __shared__ double s_xyz[3 * 7 * kRefBlock];
     const int64_t t0 = (int64_t)blockIdx.x * kRefBlock;
     const int64_t t = t0 + threadIdx.x;
     const int64_t tend = t0 + kRefBlock < ne ? t0 + kRefBlock : ne;
@@ -43,10 +42,9 @@ __global__ void __launch_bounds__(kRefBlock)
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
         const int64_t c = nc + t + edge_off[t];
         const V3 ct = vdiv(vadd(vadd(vadd(p[0], p[1]), p[2]), p[3]), 4.0);  // refine.cpp:33-34
-        int64_t loc = c - node0;
-        s_xyz[3 * loc] = ct.x;
-        s_xyz[3 * loc + 1] = ct.y;
-        s_xyz[3 * loc + 2] = ct.z;
+        coords_out[3 * c] = ct.x;
+        coords_out[3 * c + 1] = ct.y;
+        coords_out[3 * c + 2] = ct.z;
         if (centroid_node) centroid_node[t] = (int32_t)c;
         int32_t mid[6];
 #pragma unroll
@@ -60,10 +58,9 @@ __global__ void __launch_bounds__(kRefBlock)
                 const int a = k < 3 ? 0 : (k < 5 ? 1 : 2);
                 const int b = k < 3 ? k + 1 : (k < 5 ? k - 1 : 3);
                 const V3 pm = vdiv(vadd(p[a], p[b]), 2.0);  // refine.cpp:43
-                loc = node - node0;
-                s_xyz[3 * loc] = pm.x;
-                s_xyz[3 * loc + 1] = pm.y;
-                s_xyz[3 * loc + 2] = pm.z;
+                coords_out[3 * node] = pm.x;
+                coords_out[3 * node + 1] = pm.y;
+                coords_out[3 * node + 2] = pm.z;
                 if (midpoint_node) midpoint_node[id] = (int32_t)node;
             }
         }
@@ -88,9 +85,6 @@ __global__ void __launch_bounds__(kRefBlock)
     const int nrows = 11 * (int)(tend - t0);
     int4* dst = reinterpret_cast<int4*>(tets_out) + ne + 11 * t0;
     for (int r = threadIdx.x; r < nrows; r += kRefBlock) dst[r] = s_child[r];
-    const int nval = 3 * (int)(node1 - node0);
-    double* dxyz = coords_out + 3 * node0;
-    for (int r = threadIdx.x; r < nval; r += kRefBlock) dxyz[r] = s_xyz[r];
 }
 
 __global__ void __launch_bounds__(128)
