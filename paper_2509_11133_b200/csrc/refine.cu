@@ -34,9 +34,6 @@ __global__ void __launch_bounds__(kRefBlock)
     const int64_t t0 = (int64_t)blockIdx.x * kRefBlock;
     const int64_t t = t0 + threadIdx.x;
     const int64_t tend = t0 + kRefBlock < ne ? t0 + kRefBlock : ne;
-    // node run of this block: [node0, node1)
-    const int64_t node0 = nc + t0 + edge_off[t0];
-    const int64_t node1 = nc + tend + edge_off[tend];
     if (t < ne) {
         const int4 e = ldtet(tets, t);
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
@@ -47,11 +44,17 @@ __global__ void __launch_bounds__(kRefBlock)
         coords_out[3 * c + 2] = ct.z;
         if (centroid_node) centroid_node[t] = (int32_t)c;
         int32_t mid[6];
+        const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
+        const int2* eo2 = reinterpret_cast<const int2*>(edge_of_slot) + 3 * t;
+        const int2 f01 = __ldg(ef2), f23 = __ldg(ef2 + 1), f45 = __ldg(ef2 + 2);
+        const int2 o01 = __ldg(eo2), o23 = __ldg(eo2 + 1), o45 = __ldg(eo2 + 2);
+        const int32_t fs[6] = {f01.x, f01.y, f23.x, f23.y, f45.x, f45.y};
+        const int32_t os[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
             const int64_t s = 6 * t + k;
-            const int32_t first = edge_first[s];
-            const int32_t id = edge_of_slot[s];
+            const int32_t first = fs[k];
+            const int32_t id = os[k];
             const int64_t node = nc + first / 6 + 1 + id;
             mid[k] = (int32_t)node;
             if (first == (int32_t)s) {
@@ -103,11 +106,17 @@ __global__ void __launch_bounds__(128)
         coords_out[3 * c + 2] = ct.z;
         if (centroid_node) centroid_node[t] = (int32_t)c;
         int32_t mid[6];
+        const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
+        const int2* eo2 = reinterpret_cast<const int2*>(edge_of_slot) + 3 * t;
+        const int2 f01 = __ldg(ef2), f23 = __ldg(ef2 + 1), f45 = __ldg(ef2 + 2);
+        const int2 o01 = __ldg(eo2), o23 = __ldg(eo2 + 1), o45 = __ldg(eo2 + 2);
+        const int32_t fs[6] = {f01.x, f01.y, f23.x, f23.y, f45.x, f45.y};
+        const int32_t os[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
             const int64_t s = 6 * t + k;
-            const int32_t first = edge_first[s];
-            const int32_t id = edge_of_slot[s];
+            const int32_t first = fs[k];
+            const int32_t id = os[k];
             const int64_t node = nc + first / 6 + 1 + id;
             mid[k] = (int32_t)node;
             if (first == (int32_t)s) {
