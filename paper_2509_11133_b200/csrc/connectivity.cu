@@ -522,57 +522,24 @@ __device__ __forceinline__ uint32_t elem_mask(int64_t t, const int32_t* e6, cons
 __global__ void __launch_bounds__(kScanThreads)
     offsets_count_k(int64_t ne, const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
                     uint16_t* __restrict__ masks, long long* __restrict__ sums) {
-    const int64_t first = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    // striped over the tile (element base + i * kScanThreads + thread): the
+    // 24 B of edge_first and 16 B of slot_mate per element load coalesced,
+    // and the tile sum does not depend on the order
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
     long long se = 0, sf = 0;
-    uint32_t packed[kScanItems / 2];
-#pragma unroll
-    for (int c = 0; c < kScanItems / 4; ++c) {
-        // 4 elements: 24 edge slots (6 x int4) and 16 face slots (4 x int4)
-        const int64_t t0 = first + 4 * c;
-        uint32_t m[4] = {0, 0, 0, 0};
-        if (t0 + 4 <= ne) {
-            const int4* ef = reinterpret_cast<const int4*>(edge_first + 6 * t0);
-            int32_t e[24];
-#pragma unroll
-            for (int i = 0; i < 6; ++i) {
-                const int4 q = __ldg(ef + i);
-                e[4 * i] = q.x;
-                e[4 * i + 1] = q.y;
-                e[4 * i + 2] = q.z;
-                e[4 * i + 3] = q.w;
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                int4 q;
-                if (slot_mate) q = __ldg(reinterpret_cast<const int4*>(slot_mate) + t0 + j);
-                m[j] = elem_mask(t0 + j, e + 6 * j, slot_mate ? &q : nullptr);
-            }
-        } else {
-            for (int j = 0; j < 4; ++j) {
-                const int64_t t = t0 + j;
-                if (t >= ne) continue;
-                int32_t e[6];
-                for (int k = 0; k < 6; ++k) e[k] = edge_first[6 * t + k];
-                int4 q;
-                if (slot_mate) q = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-                m[j] = elem_mask(t, e, slot_mate ? &q : nullptr);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            se += __popc(m[j] & 63u);
-            sf += __popc(m[j] >> 6);
-        }
-        packed[2 * c] = m[0] | m[1] << 16;
-        packed[2 * c + 1] = m[2] | m[3] << 16;
-    }
-    if (first + kScanItems <= ne) {
-        uint4* o = reinterpret_cast<uint4*>(masks + first);
-        o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-    } else {
-        for (int i = 0; i < kScanItems; ++i)
-            if (first + i < ne) masks[first + i] = (uint16_t)(packed[i / 2] >> (16 * (i % 2)));
+#pragma unroll 4
+    for (int i = 0; i < kScanItems; ++i) {
+        const int64_t t = base + i * kScanThreads + threadIdx.x;
+        if (t >= ne) break;
+        const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
+        const int2 a01 = __ldg(ef2), a23 = __ldg(ef2 + 1), a45 = __ldg(ef2 + 2);
+        const int32_t e[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
+        int4 q;
+        if (slot_mate) q = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        const uint32_t m = elem_mask(t, e, slot_mate ? &q : nullptr);
+        masks[t] = (uint16_t)m;
+        se += __popc(m & 63u);
+        sf += __popc(m >> 6);
     }
     const long long s = block_sum_ll<kScanThreads>(se << 31 | sf);
     if (threadIdx.x == 0) sums[blockIdx.x] = s;
