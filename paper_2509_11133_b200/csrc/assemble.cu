@@ -435,9 +435,17 @@ __global__ void __launch_bounds__(kCondThreads)
 // clear the two-contributor accumulators (S diagonal, rhs_neg) of rows 0..l-1
 __global__ void __launch_bounds__(256) zero_rows_k(int64_t l, double* __restrict__ sell_val,
                                                    double* __restrict__ rhs_neg) {
-    for (int64_t R = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; R < l; R += (int64_t)gridDim.x * blockDim.x) {
-        sell_val[sell_idx(R, 0)] = 0.0;
-        rhs_neg[R] = 0.0;
+    // two rows per thread and step (16 B stores; rows 2i, 2i+1 share a slice)
+    const double2 z = make_double2(0.0, 0.0);
+    const int64_t l2 = l / 2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t R = 2 * i;
+        reinterpret_cast<double2*>(sell_val + sell_idx(R, 0))[0] = z;
+        reinterpret_cast<double2*>(rhs_neg)[i] = z;
+    }
+    if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        sell_val[sell_idx(l - 1, 0)] = 0.0;
+        rhs_neg[l - 1] = 0.0;
     }
 }
 
