@@ -17,11 +17,10 @@ namespace {
 
 using namespace phg;
 
-// Block-staged version: a block owns kRefBlock consecutive parents, whose
-// children 1..11 form one contiguous run of 11*kRefBlock rows and whose new
-// nodes (centroid + first-seen midpoints, in element order) form one
-// contiguous run of coordinates.  Both runs are assembled in shared memory
-// and streamed out with coalesced 16-byte stores.
+// A block owns kRefBlock consecutive parents, whose children 1..11 form one
+// contiguous run of 11*kRefBlock rows: they are assembled in shared memory
+// and streamed out with coalesced 16-byte stores.  The new nodes' 24-byte
+// coordinates are stored directly (staging them too halved the occupancy).
 constexpr int kRefBlock = 128;
 
 __global__ void __launch_bounds__(kRefBlock)
@@ -88,66 +87,6 @@ __global__ void __launch_bounds__(kRefBlock)
     const int nrows = 11 * (int)(tend - t0);
     int4* dst = reinterpret_cast<int4*>(tets_out) + ne + 11 * t0;
     for (int r = threadIdx.x; r < nrows; r += kRefBlock) dst[r] = s_child[r];
-}
-
-__global__ void __launch_bounds__(128)
-    refine_k(int64_t nc, int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets,
-             const int32_t* __restrict__ edge_first, const int32_t* __restrict__ edge_of_slot,
-             const int64_t* __restrict__ edge_off, double* __restrict__ coords_out, int32_t* __restrict__ tets_out,
-             int32_t* __restrict__ midpoint_node, int32_t* __restrict__ centroid_node) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
-        const int4 e = ldtet(tets, t);
-        const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
-        const int64_t c = nc + t + edge_off[t];
-        // centroid: (mesh.coords[e0] + e1 + e2 + e3) / 4.0  (refine.cpp:33-34)
-        const V3 ct = vdiv(vadd(vadd(vadd(p[0], p[1]), p[2]), p[3]), 4.0);
-        coords_out[3 * c] = ct.x;
-        coords_out[3 * c + 1] = ct.y;
-        coords_out[3 * c + 2] = ct.z;
-        if (centroid_node) centroid_node[t] = (int32_t)c;
-        int32_t mid[6];
-        const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
-        const int2* eo2 = reinterpret_cast<const int2*>(edge_of_slot) + 3 * t;
-        const int2 f01 = __ldg(ef2), f23 = __ldg(ef2 + 1), f45 = __ldg(ef2 + 2);
-        const int2 o01 = __ldg(eo2), o23 = __ldg(eo2 + 1), o45 = __ldg(eo2 + 2);
-        const int32_t fs[6] = {f01.x, f01.y, f23.x, f23.y, f45.x, f45.y};
-        const int32_t os[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
-#pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            const int64_t s = 6 * t + k;
-            const int32_t first = fs[k];
-            const int32_t id = os[k];
-            const int64_t node = nc + first / 6 + 1 + id;
-            mid[k] = (int32_t)node;
-            if (first == (int32_t)s) {
-                const int a = k < 3 ? 0 : (k < 5 ? 1 : 2);
-                const int b = k < 3 ? k + 1 : (k < 5 ? k - 1 : 3);
-                const V3 pm = vdiv(vadd(p[a], p[b]), 2.0);  // refine.cpp:43
-                coords_out[3 * node] = pm.x;
-                coords_out[3 * node + 1] = pm.y;
-                coords_out[3 * node + 2] = pm.z;
-                if (midpoint_node) midpoint_node[id] = (int32_t)node;
-            }
-        }
-        const int32_t i = e.x, j = e.y, k = e.z, l = e.w;
-        const int32_t ij = mid[0], ik = mid[1], il = mid[2], jk = mid[3], jl = mid[4], kl = mid[5];
-        const int32_t cc = (int32_t)c;
-        // the 12 children of refine.cpp:58-61; child 0 keeps slot t
-        int4* out = reinterpret_cast<int4*>(tets_out);
-        out[t] = make_int4(i, ij, ik, il);
-        int4* rest = out + ne + 11 * t;
-        rest[0] = make_int4(j, jk, ij, jl);
-        rest[1] = make_int4(k, ik, jk, kl);
-        rest[2] = make_int4(l, kl, jl, il);
-        rest[3] = make_int4(ij, ik, il, cc);
-        rest[4] = make_int4(jk, ij, jl, cc);
-        rest[5] = make_int4(ik, jk, kl, cc);
-        rest[6] = make_int4(kl, jl, il, cc);
-        rest[7] = make_int4(ij, jk, ik, cc);
-        rest[8] = make_int4(ik, kl, il, cc);
-        rest[9] = make_int4(ij, il, jl, cc);
-        rest[10] = make_int4(kl, jk, jl, cc);
-    }
 }
 
 // midpoint node of the mesh edge (a, b) through the star of min(a, b), or -1
