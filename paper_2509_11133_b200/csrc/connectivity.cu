@@ -217,10 +217,10 @@ constexpr int kFastWarps = 4;
 //   neighbour i (i < 3) = the i-th other local vertex in ascending order;
 //   edge ids  0xb15663088 >> 9 lv, 3 bits per i: local edge (lv, neighbour i)
 //             in the (0,1)(0,2)(0,3)(1,2)(1,3)(2,3) order;
-//   faces     6 bits per i: local face k (bits 0-1) containing lv and the
-//             neighbour positions of x (bits 2-3) and y (bits 4-5), the
-//             vertices following lv in that face's oriented cycle:
-//             lv 0: 0xa950, 1: 0x1b884, 2: 0x27250, 3: 0x1b1a1.
+//   faces     the face containing lv but not neighbour i is local face k,
+//             0x9c72c9 >> 6 lv, 2 bits per i; its other vertices are
+//             neighbours i+1, i+2 (mod 3), the first of them following lv
+//             in the face's oriented cycle for even lv, the second for odd.
 
 // E incidences per lane: E = 1 handles stars of <= 32 incidences (all Kuhn
 // vertices), E = 2 those of <= 64 (refined meshes reach 36).  Vertices come
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             // oriented cycle) among them; 3-bit / 6-bit packed per lv
             const int32_t o[3] = {lv == 0 ? tet.y : tet.x, lv <= 1 ? tet.z : tet.y, lv <= 2 ? tet.w : tet.z};
             const unsigned etab = (unsigned)(0xb15663088ull >> (9 * lv));
-            const unsigned ftab = lv == 0 ? 0xa950u : (lv == 1 ? 0x1b884u : (lv == 2 ? 0x27250u : 0x1b1a1u));
+            const unsigned ktab = (unsigned)(0x9c72c9u >> (6 * lv)) & 63u;
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int32_t b = o[i];
@@ -355,16 +355,18 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                 if (q && pe < LCAP) el[pe] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
                 ne_l += __popc(bal);
                 if (do_faces) {
-                    const unsigned f = (ftab >> (6 * i)) & 63u;
-                    const unsigned px = (f >> 2) & 3u, py = f >> 4;
-                    const int32_t x = px == 0 ? o[0] : (px == 1 ? o[1] : o[2]);
-                    const int32_t y = py == 0 ? o[0] : (py == 1 ? o[1] : o[2]);
-                    const bool qf = valid && x > v && y > v;
+                    // the face of lv without neighbour i: the other two
+                    // neighbours a, b; the vertex following lv in its
+                    // oriented cycle is a for even lv, b for odd lv
+                    const int32_t a = o[(i + 1) % 3], b = o[(i + 2) % 3];
+                    const int32_t lo = min(a, b), hi = max(a, b);
+                    const bool qf = valid && lo > v;
                     const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     // count in bits 2+, orientation (x < y: 1, else 2) below:
                     // exactly one slot of each orientation sums to 11
+                    const bool xy = (lv & 1) ? b < a : a < b;
                     const int pf = nf_l + __popc(balf & lt);
-                    if (qf && pf < LCAP) fl[pf] = make_int4(min(x, y), max(x, y), 4 * t + (int)(f & 3u), x < y ? 5 : 6);
+                    if (qf && pf < LCAP) fl[pf] = make_int4(lo, hi, 4 * t + (int)((ktab >> (2 * i)) & 3u), xy ? 5 : 6);
                     nf_l += __popc(balf);
                 }
             }
