@@ -382,3 +382,19 @@ def test_small_element_load_paths(oracle, kind, h):
     g = to_gpu(m)
     fo = check_connectivity(g, m, oracle)
     check_system(g, m, fo, oracle, kind=kind)
+
+
+def test_config2_level5_bit_exact(oracle):
+    """Config 2's ladder (1 cube -> 6 Kuhn tets, red refinement) to level 5
+    (1.49M tets) on the GPU vs the oracle: refined coordinates/elements/
+    boundary lists and the full edge and face tables bit for bit (SURVEY
+    8(c): bit-exact comparison at the levels the oracle can hold)."""
+    m = oracle.kuhn(1, 1, 1, dmask=0x3F)
+    g = to_gpu(m)
+    for _ in range(5):
+        m = oracle.refine(m)[0]
+        g.refine()
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(m, k)), k
+    check_connectivity(g, m, oracle)
