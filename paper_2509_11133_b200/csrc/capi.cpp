@@ -826,6 +826,7 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
         const bool do_refine = flags & PHFEM_PIPE_REFINE;
         const bool do_assemble = !(flags & PHFEM_PIPE_NO_ASSEMBLY);
         Stages st;
+        st.defer = true;  // error checks at the end of the pass (one synchronisation)
         Timer total;
         total.start();
         // rebuild everything; reuse the previous pass's device memory when no
@@ -846,7 +847,12 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
             ne_child = child->ne;
         }
         const double tot = total.stop_ms();
-        st.resolve();
+        try {
+            st.resolve();  // deferred assembly / refinement error checks
+        } catch (...) {
+            mesh->invalidate();  // the cached system is not valid
+            throw;
+        }
         if (ms) {
             ms->star = st.star;
             ms->groups = st.groups;

@@ -165,7 +165,13 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_face_class(nf, m.nd, w.claim.p, c.face_slots.p, c.face_class.p, w.counts.p, w.scratch.p,
                                reinterpret_cast<int64_t*>(w.counts.p + 3), w.err.p, SV()),
           "face class");
-    const auto cnt = read_many<unsigned long long, 4>({w.counts.p, w.counts.p + 1, w.counts.p + 2, w.counts.p + 3});
+    // the class counts and every connectivity error slot in one read (face
+    // rows below report nothing)
+    static_assert(PHG_ERR_COUNT == 7, "error slots");
+    const auto cnt = read_many<unsigned long long, 11>(
+        {w.counts.p, w.counts.p + 1, w.counts.p + 2, w.counts.p + 3, w.err.p, w.err.p + 1, w.err.p + 2,
+         w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6});
+    replay_connectivity_errors(std::vector<unsigned long long>(cnt.begin() + 4, cnt.end()), m, c);
     c.n_int = (int64_t)cnt[0];
     c.n_dir = (int64_t)cnt[1];
     c.n_neu = (int64_t)cnt[2];
@@ -174,7 +180,6 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     c.row_face.alloc(c.l);
     check(phfem_gpu_face_rows(nf, c.face_class.p, w.scratch.p, c.face_mrow.p, c.row_face.p, SV()), "face rows");
     if (st) st->span(&st->classify, t0);
-    replay_connectivity_errors(w.err.download(), m, c);
     c.has_faces = true;
     c.t_faces = std::chrono::duration<double>(std::chrono::steady_clock::now() - w1).count();
 }
@@ -217,16 +222,23 @@ std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, Refine
                                     c.edge_of_slot.p, out->nb.p, w.err.p, SV()),
           "refine boundary");
     if (st) st->span(&st->refine, t0);
-    const auto e = w.err.download();
-    if (e[PHG_ERR_BOUNDARY_EDGE] != kNone) {
-        const int64_t i = (int64_t)(e[PHG_ERR_BOUNDARY_EDGE] >> 2);
-        const int q = (int)(e[PHG_ERR_BOUNDARY_EDGE] & 3);
-        int32_t tri[3];
-        const bool dir = i < m.nd;
-        fetch_tri(dir ? m.db.p : m.nb.p, dir ? i : i - m.nd, tri);
-        const int32_t a = q == 1 ? tri[1] : tri[0], b = q == 0 ? tri[1] : tri[2];
-        throw MeshError("inconsistent mesh: boundary face edge (" + std::to_string(a + 1) + "," +
-                        std::to_string(b + 1) + ") is not an element edge");
+    auto replay = [&m](const unsigned long long* e) {
+        if (e[PHG_ERR_BOUNDARY_EDGE] != kNone) {
+            const int64_t i = (int64_t)(e[PHG_ERR_BOUNDARY_EDGE] >> 2);
+            const int q = (int)(e[PHG_ERR_BOUNDARY_EDGE] & 3);
+            int32_t tri[3];
+            const bool dir = i < m.nd;
+            fetch_tri(dir ? m.db.p : m.nb.p, dir ? i : i - m.nd, tri);
+            const int32_t a = q == 1 ? tri[1] : tri[0], b = q == 0 ? tri[1] : tri[2];
+            throw MeshError("inconsistent mesh: boundary face edge (" + std::to_string(a + 1) + "," +
+                            std::to_string(b + 1) + ") is not an element edge");
+        }
+    };
+    if (st && st->defer) {
+        st->defer_errors(w.err.p, replay);  // m outlives the pass (the caller's mesh)
+    } else {
+        const auto e = w.err.download();
+        replay(e.data());
     }
     return out;
 }
@@ -289,12 +301,19 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
         st->span(&st->assemble, t0);
         st->span(&st->assemble_kernel, ka, kb);
     }
-    const auto e = w.err.download();
     // assembly.cpp:13-14 (first element in order), then solver.cpp:128-129
-    if (e[PHG_ERR_ZERO_VOLUME] != kNone)
-        throw MeshError("degenerate element " + std::to_string(e[PHG_ERR_ZERO_VOLUME] + 1) + " (zero volume)");
-    if (e[PHG_ERR_SINGULAR] != kNone)
-        throw MeshError("degenerate element block " + std::to_string(e[PHG_ERR_SINGULAR] + 1));
+    auto replay = [](const unsigned long long* e) {
+        if (e[PHG_ERR_ZERO_VOLUME] != kNone)
+            throw MeshError("degenerate element " + std::to_string(e[PHG_ERR_ZERO_VOLUME] + 1) + " (zero volume)");
+        if (e[PHG_ERR_SINGULAR] != kNone)
+            throw MeshError("degenerate element block " + std::to_string(e[PHG_ERR_SINGULAR] + 1));
+    };
+    if (st && st->defer) {
+        st->defer_errors(w.err.p, replay);
+    } else {
+        const auto e = w.err.download();
+        replay(e.data());
+    }
 }
 
 }  // namespace phb

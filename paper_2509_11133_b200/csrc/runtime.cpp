@@ -83,9 +83,27 @@ cudaEvent_t Stages::mark() {
 }
 void Stages::span(double* field, cudaEvent_t from) { pending_.emplace_back(field, from, mark()); }
 void Stages::span(double* field, cudaEvent_t from, cudaEvent_t to) { pending_.emplace_back(field, from, to); }
+namespace {
+// page-locked slots for deferred error reads (allocated once: cudaMallocHost
+// synchronises the device)
+unsigned long long* err_slot(size_t i) {
+    constexpr size_t kSlots = 16;
+    static thread_local unsigned long long* base = nullptr;
+    if (!base) check(cudaMallocHost(reinterpret_cast<void**>(&base), kSlots * 8 * sizeof(unsigned long long)), "pinned");
+    if (i >= kSlots) throw MeshError("too many deferred error checks");
+    return base + 8 * i;
+}
+}  // namespace
+
+void Stages::defer_errors(const unsigned long long* dev_err, std::function<void(const unsigned long long*)> f) {
+    unsigned long long* h = err_slot(checks_.size());
+    check(cudaMemcpyAsync(h, dev_err, PHG_ERR_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost, S()),
+          "D2H");
+    checks_.emplace_back(h, std::move(f));
+}
+
 void Stages::resolve() {
-    if (pending_.empty()) return;
-    check(cudaEventSynchronize(std::get<2>(pending_.back())), "event sync");
+    if (pending_.empty() && checks_.empty()) return;
     sync();
     for (auto& [field, a, b] : pending_) {
         float ms = 0.f;
@@ -93,6 +111,9 @@ void Stages::resolve() {
         *field += ms;
     }
     pending_.clear();
+    auto checks = std::move(checks_);
+    checks_.clear();
+    for (auto& [h, f] : checks) f(h);
 }
 double Timer::stop_ms() {
     check(cudaEventRecord(b, S()), "event record");

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -243,12 +244,19 @@ struct Stages {
     void span(double* field, cudaEvent_t from);
     // adds the time between two recorded events to *field
     void span(double* field, cudaEvent_t from, cudaEvent_t to);
+    // resolve() also runs the error checks deferred with defer_errors()
     void resolve();
+    // Deferred error checks (one synchronisation for the whole pass): the
+    // device error slots are copied into page-locked memory now and `check`
+    // runs on them in resolve(); only when `defer` is set.
+    bool defer = false;
+    void defer_errors(const unsigned long long* dev_err, std::function<void(const unsigned long long*)> check);
 
   private:
     std::vector<cudaEvent_t> events_;
     size_t used_ = 0;
     std::vector<std::tuple<double*, cudaEvent_t, cudaEvent_t>> pending_;
+    std::vector<std::pair<unsigned long long*, std::function<void(const unsigned long long*)>>> checks_;
 };
 
 // --------------------------------------------------------------- pipeline
