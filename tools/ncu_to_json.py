@@ -19,6 +19,7 @@ METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed": "mem_throughput",
     "launch__registers_per_thread": "registers",
+    "smsp__inst_executed.sum": "warp_inst",
 }
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
@@ -55,6 +56,7 @@ def facts(rep):
             "warps_active_frac": v.get("warps_active"),
             "mem_throughput_frac": v.get("mem_throughput"),
             "registers": v.get("registers"),
+            "warp_instructions": v.get("warp_inst"),
         }
     for k, flop in fp64_flops(rep).items():
         if k in res:
