@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             }
         }
         __syncwarp();
+        const int nl_max = max(ne_l, nf_l);
         if (ne_l > LCAP || nf_l > LCAP) {  // too many candidates for this pass
             if (lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
         } else {
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
         int eh[R], fh[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if (E > 1 && 32 * r >= nl_max) break;  // warp-uniform: only the rounds in use
             eh[r] = fh[r] = -1;
             const int j = lane + 32 * r;
             if (j < ne_l) {
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
         // 3. read-back: every listed slot gets its group's result
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if (E > 1 && 32 * r >= nl_max) break;  // warp-uniform: only the rounds in use
             const int j = lane + 32 * r;
             if (eh[r] >= 0) edge_first[el[j].y] = eval[eh[r]];
             if (fh[r] >= 0) {
@@ -431,6 +434,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
         // 4. reset the touched table entries
 #pragma unroll
         for (int r = 0; r < R; ++r) {
+            if (E > 1 && 32 * r >= nl_max) break;  // warp-uniform: only the rounds in use
             if (eh[r] >= 0) {
                 ekey[eh[r]] = -1;
                 eval[eh[r]] = INT_MAX;
