@@ -371,7 +371,7 @@ def test_async_upload_matches_sync(oracle):
 
 
 @pytest.mark.parametrize("kind", [3, 4, 5])
-@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # orders 7, 8, 10, direct
+@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # orders 6 (economised), 8, 10, direct
 def test_small_element_load_paths(oracle, kind, h):
     """The Taylor-series load vector (orders 7, 8, 10 by element size, see
     problems.cuh taylor_order) against the oracle's libm evaluation: small
