@@ -180,8 +180,8 @@ __device__ __forceinline__ void load_vector(const V3 p[4], const Coef& k, double
                                       axis_zmax(p[0].z, p[1].z, p[2].z, p[3].z)));
         switch (taylor_order(zmax)) {
             case 6: load_taylor<KIND, 6>(p, cpre, k, vol, b); break;
-            case 8: load_taylor<KIND, 8>(p, cpre, k, vol, b); break;
-            case 10: load_taylor<KIND, 10>(p, cpre, k, vol, b); break;
+            case 7: load_taylor<KIND, 7>(p, cpre, k, vol, b); break;
+            case 9: load_taylor<KIND, 9>(p, cpre, k, vol, b); break;
             default:
 #pragma unroll 2
                 for (int qp = 0; qp < 64; ++qp) {

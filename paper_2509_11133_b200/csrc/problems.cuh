@@ -115,65 +115,66 @@ __device__ __forceinline__ double prob_f_fast(double x, double y, double z, doub
 // whose coefficients are formed once per element from sinpi/cospi/exp at x0;
 // one quadrature point then costs 3 + N FMA per axis.  All derivatives of
 // these g are bounded by 1 (trig) or e^x0 e^|delta| (exp), so the truncation
-// error is below zmax^(N+1)/(N+1)! relative; taylor_order() picks N with that
-// bound under 1e-17 (< ulp(1)/20), or the economised order 6 below for the
-// smallest elements.  Elements with zmax > 0.12 keep the direct
-// sinpi/cospi/exp evaluation.
+// error of the plain series is below zmax^(N+1)/(N+1)!; the economised
+// series below do better at one order less.  Elements with zmax > 0.12 keep
+// the direct sinpi/cospi/exp evaluation.
 enum { kTaySin = 0, kTayCos = 1, kTayExp = 2 };
 template <int N>
 struct AxisTaylor {
     double k[N + 1];
     double e1, e2, e3;
 };
-__device__ __forceinline__ double inv_fact(int n) {
-    constexpr double f[11] = {1.0,
-                              1.0,
-                              1.0 / 2.0,
-                              1.0 / 6.0,
-                              1.0 / 24.0,
-                              1.0 / 120.0,
-                              1.0 / 720.0,
-                              1.0 / 5040.0,
-                              1.0 / 40320.0,
-                              1.0 / 362880.0,
-                              1.0 / 3628800.0};
-    return f[n];
-}
 // |z| bound of one axis (pi-scaled; also bounds the exp axis' |delta|)
 __device__ __forceinline__ double axis_zmax(double x0, double x1, double x2, double x3) {
     return kPi * fmax(fabs(x1 - x0), fmax(fabs(x2 - x0), fabs(x3 - x0)));
 }
-// Order-6 class for |z| <= 0.028: the degree-8 cos and degree-7 sin / exp
-// series economised by one Chebyshev step each (T8 / T7 on [-0.028, 0.028]),
-// i.e. the same magnitudes as 1/n! with tiny corrections.  Measured against
-// mpmath over the interval: cos 7e-20, sin 4.2e-17, exp 5.0e-17 (relative),
-// below half an ulp; the plain Taylor order 6 would leave ~3e-15.
-__device__ __forceinline__ double econ6_trig(int n) {  // |coefficient| of z^n in sin(a + z)'s cycle
-    constexpr double c[7] = {1.0,
-                             0x1.fffffffffffa2p-1,
-                             0x1.fffffffffffcap-2,
-                             0x1.55555551aab14p-3,
-                             0x1.55555552b6e02p-5,
-                             0x1.110ec879513c9p-7,
-                             0x1.6c142550f260ep-10};
-    return c[n];
+// The series are Chebyshev-economised: the Taylor series one degree higher
+// with its top term replaced through T_{N+1} on [-zmax, zmax] (the same
+// magnitudes as 1/n! with tiny corrections).  Classes and their errors
+// measured against mpmath over the interval (relative):
+//   N = 6, |z| <= 0.028: cos 7e-20, sin 4.2e-17, exp 5.0e-17
+//   N = 7, |z| <= 0.05:  cos 7.6e-18, sin 5.4e-18, exp 1.2e-17
+//   N = 9, |z| <= 0.12:  cos 3.4e-19, sin 1.9e-18, exp 2.0e-18
+// all below half an ulp (plain Taylor at these orders would leave up to
+// ~3e-15).  Table entry n = |coefficient of z^n| (the sign comes from the
+// derivative cycle of sin / cos; all positive for exp).
+template <int N>
+__device__ __forceinline__ double econ_trig(int n) {
+    if constexpr (N == 6) {
+        constexpr double c[7] = {1.0, 0x1.fffffffffffa2p-1, 0x1.fffffffffffcap-2, 0x1.55555551aab14p-3,
+                                 0x1.55555552b6e02p-5, 0x1.110ec879513c9p-7, 0x1.6c142550f260ep-10};
+        return c[n];
+    } else if constexpr (N == 7) {
+        constexpr double c[8] = {1.0, 1.0, 0x1.ffffffffff92fp-2, 0x1.5555555555555p-3, 0x1.5555553ab3ecdp-5,
+                                 0x1.1111111111111p-7, 0x1.6c0e6efb6a97fp-10, 0x1.a01a01a01a01ap-13};
+        return c[n];
+    } else {
+        constexpr double c[10] = {1.0, 1.0, 0x1.fffffffffffebp-2, 0x1.5555555555555p-3, 0x1.555555553eb70p-5,
+                                  0x1.1111111111111p-7, 0x1.6c16bf4655446p-10, 0x1.a01a01a01a01ap-13,
+                                  0x1.9fef65c59e4bfp-16, 0x1.71de3a556c734p-19};
+        return c[n];
+    }
 }
-__device__ __forceinline__ double econ6_exp(int n) {
-    constexpr double c[7] = {1.0,
-                             0x1.000000000002fp+0,
-                             0x1.0000000000000p-1,
-                             0x1.55555551aab14p-3,
-                             0x1.5555555555555p-5,
-                             0x1.111359a8d0e59p-7,
-                             0x1.6c16c16c16c17p-10};
-    return c[n];
+template <int N>
+__device__ __forceinline__ double econ_exp(int n) {
+    if constexpr (N == 6) {
+        constexpr double c[7] = {1.0, 0x1.000000000002fp+0, 0x1.0000000000000p-1, 0x1.55555551aab14p-3,
+                                 0x1.5555555555555p-5, 0x1.111359a8d0e59p-7, 0x1.6c16c16c16c17p-10};
+        return c[n];
+    } else if constexpr (N == 7) {
+        constexpr double c[8] = {1.0, 1.0, 0x1.0000000000369p-1, 0x1.5555555555555p-3, 0x1.5555553ab3ecdp-5,
+                                 0x1.1111111111111p-7, 0x1.6c1f13dcc2eaep-10, 0x1.a01a01a01a01ap-13};
+        return c[n];
+    } else {
+        constexpr double c[10] = {1.0, 1.0, 0x1.fffffffffffebp-2, 0x1.5555555555555p-3, 0x1.555555556bf3bp-5,
+                                  0x1.1111111111111p-7, 0x1.6c16bf4655446p-10, 0x1.a01a01a01a01ap-13,
+                                  0x1.a0449d7a95b75p-16, 0x1.71de3a556c734p-19};
+        return c[n];
+    }
 }
-// 0 = out of range (direct evaluation)
+// 0 = out of range (direct evaluation by sinpi / cospi / exp)
 __device__ __forceinline__ int taylor_order(double zmax) {
-    // economised order 6 (above); Taylor 0.05^9/9! = 5.4e-18,
-    // 0.12^11/11! = 1.9e-18; coarser elements (small meshes) take the
-    // direct evaluation
-    return zmax <= 0.028 ? 6 : (zmax <= 0.05 ? 8 : (zmax <= 0.12 ? 10 : 0));
+    return zmax <= 0.028 ? 6 : (zmax <= 0.05 ? 7 : (zmax <= 0.12 ? 9 : 0));
 }
 template <int N, int G>
 __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, double x2, double x3) {
@@ -185,7 +186,7 @@ __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, doubl
     if constexpr (G == kTayExp) {
         const double e0 = exp(x0);
 #pragma unroll
-        for (int n = 0; n <= N; ++n) a.k[n] = e0 * (N == 6 ? econ6_exp(n) : inv_fact(n));
+        for (int n = 0; n <= N; ++n) a.k[n] = e0 * econ_exp<N>(n);
     } else {
         double s0, c0;
         sincospi(x0, &s0, &c0);
@@ -193,7 +194,7 @@ __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, doubl
         const double d[4] = {G == kTaySin ? s0 : c0, G == kTaySin ? c0 : -s0, G == kTaySin ? -s0 : -c0,
                              G == kTaySin ? -c0 : s0};
 #pragma unroll
-        for (int n = 0; n <= N; ++n) a.k[n] = d[n & 3] * (N == 6 ? econ6_trig(n) : inv_fact(n));
+        for (int n = 0; n <= N; ++n) a.k[n] = d[n & 3] * econ_trig<N>(n);
     }
     return a;
 }

@@ -371,10 +371,10 @@ def test_async_upload_matches_sync(oracle):
 
 
 @pytest.mark.parametrize("kind", [3, 4, 5])
-@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # orders 6 (economised), 8, 10, direct
+@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # economised orders 6, 7, 9 and direct
 def test_small_element_load_paths(oracle, kind, h):
-    """The Taylor-series load vector (orders 7, 8, 10 by element size, see
-    problems.cuh taylor_order) against the oracle's libm evaluation: small
+    """The series load vector (economised orders 6, 7, 9 by element size,
+    see problems.cuh taylor_order) against the oracle's libm evaluation: small
     jittered Kuhn meshes with cells of size h, moved away from the origin so
     that sin and cos are both far from zero."""
     m = oracle.kuhn(3, 3, 2, lx=3 * h, ly=3 * h, lz=2 * h, jitter=0.2, dmask=0x15)
