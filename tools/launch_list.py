@@ -17,4 +17,4 @@ for i, v in by.items():
     t = v.get("gpu__time_duration.sum", 0) / 1e3
     r = v.get("dram__bytes_read.sum", 0) / 1e6
     w = v.get("dram__bytes_write.sum", 0) / 1e6
-    print(f"{i:>4} {v['name'][:34]:34s} {t:9.1f} us  R {r:8.1f} MB  W {w:8.1f} MB  {(r + w) / t / 1e3 if t else 0:6.2f} TB/s")
+    print(f"{i:>4} {v['name'][:34]:34s} {t:9.1f} us  R {r:8.1f} MB  W {w:8.1f} MB  {(r + w) / t if t else 0:6.2f} TB/s")
