@@ -79,8 +79,8 @@ __device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict_
 }
 
 // Gauss-64 load vector of the transcendental kinds with the trig / exp
-// factors as order-N Taylor series around vertex 0 (problems.cuh), walking
-// the rule in its collapsed-product order (a, b, c):
+// factors as order-N economised series around vertex 0 (problems.cuh),
+// walking the rule in its collapsed-product order (a, b, c):
 //   z = lambda1 e1 + lambda2 e2 + lambda3 e3 = A(a, b) + lambda3 e3, with
 //       A(a, b) = fma(lambda2, e2, lambda1 e1) formed once per (a, b): the
 //       same operations as the per-point fma chain, a third of the cost;
@@ -107,7 +107,9 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
     const double c0 = KIND == 4 ? p[0].z : p[0].x;
     const double d1 = (KIND == 4 ? p[1].z : p[1].x) - c0, d2 = (KIND == 4 ? p[2].z : p[2].x) - c0,
                  d3 = (KIND == 4 ? p[3].z : p[3].x) - c0;
-    double S = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+    // two b3 accumulators and a pairwise U keep the per-(a, b) dependency
+    // chains at depth 2 (the loop is short of independent work otherwise)
+    double S = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0, b3o = 0.0;
     for (int a = 0; a < 4; ++a) {
         const double l1 = c_l1[a];
         double T = 0.0;
@@ -116,7 +118,7 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
             const double l2 = c_l2[4 * a + bb];
             const double ax = fma(l2, tx.e2, l1 * tx.e1), ay = fma(l2, ty.e2, l1 * ty.e1),
                          az = fma(l2, tz.e2, l1 * tz.e1), al = fma(l2, d2, fma(l1, d1, c0));
-            double U = 0.0;
+            double fw[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const int qp = 16 * a + 4 * bb + c;
@@ -135,16 +137,19 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
                     const double sv = horner(ty, fma(l3, ty.e3, ay)) * horner(tz, fma(l3, tz.e3, az));
                     f = fma(cpre, xc * (8.0 - xc) * sv, 2.0 * k.a0 * sv);
                 }
-                const double fw = c_w5[qp] * f;
-                U += fw;
-                b3 = fma(fw, l3, b3);
+                fw[c] = c_w5[qp] * f;
             }
+            const int q0 = 16 * a + 4 * bb;
+            b3 = fma(fw[2], c_l3[q0 + 2], fma(fw[0], c_l3[q0], b3));
+            b3o = fma(fw[3], c_l3[q0 + 3], fma(fw[1], c_l3[q0 + 1], b3o));
+            const double U = (fw[0] + fw[1]) + (fw[2] + fw[3]);
             T += U;
             b2 = fma(U, l2, b2);
         }
         S += T;
         b1 = fma(T, l1, b1);
     }
+    b3 += b3o;
     const double sc = KIND == 3 ? vol * cpre : vol;
     b[0] = (((S - b1) - b2) - b3) * sc;
     b[1] = b1 * sc;

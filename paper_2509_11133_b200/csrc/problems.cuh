@@ -130,8 +130,9 @@ __device__ __forceinline__ double axis_zmax(double x0, double x1, double x2, dou
 }
 // The series are Chebyshev-economised: the Taylor series one degree higher
 // with its top term replaced through T_{N+1} on [-zmax, zmax] (the same
-// magnitudes as 1/n! with tiny corrections).  Classes and their errors
-// measured against mpmath over the interval (relative):
+// magnitudes as 1/n! with tiny corrections; generated and checked by
+// tools/econ_tables.py, tests/test_econ_tables.py).  Classes and their
+// errors measured against mpmath over the interval (relative):
 //   N = 6, |z| <= 0.028: cos 7e-20, sin 4.2e-17, exp 5.0e-17
 //   N = 7, |z| <= 0.05:  cos 7.6e-18, sin 5.4e-18, exp 1.2e-17
 //   N = 9, |z| <= 0.12:  cos 3.4e-19, sin 1.9e-18, exp 2.0e-18

@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libphfem.so")
+# PHFEM_LIB selects another build of the same library (experiment builds)
+LIB_PATH = os.environ.get("PHFEM_LIB") or os.path.join(HERE, "lib", "libphfem.so")
 
 OK, ERR_ARGUMENT, ERR_MESH, ERR_SOLVER, ERR_IO = 0, 1, 2, 3, 4
 PROBLEM_MANUFACTURED, PROBLEM_LINEAR, PROBLEM_ZERO = 0, 1, 2
