@@ -251,7 +251,10 @@ __global__ void __launch_bounds__(32 * kFastWarps)
     constexpr int R = LCAP / 32;  // rounds of 32 over a full list
     __shared__ int32_t s_ekey[kFastWarps][CAP], s_eval[kFastWarps][CAP];
     __shared__ unsigned long long s_fkey[kFastWarps][CAP];
-    __shared__ int32_t s_flo[kFastWarps][CAP], s_fhi[kFastWarps][CAP], s_fcnt[kFastWarps][CAP];
+    // face groups: count << 2 | orientation bits, and the (at most two,
+    // else an error) slots in arrival order -- one atomic per candidate
+    __shared__ int32_t s_fcnt[kFastWarps][CAP];
+    __shared__ int2 s_fsl[kFastWarps][CAP];
     __shared__ int2 s_el[kFastWarps][LCAP];  // (b, edge slot)
     __shared__ int4 s_fl[kFastWarps][LCAP];  // (lo, hi, face slot, count increment)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -259,17 +262,14 @@ __global__ void __launch_bounds__(32 * kFastWarps)
     int32_t* ekey = s_ekey[warp];
     int32_t* eval = s_eval[warp];
     unsigned long long* fkey = s_fkey[warp];
-    int32_t* flo = s_flo[warp];
-    int32_t* fhi = s_fhi[warp];
     int32_t* fcnt = s_fcnt[warp];
+    int32_t* fsl = reinterpret_cast<int32_t*>(s_fsl[warp]);
     int2* el = s_el[warp];
     int4* fl = s_fl[warp];
     for (int i = lane; i < CAP; i += 32) {
         ekey[i] = -1;
         eval[i] = INT_MAX;
         fkey[i] = ~0ull;
-        flo[i] = INT_MAX;
-        fhi[i] = -1;
         fcnt[i] = 0;
     }
     __syncwarp();
@@ -319,12 +319,14 @@ __global__ void __launch_bounds__(32 * kFastWarps)
     load_inc(P2, I2);
     Ptr P3 = load_ptr(it0 + 2 * nwarps);
     for (int64_t it = it0; it < n; it += nwarps) {
-        // stages for it + nwarps (tets) and it + 2 nwarps (incidences, ptrs)
-        int4 T2[E];
-        load_tet(I2, T2);
+        // stages for it + nwarps (tets) and it + 2 nwarps (incidences, ptrs);
+        // the pointer loads go first: issued after the 16-byte tet loads they
+        // waited for those loads to release their address registers
+        const Ptr P4 = load_ptr(it + 3 * nwarps);
         int32_t I3[E];
         load_inc(P3, I3);
-        const Ptr P4 = load_ptr(it + 3 * nwarps);
+        int4 T2[E];
+        load_tet(I2, T2);
         const int32_t v = P1.v;
         const int m = (int)(P1.end - P1.beg);
         const bool deferred = m > 32 * E;
@@ -404,9 +406,8 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     h = (h + 1) & mask;
                 }
                 fh[r] = (int)h;
-                atomicMin(flo + h, c.z);
-                atomicMax(fhi + h, c.z);
-                atomicAdd(fcnt + h, c.w);
+                const int pos = atomicAdd(fcnt + h, c.w) >> 2;
+                if (pos < 2) fsl[2 * h + pos] = c.z;
             }
         }
         __syncwarp();
@@ -419,15 +420,17 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             if (fh[r] >= 0) {
                 const int h = fh[r];
                 const int32_t slot = fl[j].z;
-                const int32_t c = fcnt[h], lo = flo[h], hi = fhi[h];
+                const int32_t c = fcnt[h];
                 const int cnt = c >> 2;
+                const int2 pr = s_fsl[warp][h];
+                const int32_t lo = min(pr.x, pr.y), hi = max(pr.x, pr.y);
                 if (cnt > 2 || (cnt == 2 && c != 11)) {
                     // same orientation twice: "elements A and B claim the
                     // same oriented face" (connectivity.cpp:62-68)
                     const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
                     report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                 }
-                slot_mate[slot] = cnt >= 2 ? (slot == lo ? hi : lo) : -1;
+                slot_mate[slot] = cnt >= 2 ? (slot == pr.x ? pr.y : pr.x) : -1;
             }
         }
         __syncwarp();
@@ -441,8 +444,6 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             }
             if (fh[r] >= 0) {
                 fkey[fh[r]] = ~0ull;
-                flo[fh[r]] = INT_MAX;
-                fhi[fh[r]] = -1;
                 fcnt[fh[r]] = 0;
             }
         }
