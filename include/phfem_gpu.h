@@ -107,7 +107,9 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
 /* Per-element slot masks [ne] (bit k < 6: edge slot 6t+k is its edge's
  * first occurrence; bit 6+k: face slot 4t+k owns its face) and the exclusive
  * offsets [ne + 1] of their popcounts: edge_off, face_off (skipped when
- * slot_mate is NULL).  scratch needs phfem_gpu_element_offsets_scratch(ne)
+ * slot_mate is NULL).  Entry t < ne packs the offset (low 32 bits; totals
+ * stay below 2^31) with element t's edge / face mask above it; entry ne is
+ * the plain total.  scratch needs phfem_gpu_element_offsets_scratch(ne)
  * bytes. */
 size_t phfem_gpu_element_offsets_scratch(int64_t ne);
 int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate, uint16_t* masks,
@@ -119,8 +121,7 @@ int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32
  * first element), the edge/face tables, sigma and the face areas.  Either
  * output group may be NULL (edge_first / slot_mate NULL). */
 int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords,
-                     const int32_t* edge_first, const int64_t* edge_off, const uint16_t* masks,
-                     int32_t* edge_of_slot,
+                     const int32_t* edge_first, const int64_t* edge_off, int32_t* edge_of_slot,
                      int32_t* edge_nodes, const int32_t* slot_mate, const int64_t* face_off,
                      int32_t* face_of_slot, int8_t* sigma, int32_t* faces, int32_t* face_slots,
                      double* face_area, unsigned long long* err, void* stream);

@@ -510,9 +510,11 @@ __device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mat
 //                    (edges << 31 | faces; 6 nE < 2^31 is enforced at
 //                    upload, so no carry)
 //   scan_sums        the tile sums
-//   offsets_scan_k   16 elements per thread from 32 B of masks
-// number() ranks non-first slots in their group's first element with the
-// same masks (one 2-byte gather instead of re-reading edge_first).
+//   offsets_scan_k   16 elements per thread from 32 B of masks; writes
+//                    edge_off[t] = offset | edge mask << 32 and
+//                    face_off[t] = offset | face mask << 32
+// number() ranks non-first slots in their group's first element from that
+// one 8-byte word (offset + mask in a single gather).
 __device__ __forceinline__ uint32_t elem_mask(int64_t t, const int32_t* e6, const int4* mate) {
     uint32_t m = 0;
 #pragma unroll
@@ -558,24 +560,22 @@ __global__ void __launch_bounds__(kScanThreads)
     __shared__ long long stage[kScanTile + kScanTile / 16];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     const int64_t first = base + (int64_t)threadIdx.x * kScanItems;
-    uint8_t ce[kScanItems], cf[kScanItems];
+    uint16_t mk[kScanItems];
     if (first + kScanItems <= ne) {
         const uint4* p = reinterpret_cast<const uint4*>(masks + first);
         const uint4 q0 = __ldg(p), q1 = __ldg(p + 1);
         const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-        for (int i = 0; i < kScanItems; ++i) {
-            const uint32_t m = (w[i / 2] >> (16 * (i % 2))) & 0xffffu;
-            ce[i] = (uint8_t)__popc(m & 63u);
-            cf[i] = (uint8_t)__popc(m >> 6);
-        }
+        for (int i = 0; i < kScanItems; ++i) mk[i] = (uint16_t)(w[i / 2] >> (16 * (i % 2)));
     } else {
 #pragma unroll
-        for (int i = 0; i < kScanItems; ++i) {
-            const uint32_t m = first + i < ne ? masks[first + i] : 0u;
-            ce[i] = (uint8_t)__popc(m & 63u);
-            cf[i] = (uint8_t)__popc(m >> 6);
-        }
+        for (int i = 0; i < kScanItems; ++i) mk[i] = first + i < ne ? masks[first + i] : (uint16_t)0;
+    }
+    uint8_t ce[kScanItems], cf[kScanItems];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        ce[i] = (uint8_t)__popc(mk[i] & 63u);
+        cf[i] = (uint8_t)__popc((uint32_t)mk[i] >> 6);
     }
     long long se = 0, sf = 0;
 #pragma unroll
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kScanThreads)
     long long run = packed >> 31;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
+        stage[scan_pad(threadIdx.x * kScanItems + i)] = run | (long long)(mk[i] & 63u) << 32;
         run += ce[i];
     }
     __syncthreads();
@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kScanThreads)
     run = packed & 0x7fffffffll;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        stage[scan_pad(threadIdx.x * kScanItems + i)] = run;
+        stage[scan_pad(threadIdx.x * kScanItems + i)] = run | (long long)((uint32_t)mk[i] >> 6) << 32;
         run += cf[i];
     }
     __syncthreads();
@@ -620,7 +620,7 @@ __global__ void offsets_total_k(const int64_t* __restrict__ packed_total, int64_
 __global__ void __launch_bounds__(256)
     number(int64_t ne, const int32_t* __restrict__ tets, const double* __restrict__ coords,
            const int32_t* __restrict__ edge_first, const int64_t* __restrict__ edge_off,
-           const uint16_t* __restrict__ masks, int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
+           int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ edge_nodes,
            const int32_t* __restrict__ slot_mate, const int64_t* __restrict__ face_off,
            int32_t* __restrict__ face_of_slot, int8_t* __restrict__ sigma, int32_t* __restrict__ faces,
            int32_t* __restrict__ face_slots, double* __restrict__ face_area, unsigned long long* err) {
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(256)
         const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
         const int2 a01 = __ldg(ef2), a23 = __ldg(ef2 + 1), a45 = __ldg(ef2 + 2);
         const int32_t ef[6] = {a01.x, a01.y, a23.x, a23.y, a45.x, a45.y};
-        int64_t id = edge_off[t];
+        int64_t id = (uint32_t)edge_off[t];
         int32_t ids[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) {
@@ -648,7 +648,8 @@ __global__ void __launch_bounds__(256)
                 // rank of slot f among the first-occurrence slots of its element
                 const int64_t g = f / 6;
                 const uint32_t below = (1u << (f - 6 * g)) - 1u;
-                ids[k] = (int32_t)(__ldg(edge_off + g) + __popc(__ldg(masks + g) & below));
+                const unsigned long long w = (unsigned long long)__ldg(edge_off + g);
+                ids[k] = (int32_t)((uint32_t)w + __popc((uint32_t)(w >> 32) & below));
             }
         }
         int2* eo = reinterpret_cast<int2*>(edge_of_slot) + 3 * t;
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(256)
         eo[2] = make_int2(ids[4], ids[5]);
     }
     if (slot_mate) {
-        int64_t id = face_off[t];
+        int64_t id = (uint32_t)face_off[t];
         const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
         int32_t fid[4];
         int sg[4];
@@ -686,7 +687,8 @@ __global__ void __launch_bounds__(256)
                 // checked in star_groups)
                 const int64_t g = mate >> 2;
                 const uint32_t below = (1u << (mate & 3)) - 1u;
-                fid[k] = (int32_t)(__ldg(face_off + g) + __popc((__ldg(masks + g) >> 6) & below));
+                const unsigned long long w = (unsigned long long)__ldg(face_off + g);
+                fid[k] = (int32_t)((uint32_t)w + __popc((uint32_t)(w >> 32) & below));
                 sg[k] = -1;
             }
         }
@@ -944,14 +946,14 @@ extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, 
 }
 
 extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords, const int32_t* edge_first,
-                                const int64_t* edge_off, const uint16_t* masks, int32_t* edge_of_slot,
+                                const int64_t* edge_off, int32_t* edge_of_slot,
                                 int32_t* edge_nodes,
                                 const int32_t* slot_mate, const int64_t* face_off, int32_t* face_of_slot,
                                 int8_t* sigma, int32_t* faces, int32_t* face_slots, double* face_area,
                                 unsigned long long* err, void* stream) {
     if (ne == 0) return 0;
     number<<<(unsigned)((ne + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        ne, tets, coords, edge_first, edge_off, masks, edge_of_slot, edge_nodes, slot_mate, face_off, face_of_slot, sigma,
+        ne, tets, coords, edge_first, edge_off, edge_of_slot, edge_nodes, slot_mate, face_off, face_of_slot, sigma,
         faces, face_slots, face_area, err);
     phg::count_launches(1);
     return (int)cudaGetLastError();

@@ -131,7 +131,7 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
         c.face_slots.alloc(2 * c.nf);
         c.face_area.alloc(c.nf);
     }
-    check(phfem_gpu_number(ne, m.tets.p, m.coords.p, c.edge_first.p, c.edge_off.p, w.masks.p, c.edge_of_slot.p,
+    check(phfem_gpu_number(ne, m.tets.p, m.coords.p, c.edge_first.p, c.edge_off.p, c.edge_of_slot.p,
                            c.edge_nodes.p,
                            faces ? c.slot_mate.p : nullptr, faces ? w.face_off.p : nullptr,
                            faces ? c.face_of_slot.p : nullptr, faces ? c.sigma.p : nullptr,

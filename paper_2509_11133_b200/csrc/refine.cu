@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kRefBlock)
     if (t < ne) {
         const int4 e = ldtet(tets, t);
         const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
-        const int64_t c = nc + t + edge_off[t];
+        const int64_t c = nc + t + (uint32_t)edge_off[t];  // low word: the offset
         const V3 ct = vdiv(vadd(vadd(vadd(p[0], p[1]), p[2]), p[3]), 4.0);  // refine.cpp:33-34
         coords_out[3 * c] = ct.x;
         coords_out[3 * c + 1] = ct.y;

@@ -52,7 +52,7 @@ def main():
     tabs = line_table(obj, kernel, depth)
     fn = sorted(tabs, key=len)[0]
     tab = tabs[fn]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + kernel.split("I")[0],
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", "regex:" + re.match(r"[a-z_0-9]+", kernel).group(0),
                           "-c", "1"], capture_output=True, text=True).stdout
     hdr, base, agg = None, None, collections.defaultdict(lambda: [0.0, 0.0, 0.0])
     for x in csv.reader(out.splitlines()):
