@@ -658,6 +658,8 @@ __global__ void __launch_bounds__(256)
         eo[2] = make_int2(ids[4], ids[5]);
     }
     if (slot_mate) {
+        // the element's four nodes once (owned faces' areas), not per face
+        const V3 pn[4] = {ldnode(coords, tet.x), ldnode(coords, tet.y), ldnode(coords, tet.z), ldnode(coords, tet.w)};
         int64_t id = (uint32_t)face_off[t];
         const int4 m = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
         int32_t fid[4];
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(256)
                 faces[3 * id + 2] = f2;
                 reinterpret_cast<int2*>(face_slots)[id] = make_int2(s, mate);
                 // face_area_and_normal (mesh.cpp:76-84): area = 0.5*|(z-x)x(y-x)|
-                const V3 p0 = ldnode(coords, f0), p1 = ldnode(coords, f1), p2 = ldnode(coords, f2);
+                const V3 p0 = pn[face_vert(k, 0)], p1 = pn[face_vert(k, 1)], p2 = pn[face_vert(k, 2)];
                 const V3 n = vcross(vsub(p2, p0), vsub(p1, p0));
                 const double len = __dsqrt_rn(vdot(n, n));
                 if (len == 0.0) report(err, PHG_ERR_FACE, (unsigned long long)id << 2 | 0);
