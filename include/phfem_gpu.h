@@ -184,11 +184,16 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * reduced deterministically through partials[2 * grid].  redo [ne + 1] is
  * scratch: the count and list of elements whose operands leave the
  * reciprocal-division window and are recomputed with IEEE division.
- * ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the main kernel. */
+ * face_bval [nf] is scratch: the boundary faces' Dirichlet traces / Neumann
+ * terms, formed first by a per-face pass (face_class, face_slots of the
+ * classification).  ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the
+ * main kernel. */
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
-                                const double* face_area, int32_t* sell_col, double* sell_val,
+                                const double* face_area, int64_t nf, const uint8_t* face_class,
+                                const int32_t* face_slots, double* face_bval, int32_t* sell_col,
+                                double* sell_val,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, double* norms,
                                 double* partials, int32_t* redo, unsigned long long* err, void* ev_begin,

@@ -211,6 +211,7 @@ struct FaceIn {
     const int32_t* __restrict__ slot_mate;
     const int32_t* __restrict__ face_mrow;
     const double* __restrict__ face_area;
+    const double* __restrict__ face_bval;  // boundary_terms_k, boundary faces only
 };
 
 // One element's assembly and condensation, streamed straight into the face
@@ -259,33 +260,24 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     double area[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) area[q] = __ldg(fin.face_area + sl.face[q]);
-    // boundary data: Neumann terms (assembly.cpp:81-94; this element's
-    // Neumann faces in face order == local slot order) and Dirichlet traces
-    // b_D = |F| u_D(centroid) (assembly.cpp:96-104; stored tuple = owner's)
+    // boundary data (boundary_terms_k): Neumann terms (assembly.cpp:81-94;
+    // this element's Neumann faces in face order == local slot order) and
+    // Dirichlet traces b_D = |F| u_D(centroid) (assembly.cpp:96-104)
     double ln[4] = {0.0, 0.0, 0.0, 0.0};
     double bdv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         bdv[q] = 0.0;
         if (!sl.bnd[q]) continue;
-        const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
-        const V3 q0 = p[i0], q1 = p[i1], q2 = p[i2];
-        const V3 s3 = vadd(vadd(q0, q1), q2);
-        const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
+        const double v = __ldg(fin.face_bval + sl.face[q]);
         if (sl.row[q] >= 0) {
-            bdv[q] = mul(area[q], prob_u<KIND>(cen.x, cen.y, cen.z));
+            bdv[q] = v;
             continue;
         }
-        const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
-        const double len = __dsqrt_rn(vdot(n, n));
-        const double ar = mul(0.5, len);
-        const Div dl = dv.make(len);
-        const V3 un = {dv.div(n.x, dl), dv.div(n.y, dl), dv.div(n.z, dl)};
-        const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-        const double contrib = dv.div(mul(ar, gc), kDiv3);
-        ln[i0] = add(ln[i0], contrib);
-        ln[i1] = add(ln[i1], contrib);
-        ln[i2] = add(ln[i2], contrib);
+        const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+        ln[i0] = add(ln[i0], v);
+        ln[i1] = add(ln[i1], v);
+        ln[i2] = add(ln[i2], v);
     }
 #pragma unroll
     for (int v = 0; v < 4; ++v) bt[v] = add(bt[v], ln[v]);  // B_T = b + LN (assembly.cpp:135)
@@ -392,6 +384,59 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     return 0;
 }
 
+// Boundary terms, one thread per boundary face (face_class 1 Dirichlet, 2
+// Neumann), computed as the element loop of assembly.cpp does from the
+// owner element's local vertex order, with IEEE division (the values are
+// the ones the element kernel would form):
+//   Dirichlet: |F| u_D(centroid)                       (assembly.cpp:96-104)
+//   Neumann:   0.5 |n| g(centroid, n / |n|) / 3, n = (q2 - q0) x (q1 - q0)
+//                                                      (assembly.cpp:81-94)
+// Kept out of assemble_k: its code (u, g with their transcendentals) ran in
+// ~1 warp in 9 with a few lanes active and crowded the instruction cache.
+template <int KIND>
+__global__ void __launch_bounds__(256)
+    boundary_terms_k(int64_t nf, const uint8_t* __restrict__ face_class, const int32_t* __restrict__ face_slots,
+                     const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
+                     const double* __restrict__ face_area, double* __restrict__ face_bval) {
+    const int64_t n16 = (nf + 15) / 16;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (16 * i + 16 <= nf) {
+            w = __ldg(reinterpret_cast<const uint4*>(face_class) + i);
+        } else {
+            uint8_t* b = reinterpret_cast<uint8_t*>(&w);
+            for (int j = 0; j < 16 && 16 * i + j < nf; ++j) b[j] = face_class[16 * i + j];
+        }
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t cls = (ws[j >> 2] >> (8 * (j & 3))) & 0xffu;
+            if (cls == 0) continue;
+            const int64_t f = 16 * i + j;
+            const int32_t slot = face_slots[2 * f];
+            const int64_t t = slot >> 2;
+            const int q = slot & 3;
+            const int4 e = ldtet(tets, t);
+            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+            const V3 q0 = ldnode(coords, tv(e, i0)), q1 = ldnode(coords, tv(e, i1)), q2 = ldnode(coords, tv(e, i2));
+            ExactDiv dv;
+            const V3 s3 = vadd(vadd(q0, q1), q2);
+            const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
+            if (cls == 1) {
+                face_bval[f] = mul(face_area[f], prob_u<KIND>(cen.x, cen.y, cen.z));
+                continue;
+            }
+            const Coef k = load_coef(prob, t);
+            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+            const double len = __dsqrt_rn(vdot(n, n));
+            const double ar = mul(0.5, len);
+            const Div dl = dv.make(len);
+            const V3 un = {dv.div(n.x, dl), dv.div(n.y, dl), dv.div(n.z, dl)};
+            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+            face_bval[f] = dv.div(mul(ar, gc), kDiv3);
+        }
+    }
+}
+
 // Fast pass: one element per thread, blocks in element order (the elements
 // in flight and the S rows they scatter into stay in an L2-resident window),
 // FastDiv division.  Elements whose operands left the exact window are
@@ -401,14 +446,15 @@ __global__ void __launch_bounds__(kCondThreads, 4)
     assemble_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
-               double* __restrict__ rhs, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+               const double* __restrict__ face_bval, double* __restrict__ rhs, int32_t* __restrict__ sell_col,
+               double* __restrict__ sell_val,
                double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
                double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, int32_t* __restrict__ redo_list,
                int32_t* __restrict__ redo_count, unsigned long long* err) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= ne) return;
     FastDiv fd;
-    const int st = assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area},
+    const int st = assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area, face_bval},
                                        a_blocks, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, fd);
     if (st == 1) redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
     // "degenerate element block" (solver.cpp:103-109)
@@ -424,14 +470,15 @@ __global__ void __launch_bounds__(kCondThreads)
                     const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                     const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                     const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
-                    double* __restrict__ rhs, int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+                    const double* __restrict__ face_bval, double* __restrict__ rhs, int32_t* __restrict__ sell_col,
+                    double* __restrict__ sell_val,
                     double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
                     double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, unsigned long long* err) {
     const int32_t n = *redo_count;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int64_t t = redo_list[i];
         ExactDiv ed;
-        if (assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area}, a_blocks,
+        if (assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area, face_bval}, a_blocks,
                                 sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, ed) == 2)
             report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
     }
@@ -543,7 +590,9 @@ extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
 extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                            const phg_problem* prob, const int32_t* face_of_slot,
                                            const int32_t* slot_mate, const int32_t* face_mrow,
-                                           const double* face_area, int32_t* sell_col, double* sell_val,
+                                           const double* face_area, int64_t nf, const uint8_t* face_class,
+                                           const int32_t* face_slots, double* face_bval, int32_t* sell_col,
+                                           double* sell_val,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
                                            int32_t* redo, unsigned long long* err, void* ev_begin, void* ev_end,
@@ -555,14 +604,15 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
     zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, sell_val, rhs_neg);
 #define PHG_ASM(K)                                                                                                   \
+    boundary_terms_k<K><<<kSMs * 4, 256, 0, s>>>(nf, face_class, face_slots, coords, tets, p, face_area, face_bval);   \
     if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);                                                         \
     assemble_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
-                                                rhs, sell_col, sell_val, rhs_neg, bd, a_blocks, slot_coef,          \
-                                                slot_mrow, redo + 1, redo, err);                                    \
+                                                face_bval, rhs, sell_col, sell_val, rhs_neg, bd, a_blocks,          \
+                                                slot_coef, slot_mrow, redo + 1, redo, err);                         \
     if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);                                                             \
     assemble_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
-                                                     face_mrow, face_area, rhs, sell_col, sell_val, rhs_neg, bd,    \
-                                                     a_blocks, slot_coef, slot_mrow, err)
+                                                     face_mrow, face_area, face_bval, rhs, sell_col, sell_val,      \
+                                                     rhs_neg, bd, a_blocks, slot_coef, slot_mrow, err)
     switch (p.kind) {
         case 0: PHG_ASM(0); break;
         case 1: PHG_ASM(1); break;
@@ -575,6 +625,6 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
 #undef PHG_ASM
     sumsq2_k<<<kNormGrid, 256, 0, s>>>(rhs, 4 * ne, bd, l, partials);
     reduce_pairs<<<1, 1024, 0, s>>>(partials, kNormGrid, norms);
-    phg::count_launches(5);
+    phg::count_launches(6);
     return (int)cudaGetLastError();
 }

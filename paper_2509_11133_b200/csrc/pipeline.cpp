@@ -290,8 +290,10 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     const phg_problem p = device_problem(k, problem);
     // the main kernel alone
     cudaEvent_t ka = st ? st->event() : nullptr, kb = st ? st->event() : nullptr;
+    w.face_bval.alloc(c.nf);
     check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
-                                      c.face_mrow.p, c.face_area.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
+                                      c.face_mrow.p, c.face_area.p, c.nf, c.face_class.p, c.face_slots.p,
+                                      w.face_bval.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,
                                       debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p,
