@@ -39,6 +39,9 @@ namespace {
 using namespace phg;
 
 constexpr int kCondThreads = 128;
+#ifndef PHG_COND_MINB
+#define PHG_COND_MINB 4  // resident blocks per SM the register budget is sized for
+#endif
 
 __device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
     return (row >> 5) * (PHG_SELL_C * PHG_SELL_W) + pos * PHG_SELL_C + (row & 31);
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(256)
 // FastDiv division.  Elements whose operands left the exact window are
 // appended to redo_list.
 template <int KIND>
-__global__ void __launch_bounds__(kCondThreads, 4)
+__global__ void __launch_bounds__(kCondThreads, PHG_COND_MINB)
     assemble_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
