@@ -127,14 +127,14 @@ int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords,
                      double* face_area, unsigned long long* err, void* stream);
 
 /* Boundary classification (connectivity.cpp:156-175): entries of db then nb
- * are matched through the star of their smallest vertex. */
+ * are matched through the star of their smallest vertex; entry_face [nd +
+ * nn] receives each entry's face id (-1: none), which the check pass and the
+ * assembly's boundary terms reuse. */
 int phfem_gpu_classify(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
                        const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                        const int32_t* face_of_slot, const int32_t* face_slots, uint32_t* claim,
-                       unsigned long long* err, void* stream);
-int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
-                             const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
-                             const int32_t* face_of_slot, const uint32_t* claim,
+                       int32_t* entry_face, unsigned long long* err, void* stream);
+int phfem_gpu_classify_check(int64_t nd, int64_t nn, const int32_t* entry_face, const uint32_t* claim,
                              unsigned long long* err, void* stream);
 /* face classes (connectivity.cpp:177-201); claim[f] is the first list entry
  * naming face f (all ones: none); counts[3] += interior, dirichlet, neumann
@@ -185,14 +185,15 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * scratch: the count and list of elements whose operands leave the
  * reciprocal-division window and are recomputed with IEEE division.
  * face_bval [nf] is scratch: the boundary faces' Dirichlet traces / Neumann
- * terms, formed first by a per-face pass (face_class, face_slots of the
- * classification).  ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the
+ * terms, formed first by a pass over the nd + nn boundary entries
+ * (entry_face of the classification, face_slots).  ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the
  * main kernel. */
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
-                                const double* face_area, int64_t nf, const uint8_t* face_class,
-                                const int32_t* face_slots, double* face_bval, int32_t* sell_col,
+                                const double* face_area, int64_t nd, int64_t nn,
+                                const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
+                                int32_t* sell_col,
                                 double* sell_val,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, double* norms,

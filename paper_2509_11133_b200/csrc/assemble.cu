@@ -387,56 +387,45 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     return 0;
 }
 
-// Boundary terms, one thread per boundary face (face_class 1 Dirichlet, 2
-// Neumann), computed as the element loop of assembly.cpp does from the
-// owner element's local vertex order, with IEEE division (the values are
-// the ones the element kernel would form):
+// Boundary terms, one thread per boundary list entry (db then nb, mapped to
+// faces by the classification), computed as the element loop of
+// assembly.cpp does from the owner element's local vertex order, with IEEE
+// division (the values are the ones the element kernel would form):
 //   Dirichlet: |F| u_D(centroid)                       (assembly.cpp:96-104)
 //   Neumann:   0.5 |n| g(centroid, n / |n|) / 3, n = (q2 - q0) x (q1 - q0)
 //                                                      (assembly.cpp:81-94)
 // Kept out of assemble_k: its code (u, g with their transcendentals) ran in
 // ~1 warp in 9 with a few lanes active and crowded the instruction cache.
 template <int KIND>
-__global__ void __launch_bounds__(256)
-    boundary_terms_k(int64_t nf, const uint8_t* __restrict__ face_class, const int32_t* __restrict__ face_slots,
-                     const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
-                     const double* __restrict__ face_area, double* __restrict__ face_bval) {
-    const int64_t n16 = (nf + 15) / 16;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
-        uint4 w = make_uint4(0, 0, 0, 0);
-        if (16 * i + 16 <= nf) {
-            w = __ldg(reinterpret_cast<const uint4*>(face_class) + i);
-        } else {
-            uint8_t* b = reinterpret_cast<uint8_t*>(&w);
-            for (int j = 0; j < 16 && 16 * i + j < nf; ++j) b[j] = face_class[16 * i + j];
+__global__ void __launch_bounds__(128)
+    boundary_terms_k(int64_t nd, int64_t nn, const int32_t* __restrict__ entry_face,
+                     const int32_t* __restrict__ face_slots, const double* __restrict__ coords,
+                     const int32_t* __restrict__ tets, phg_problem prob, const double* __restrict__ face_area,
+                     double* __restrict__ face_bval) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd + nn; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = entry_face[i];
+        if (f < 0) continue;  // reported by the classification
+        const int32_t slot = face_slots[2 * (int64_t)f];
+        const int64_t t = slot >> 2;
+        const int q = slot & 3;
+        const int4 e = ldtet(tets, t);
+        const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
+        const V3 q0 = ldnode(coords, tv(e, i0)), q1 = ldnode(coords, tv(e, i1)), q2 = ldnode(coords, tv(e, i2));
+        ExactDiv dv;
+        const V3 s3 = vadd(vadd(q0, q1), q2);
+        const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
+        if (i < nd) {
+            face_bval[f] = mul(face_area[f], prob_u<KIND>(cen.x, cen.y, cen.z));
+            continue;
         }
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t cls = (ws[j >> 2] >> (8 * (j & 3))) & 0xffu;
-            if (cls == 0) continue;
-            const int64_t f = 16 * i + j;
-            const int32_t slot = face_slots[2 * f];
-            const int64_t t = slot >> 2;
-            const int q = slot & 3;
-            const int4 e = ldtet(tets, t);
-            const int i0 = face_vert(q, 0), i1 = face_vert(q, 1), i2 = face_vert(q, 2);
-            const V3 q0 = ldnode(coords, tv(e, i0)), q1 = ldnode(coords, tv(e, i1)), q2 = ldnode(coords, tv(e, i2));
-            ExactDiv dv;
-            const V3 s3 = vadd(vadd(q0, q1), q2);
-            const V3 cen = {dv.div(s3.x, kDiv3), dv.div(s3.y, kDiv3), dv.div(s3.z, kDiv3)};
-            if (cls == 1) {
-                face_bval[f] = mul(face_area[f], prob_u<KIND>(cen.x, cen.y, cen.z));
-                continue;
-            }
-            const Coef k = load_coef(prob, t);
-            const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
-            const double len = __dsqrt_rn(vdot(n, n));
-            const double ar = mul(0.5, len);
-            const Div dl = dv.make(len);
-            const V3 un = {dv.div(n.x, dl), dv.div(n.y, dl), dv.div(n.z, dl)};
-            const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
-            face_bval[f] = dv.div(mul(ar, gc), kDiv3);
-        }
+        const Coef k = load_coef(prob, t);
+        const V3 n = vcross(vsub(q2, q0), vsub(q1, q0));
+        const double len = __dsqrt_rn(vdot(n, n));
+        const double ar = mul(0.5, len);
+        const Div dl = dv.make(len);
+        const V3 un = {dv.div(n.x, dl), dv.div(n.y, dl), dv.div(n.z, dl)};
+        const double gc = prob_g<KIND>(cen.x, cen.y, cen.z, un, k);
+        face_bval[f] = dv.div(mul(ar, gc), kDiv3);
     }
 }
 
@@ -593,8 +582,9 @@ extern "C" int phfem_gpu_assemble_grid(int64_t ne) {
 extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                            const phg_problem* prob, const int32_t* face_of_slot,
                                            const int32_t* slot_mate, const int32_t* face_mrow,
-                                           const double* face_area, int64_t nf, const uint8_t* face_class,
-                                           const int32_t* face_slots, double* face_bval, int32_t* sell_col,
+                                           const double* face_area, int64_t nd, int64_t nn,
+                                           const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
+                                           int32_t* sell_col,
                                            double* sell_val,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
@@ -607,7 +597,9 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
     zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, sell_val, rhs_neg);
 #define PHG_ASM(K)                                                                                                   \
-    boundary_terms_k<K><<<kSMs * 4, 256, 0, s>>>(nf, face_class, face_slots, coords, tets, p, face_area, face_bval);   \
+    if (nd + nn > 0)                                                                                                 \
+        boundary_terms_k<K><<<(unsigned)((nd + nn + 127) / 128), 128, 0, s>>>(nd, nn, entry_face, face_slots, coords, \
+                                                                             tets, p, face_area, face_bval);        \
     if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);                                                         \
     assemble_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
                                                 face_bval, rhs, sell_col, sell_val, rhs_neg, bd, a_blocks,          \

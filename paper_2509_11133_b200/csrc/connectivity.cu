@@ -734,10 +734,11 @@ __global__ void classify(int64_t nd, const int32_t* __restrict__ db, int64_t nn,
                          const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
                          const int32_t* __restrict__ tets, const int32_t* __restrict__ face_of_slot,
                          const int32_t* __restrict__ face_slots, uint32_t* __restrict__ claim,
-                         unsigned long long* err) {
+                         int32_t* __restrict__ entry_face, unsigned long long* err) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd + nn; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t* tri = i < nd ? db + 3 * i : nb + 3 * (i - nd);
         const int32_t f = find_face(tri[0], tri[1], tri[2], star_ptr, star, tets, face_of_slot);
+        entry_face[i] = f;
         if (f < 0) {
             report(err, PHG_ERR_CLASSIFY, (unsigned long long)i << 2 | 0);
             continue;
@@ -747,14 +748,10 @@ __global__ void classify(int64_t nd, const int32_t* __restrict__ db, int64_t nn,
     }
 }
 
-__global__ void classify_check(int64_t nd, const int32_t* __restrict__ db, int64_t nn,
-                               const int32_t* __restrict__ nb, const int64_t* __restrict__ star_ptr,
-                               const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
-                               const int32_t* __restrict__ face_of_slot, const uint32_t* __restrict__ claim,
-                               unsigned long long* err) {
+__global__ void classify_check(int64_t nd, int64_t nn, const int32_t* __restrict__ entry_face,
+                               const uint32_t* __restrict__ claim, unsigned long long* err) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nd + nn; i += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t* tri = i < nd ? db + 3 * i : nb + 3 * (i - nd);
-        const int32_t f = find_face(tri[0], tri[1], tri[2], star_ptr, star, tets, face_of_slot);
+        const int32_t f = entry_face[i];
         if (f >= 0 && claim[f] != (uint32_t)i) report(err, PHG_ERR_CLASSIFY, (unsigned long long)i << 2 | 1);
     }
 }
@@ -964,20 +961,18 @@ extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* c
 extern "C" int phfem_gpu_classify(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
                                   const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                                   const int32_t* face_of_slot, const int32_t* face_slots, uint32_t* claim,
-                                  unsigned long long* err, void* stream) {
+                                  int32_t* entry_face, unsigned long long* err, void* stream) {
     if (nd + nn == 0) return 0;
     classify<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
-                                                                      face_of_slot, face_slots, claim, err); phg::count_launches(1);
+                                                                      face_of_slot, face_slots, claim, entry_face,
+                                                                      err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
-extern "C" int phfem_gpu_classify_check(int64_t nd, const int32_t* db, int64_t nn, const int32_t* nb,
-                                        const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
-                                        const int32_t* face_of_slot, const uint32_t* claim, unsigned long long* err,
-                                        void* stream) {
+extern "C" int phfem_gpu_classify_check(int64_t nd, int64_t nn, const int32_t* entry_face, const uint32_t* claim,
+                                        unsigned long long* err, void* stream) {
     if (nd + nn == 0) return 0;
-    classify_check<<<grid_cap(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(nd, db, nn, nb, star_ptr, star, tets,
-                                                                            face_of_slot, claim, err); phg::count_launches(1);
+    classify_check<<<grid_cap(nd + nn, 256), 256, 0, (cudaStream_t)stream>>>(nd, nn, entry_face, claim, err); phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

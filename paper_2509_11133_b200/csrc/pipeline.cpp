@@ -152,12 +152,11 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     const int64_t nf = c.nf;
     w.claim.alloc(nf);
     w.claim.fill_bytes(0xff);
+    c.entry_face.alloc(m.nd + m.nn);
     check(phfem_gpu_classify(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
-                             c.face_slots.p, w.claim.p, w.err.p, SV()),
+                             c.face_slots.p, w.claim.p, c.entry_face.p, w.err.p, SV()),
           "classify");
-    check(phfem_gpu_classify_check(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
-                                   w.claim.p, w.err.p, SV()),
-          "classify check");
+    check(phfem_gpu_classify_check(m.nd, m.nn, c.entry_face.p, w.claim.p, w.err.p, SV()), "classify check");
     c.face_class.alloc(nf + 16);
     w.counts.alloc(4);
     w.counts.zero();
@@ -292,7 +291,7 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     cudaEvent_t ka = st ? st->event() : nullptr, kb = st ? st->event() : nullptr;
     w.face_bval.alloc(c.nf);
     check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
-                                      c.face_mrow.p, c.face_area.p, c.nf, c.face_class.p, c.face_slots.p,
+                                      c.face_mrow.p, c.face_area.p, m.nd, m.nn, c.entry_face.p, c.face_slots.p,
                                       w.face_bval.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,

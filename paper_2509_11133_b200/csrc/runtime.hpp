@@ -204,6 +204,7 @@ struct Connectivity {
     DBuf<int8_t> sigma;
     DBuf<uint8_t> face_class;
     DBuf<double> face_area;
+    DBuf<int32_t> entry_face;  // boundary list entry (db then nb) -> face id
     // timings (seconds)
     double t_edges = 0.0, t_faces = 0.0;
 };
