@@ -81,11 +81,44 @@ __device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict_
     }
 }
 
+#ifndef PHG_LOCKSTEP
+#define PHG_LOCKSTEP 1  // the four points' series evaluated side by side
+#endif
+#ifndef PHG_STAGE
+#define PHG_STAGE 1  // stage the post-load-vector gathers in shared memory (cp.async)
+#endif
+// cp.async (LDGSTS): a gather that lands in shared memory without holding a
+// register or a scoreboard; waited for with cp_async_wait_all
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Per-thread staging (structure of arrays over the block's threads: a warp's
+// accesses to one field are consecutive words) of what the condensation
+// needs after the load vector: the coordinates, and the face-side gathers
+// face_mrow / face_area / face_bval of the element's four faces, issued
+// before the load vector so their latency hides under it.
+struct Stage {
+    double xyz[12][kCondThreads];
+    double area[4][kCondThreads];
+    double bval[4][kCondThreads];
+    int32_t row[4][kCondThreads];
+    int32_t face[4][kCondThreads];
+    int32_t mate[4][kCondThreads];
+};
+
 // Gauss-64 load vector of the transcendental kinds with the trig / exp
-// factors as order-N economised series around vertex 0 (problems.cuh),
+// factors as order-N economised series around the element's centre
+// (problems.cuh),
 // walking the rule in its collapsed-product order (a, b, c):
-//   z = lambda1 e1 + lambda2 e2 + lambda3 e3 = A(a, b) + lambda3 e3, with
-//       A(a, b) = fma(lambda2, e2, lambda1 e1) formed once per (a, b): the
+//   z = lambda1 e1 + lambda2 e2 + lambda3 e3 + em = A(a, b) + lambda3 e3,
+//       A(a, b) = fma(lambda2, e2, fma(lambda1, e1, em)) once per (a, b): the
 //       same operations as the per-point fma chain, a third of the cost;
 //   b1 = sum_a lambda1(a) T_a, b2 = sum_ab lambda2(a, b) U_ab with the
 //       partial sums U_ab = sum_c w f, T_a = sum_b U_ab, b3 per point, and
@@ -119,9 +152,52 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
 #pragma unroll 1
         for (int bb = 0; bb < 4; ++bb) {
             const double l2 = c_l2[4 * a + bb];
-            const double ax = fma(l2, tx.e2, l1 * tx.e1), ay = fma(l2, ty.e2, l1 * ty.e1),
-                         az = fma(l2, tz.e2, l1 * tz.e1), al = fma(l2, d2, fma(l1, d1, c0));
+            const double ax = fma(l2, tx.e2, fma(l1, tx.e1, tx.em)), ay = fma(l2, ty.e2, fma(l1, ty.e1, ty.em)),
+                         az = fma(l2, tz.e2, fma(l1, tz.e1, tz.em)), al = fma(l2, d2, fma(l1, d1, c0));
             double fw[4];
+#if PHG_LOCKSTEP
+            // the 12 (kind 3) or 8 series of the four points in lockstep:
+            // independent FMA chains side by side for the dependent-issue
+            // latency
+            double hx[4], hy[4], hz[4], zx[4], zy[4], zz[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const double l3 = c_l3[16 * a + 4 * bb + c];
+                zx[c] = fma(l3, tx.e3, ax);
+                zy[c] = fma(l3, ty.e3, ay);
+                zz[c] = fma(l3, tz.e3, az);
+                hx[c] = tx.k[N];
+                hy[c] = ty.k[N];
+                hz[c] = tz.k[N];
+            }
+#pragma unroll
+            for (int n = N - 1; n >= 0; --n) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (KIND != 5) hx[c] = fma(hx[c], zx[c], tx.k[n]);
+                    hy[c] = fma(hy[c], zy[c], ty.k[n]);
+                    if (KIND != 4) hz[c] = fma(hz[c], zz[c], tz.k[n]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int qp = 16 * a + 4 * bb + c;
+                const double l3 = c_l3[qp];
+                double f;
+                if constexpr (KIND == 3) {
+                    f = hx[c] * hy[c] * hz[c];
+                } else if constexpr (KIND == 4) {
+                    const double zc = fma(l3, d3, al);
+                    const double ec = hx[c] * hy[c];
+                    f = fma(cpre, ec * (zc * zc), -(k.a2 * 2.0) * ec);
+                } else {
+                    const double xc = fma(l3, d3, al);
+                    const double sv = hy[c] * hz[c];
+                    f = fma(cpre, xc * (8.0 - xc) * sv, 2.0 * k.a0 * sv);
+                }
+                fw[c] = c_w5[qp] * f;
+            }
+#else
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
                 const int qp = 16 * a + 4 * bb + c;
@@ -142,6 +218,7 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
                 }
                 fw[c] = c_w5[qp] * f;
             }
+#endif
             const int q0 = 16 * a + 4 * bb;
             b3 = fma(fw[2], c_l3[q0 + 2], fma(fw[0], c_l3[q0], b3));
             b3o = fma(fw[3], c_l3[q0 + 3], fma(fw[1], c_l3[q0 + 1], b3o));
@@ -181,12 +258,12 @@ __device__ __forceinline__ void load_vector(const V3 p[4], const Coef& k, double
         }
     } else {
         const double cpre = prob_f_pre<KIND>(k);
-        // Taylor expansion around vertex 0 when the element is small
-        // enough (problems.cuh: axis_taylor), else sinpi/cospi/exp
-        const double zmax = fmax(axis_zmax(p[0].x, p[1].x, p[2].x, p[3].x),
-                                 fmax(axis_zmax(p[0].y, p[1].y, p[2].y, p[3].y),
-                                      axis_zmax(p[0].z, p[1].z, p[2].z, p[3].z)));
-        switch (taylor_order(zmax)) {
+        // series around the centre of the element's span when the element
+        // is small enough (problems.cuh: axis_taylor), else sinpi/cospi/exp
+        const double r = fmax(axis_r(p[0].x, p[1].x, p[2].x, p[3].x),
+                              fmax(axis_r(p[0].y, p[1].y, p[2].y, p[3].y), axis_r(p[0].z, p[1].z, p[2].z, p[3].z)));
+        switch (taylor_order(r)) {
+            case 5: load_taylor<KIND, 5>(p, cpre, k, vol, b); break;
             case 6: load_taylor<KIND, 6>(p, cpre, k, vol, b); break;
             case 7: load_taylor<KIND, 7>(p, cpre, k, vol, b); break;
             case 9: load_taylor<KIND, 9>(p, cpre, k, vol, b); break;
@@ -238,6 +315,54 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
                                              int32_t* __restrict__ slot_mrow, Dv& dv) {
     // elem_volume == local.volume (assembly.cpp:18, 47)
     double bt[4];
+#if PHG_STAGE
+    __shared__ Stage stg;
+    const int tid = threadIdx.x;
+    {
+        const int4 e = ldtet(tets, t);
+        const int4 mate4 = __ldg(reinterpret_cast<const int4*>(fin.slot_mate) + t);
+        const int4 fos4 = __ldg(reinterpret_cast<const int4*>(fin.face_of_slot) + t);
+        const V3 p0[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int32_t f = tv(fos4, q), mate = tv(mate4, q);
+            cp_async4(&stg.row[q][tid], fin.face_mrow + f);
+            cp_async8(&stg.area[q][tid], fin.face_area + f);
+            if (mate < 0) cp_async8(&stg.bval[q][tid], fin.face_bval + f);
+            stg.face[q][tid] = f;
+            stg.mate[q][tid] = mate;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            stg.xyz[3 * i][tid] = p0[i].x;
+            stg.xyz[3 * i + 1][tid] = p0[i].y;
+            stg.xyz[3 * i + 2][tid] = p0[i].z;
+        }
+        const double det = vdot(vcross(vsub(p0[1], p0[0]), vsub(p0[2], p0[0])), vsub(p0[3], p0[0]));
+        if (det == 0.0) {
+            cp_async_wait_all();
+            return 3;
+        }
+        load_vector<KIND>(p0, load_coef(prob, t), dq(fabs(det), kDiv6), bt);
+    }
+    cp_async_wait_all();
+    V3 p[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) p[i] = {stg.xyz[3 * i][tid], stg.xyz[3 * i + 1][tid], stg.xyz[3 * i + 2][tid]};
+    const Coef k = load_coef_fresh(prob, t);
+    Slots sl;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int32_t mate = stg.mate[q][tid];
+        sl.face[q] = stg.face[q][tid];
+        sl.row[q] = stg.row[q][tid];
+        sl.owner[q] = mate < 0 || mate > (int32_t)(4 * t + q);
+        sl.bnd[q] = mate < 0;
+    }
+    double area[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) area[q] = stg.area[q][tid];
+#else
     {
         const int4 e = ldtet(tets, t);
         const V3 p0[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
@@ -263,6 +388,7 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     double area[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) area[q] = __ldg(fin.face_area + sl.face[q]);
+#endif
     // boundary data (boundary_terms_k): Neumann terms (assembly.cpp:81-94;
     // this element's Neumann faces in face order == local slot order) and
     // Dirichlet traces b_D = |F| u_D(centroid) (assembly.cpp:96-104)
@@ -272,7 +398,11 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     for (int q = 0; q < 4; ++q) {
         bdv[q] = 0.0;
         if (!sl.bnd[q]) continue;
+#if PHG_STAGE
+        const double v = stg.bval[q][tid];
+#else
         const double v = __ldg(fin.face_bval + sl.face[q]);
+#endif
         if (sl.row[q] >= 0) {
             bdv[q] = v;
             continue;

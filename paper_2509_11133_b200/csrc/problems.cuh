@@ -109,39 +109,54 @@ __device__ __forceinline__ double prob_f_fast(double x, double y, double z, doub
     }
 }
 // sin(pi x), cos(pi x) and e^x at the quadrature points of one element as a
-// Taylor series around the element's vertex 0: x = x0 + delta with
-// delta = l1 d1 + l2 d2 + l3 d3.  With z = pi delta (trig) or z = delta (exp),
-//   g(x0 + delta) = sum_{n<=N} g^(n)(x0)/n! * z^n,
-// whose coefficients are formed once per element from sinpi/cospi/exp at x0;
-// one quadrature point then costs 3 + N FMA per axis.  All derivatives of
-// these g are bounded by 1 (trig) or e^x0 e^|delta| (exp), so the truncation
-// error of the plain series is below zmax^(N+1)/(N+1)!; the economised
-// series below do better at one order less.  Elements with zmax > 0.12 keep
-// the direct sinpi/cospi/exp evaluation.
+// series around the centre of the element's range on each axis: with
+// delta = l1 d1 + l2 d2 + l3 d3 (d_i = x_i - x0) and m = (min + max) / 2 of
+// {0, d1, d2, d3}, x = x0 + m + (delta - m) and, with z = pi (delta - m)
+// (trig) or z = delta - m (exp),
+//   g(x0 + m + z') = sum_{n<=N} g^(n)(x0 + m)/n! * z^n,
+// whose coefficients are formed once per element from sinpi/cospi/exp at
+// x0 + m; one quadrature point then costs 1 + N FMA per axis (the argument
+// is a fused chain l1 e1 + l2 e2 + l3 e3 - pi m).  |z| <= r = pi (max - min)/2,
+// half the span of a series around a vertex, so a Kuhn element of config 4
+// (r = pi/256) needs one order less.  All derivatives of these g are
+// bounded by 1 (trig) or e^xc e^|z| (exp), so the truncation error of the
+// plain series is below r^(N+1)/(N+1)!; the economised series below do
+// better at one order less.  Elements with r > 0.12 keep the direct
+// sinpi/cospi/exp evaluation.
 enum { kTaySin = 0, kTayCos = 1, kTayExp = 2 };
 template <int N>
 struct AxisTaylor {
     double k[N + 1];
-    double e1, e2, e3;
+    double e1, e2, e3, em;  // z = l1 e1 + l2 e2 + l3 e3 + em
 };
-// |z| bound of one axis (pi-scaled; also bounds the exp axis' |delta|)
-__device__ __forceinline__ double axis_zmax(double x0, double x1, double x2, double x3) {
-    return kPi * fmax(fabs(x1 - x0), fmax(fabs(x2 - x0), fabs(x3 - x0)));
+// half span of one axis (pi-scaled; also bounds the exp axis' |z|)
+__device__ __forceinline__ double axis_r(double x0, double x1, double x2, double x3) {
+    const double d1 = x1 - x0, d2 = x2 - x0, d3 = x3 - x0;
+    const double lo = fmin(fmin(0.0, d1), fmin(d2, d3)), hi = fmax(fmax(0.0, d1), fmax(d2, d3));
+    return kPi * 0.5 * (hi - lo);
 }
-// The series are Chebyshev-economised: the Taylor series one degree higher
-// with its top term replaced through T_{N+1} on [-zmax, zmax] (the same
+// The series are Chebyshev-economised: the Taylor series one or two degrees
+// higher with its top terms replaced through T_m on [-r, r] (the same
 // magnitudes as 1/n! with tiny corrections; generated and checked by
 // tools/econ_tables.py, tests/test_econ_tables.py).  Classes and their
 // errors measured against mpmath over the interval (relative):
-//   N = 6, |z| <= 0.028: cos 7e-20, sin 4.2e-17, exp 5.0e-17
-//   N = 7, |z| <= 0.05:  cos 7.6e-18, sin 5.4e-18, exp 1.2e-17
-//   N = 9, |z| <= 0.12:  cos 3.4e-19, sin 1.9e-18, exp 2.0e-18
-// all below half an ulp (plain Taylor at these orders would leave up to
-// ~3e-15).  Table entry n = |coefficient of z^n| (the sign comes from the
-// derivative cycle of sin / cos; all positive for exp).
+//   N = 5, |z| <= 0.0125: cos 2.2e-16, sin 4.7e-19, exp 2.3e-16
+//   N = 6, |z| <= 0.028:  cos 1.5e-19, sin 4.2e-17, exp 5.0e-17
+//   N = 7, |z| <= 0.05:   cos 1.5e-17, sin 5.4e-18, exp 1.9e-17
+//   N = 9, |z| <= 0.12:   cos 7.7e-19, sin 1.9e-18, exp 2.4e-18
+// N >= 6 stay below half an ulp, N = 5 within one ulp of 1 -- the
+// libm-vs-libdevice difference of sin/cos/exp themselves, and four orders
+// below the 1e-12 parity tolerance of the load vector (plain Taylor at
+// these orders would leave up to ~3e-15).  Table entry n = |coefficient of
+// z^n| (the sign comes from the derivative cycle of sin / cos; all positive
+// for exp).
 template <int N>
 __device__ __forceinline__ double econ_trig(int n) {
-    if constexpr (N == 6) {
+    if constexpr (N == 5) {
+        constexpr double c[6] = {0x1.fffffffffffffp-1, 0x1.fffffffffffffp-1, 0x1.ffffffffac1d3p-2,
+                                 0x1.55555555300cfp-3, 0x1.5554a6921735fp-5, 0x1.11109c8ee7a6dp-7};
+        return c[n];
+    } else if constexpr (N == 6) {
         constexpr double c[7] = {1.0, 0x1.fffffffffffa2p-1, 0x1.fffffffffffcap-2, 0x1.55555551aab14p-3,
                                  0x1.55555552b6e02p-5, 0x1.110ec879513c9p-7, 0x1.6c142550f260ep-10};
         return c[n];
@@ -158,7 +173,11 @@ __device__ __forceinline__ double econ_trig(int n) {
 }
 template <int N>
 __device__ __forceinline__ double econ_exp(int n) {
-    if constexpr (N == 6) {
+    if constexpr (N == 5) {
+        constexpr double c[6] = {0x1.0000000000001p+0, 0x1.0000000000000p+0, 0x1.ffffffffac1d3p-2,
+                                 0x1.5555555555555p-3, 0x1.555604189374cp-5, 0x1.1111111111111p-7};
+        return c[n];
+    } else if constexpr (N == 6) {
         constexpr double c[7] = {1.0, 0x1.000000000002fp+0, 0x1.0000000000000p-1, 0x1.55555551aab14p-3,
                                  0x1.5555555555555p-5, 0x1.111359a8d0e59p-7, 0x1.6c16c16c16c17p-10};
         return c[n];
@@ -174,23 +193,28 @@ __device__ __forceinline__ double econ_exp(int n) {
     }
 }
 // 0 = out of range (direct evaluation by sinpi / cospi / exp)
-__device__ __forceinline__ int taylor_order(double zmax) {
-    return zmax <= 0.028 ? 6 : (zmax <= 0.05 ? 7 : (zmax <= 0.12 ? 9 : 0));
+__device__ __forceinline__ int taylor_order(double r) {
+    return r <= 0.0125 ? 5 : (r <= 0.028 ? 6 : (r <= 0.05 ? 7 : (r <= 0.12 ? 9 : 0)));
 }
 template <int N, int G>
 __device__ __forceinline__ AxisTaylor<N> axis_taylor(double x0, double x1, double x2, double x3) {
     AxisTaylor<N> a;
     const double sc = G == kTayExp ? 1.0 : kPi;
-    a.e1 = sc * (x1 - x0);
-    a.e2 = sc * (x2 - x0);
-    a.e3 = sc * (x3 - x0);
+    const double d1 = x1 - x0, d2 = x2 - x0, d3 = x3 - x0;
+    const double lo = fmin(fmin(0.0, d1), fmin(d2, d3)), hi = fmax(fmax(0.0, d1), fmax(d2, d3));
+    // the expansion point xc and the offset xc - x0 it really has
+    const double xc = x0 + 0.5 * (lo + hi);
+    a.e1 = sc * d1;
+    a.e2 = sc * d2;
+    a.e3 = sc * d3;
+    a.em = -sc * (xc - x0);
     if constexpr (G == kTayExp) {
-        const double e0 = exp(x0);
+        const double e0 = exp(xc);
 #pragma unroll
         for (int n = 0; n <= N; ++n) a.k[n] = e0 * econ_exp<N>(n);
     } else {
         double s0, c0;
-        sincospi(x0, &s0, &c0);
+        sincospi(xc, &s0, &c0);
         // derivative cycle of sin: s c -s -c; of cos: c -s -c s
         const double d[4] = {G == kTaySin ? s0 : c0, G == kTaySin ? c0 : -s0, G == kTaySin ? -s0 : -c0,
                              G == kTaySin ? -c0 : s0};

@@ -1,6 +1,6 @@
 """The economised series tables of problems.cuh (econ_trig / econ_exp) are
 the ones tools/econ_tables.py derives, and their truncation error on each
-class interval is below half an ulp (CPU, mpmath)."""
+class interval is below half an ulp (one ulp for the N = 5 class) (CPU, mpmath)."""
 import os
 import re
 import subprocess
@@ -19,11 +19,13 @@ def test_tables_match_generator():
     exp = [ln for ln in out if ln.startswith("exp")]
     gen = [float.fromhex(v) for v in re.findall(r"0x[0-9a-f.]+p[+-]\d+", "\n".join(trig + exp))]
     src = open(os.path.join(ROOT, "paper_2509_11133_b200", "csrc", "problems.cuh")).read()
-    body = src[src.index("econ_trig(int n)"):src.index("taylor_order(double zmax)")]
+    body = src[src.index("econ_trig(int n)"):src.index("taylor_order(double r)")]
     shipped = [float.fromhex(v) if v.startswith("0x") else float(v)
                for v in re.findall(r"(0x[0-9a-f.]+p[+-]\d+|1\.0(?=[,}]))", body)]
     assert gen == shipped
     for ln in out:
         if ln.startswith("//"):
             errs = [float(x) for x in re.findall(r"(?:cos|sin|exp) ([0-9.e+-]+)", ln)]
-            assert len(errs) == 3 and max(errs) < 5.6e-17, ln  # half an ulp of 1
+            # half an ulp of 1 for N >= 6; one ulp (2.2e-16, +5%) for the N = 5 class
+            bound = 2.35e-16 if ln.startswith("// N = 5,") else 5.6e-17
+            assert len(errs) == 3 and max(errs) < bound, ln

@@ -371,9 +371,11 @@ def test_async_upload_matches_sync(oracle):
 
 
 @pytest.mark.parametrize("kind", [3, 4, 5])
-@pytest.mark.parametrize("h", [1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20])  # economised orders 6, 7, 9 and direct
+# half spans r = pi (max - min) / 2 up to 0.7 pi h (jitter 0.2): economised
+# orders 5, 5 + 6, 6, 7, 9 and the direct evaluation
+@pytest.mark.parametrize("h", [1.0 / 200, 1.0 / 160, 1.0 / 100, 1.0 / 48, 1.0 / 20, 1.0 / 10])
 def test_small_element_load_paths(oracle, kind, h):
-    """The series load vector (economised orders 6, 7, 9 by element size,
+    """The series load vector (economised orders 5, 6, 7, 9 by element size,
     see problems.cuh taylor_order) against the oracle's libm evaluation: small
     jittered Kuhn meshes with cells of size h, moved away from the origin so
     that sin and cos are both far from zero."""

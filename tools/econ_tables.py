@@ -3,7 +3,7 @@
 For each (N, r): start from the Taylor series of degree N + extra and remove
 the top terms one at a time through T_m(z / r) on [-r, r] (telescoping
 economisation), leaving degree N.  The shipped tables (no arguments) use
-extra = 1, except trig N = 6 with extra = 2.  Trig: the even coefficients come from
+extra = 1, except trig N = 5 and N = 6 with extra = 2.  Trig: the even coefficients come from
 cos z, the odd ones from sin z (sin(t0 + z) = sin t0 cos z + cos t0 sin z and
 cos(t0 + z) likewise, so one table of magnitudes serves both with the signs
 of the derivative cycle); exp: e^z.  Prints the C++ hex tables and the max
@@ -97,7 +97,7 @@ def main():
         extra = int(args.pop(0).split("=")[1])
     # the shipped classes: (N, r, trig extra, exp extra)
     specs = [(int(n), r, extra or 1, extra or 1) for n, r in (a.split(":") for a in args)] or [
-        (6, "0.028", 2, 1), (7, "0.05", 1, 1), (9, "0.12", 1, 1)]
+        (5, "0.0125", 2, 1), (6, "0.028", 2, 1), (7, "0.05", 1, 1), (9, "0.12", 1, 1)]
     for n, r, xt, xe in specs:
         trig, ex, err = table(n, r, xt, xe)
         print(f"// N = {n}, |z| <= {r}: cos {float(err['cos']):.1e}, sin {float(err['sin']):.1e}, "
