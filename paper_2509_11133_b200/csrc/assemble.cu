@@ -65,28 +65,6 @@ struct Slots {
     bool owner[4], bnd[4];
 };
 
-__device__ __forceinline__ void load_slots(int64_t t, const int32_t* __restrict__ face_of_slot,
-                                           const int32_t* __restrict__ slot_mate,
-                                           const int32_t* __restrict__ face_mrow, Slots& s) {
-    const int4 mate4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-    const int4 fos4 = __ldg(reinterpret_cast<const int4*>(face_of_slot) + t);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int32_t sl = (int32_t)(4 * t + q);
-        const int32_t mate = tv(mate4, q);
-        s.face[q] = tv(fos4, q);
-        s.row[q] = __ldg(face_mrow + s.face[q]);
-        s.owner[q] = mate < 0 || mate > sl;
-        s.bnd[q] = mate < 0;
-    }
-}
-
-#ifndef PHG_LOCKSTEP
-#define PHG_LOCKSTEP 1  // the four points' series evaluated side by side
-#endif
-#ifndef PHG_STAGE
-#define PHG_STAGE 1  // stage the post-load-vector gathers in shared memory (cp.async)
-#endif
 // cp.async (LDGSTS): a gather that lands in shared memory without holding a
 // register or a scoreboard; waited for with cp_async_wait_all
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -155,7 +133,6 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
             const double ax = fma(l2, tx.e2, fma(l1, tx.e1, tx.em)), ay = fma(l2, ty.e2, fma(l1, ty.e1, ty.em)),
                          az = fma(l2, tz.e2, fma(l1, tz.e1, tz.em)), al = fma(l2, d2, fma(l1, d1, c0));
             double fw[4];
-#if PHG_LOCKSTEP
             // the 12 (kind 3) or 8 series of the four points in lockstep:
             // independent FMA chains side by side for the dependent-issue
             // latency
@@ -197,28 +174,6 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
                 }
                 fw[c] = c_w5[qp] * f;
             }
-#else
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int qp = 16 * a + 4 * bb + c;
-                const double l3 = c_l3[qp];
-                double f;
-                if constexpr (KIND == 3) {
-                    // the constant factor cpre is applied once after the loop
-                    f = horner(tx, fma(l3, tx.e3, ax)) * horner(ty, fma(l3, ty.e3, ay)) *
-                        horner(tz, fma(l3, tz.e3, az));
-                } else if constexpr (KIND == 4) {
-                    const double zc = fma(l3, d3, al);
-                    const double ec = horner(tx, fma(l3, tx.e3, ax)) * horner(ty, fma(l3, ty.e3, ay));
-                    f = fma(cpre, ec * (zc * zc), -(k.a2 * 2.0) * ec);
-                } else {
-                    const double xc = fma(l3, d3, al);
-                    const double sv = horner(ty, fma(l3, ty.e3, ay)) * horner(tz, fma(l3, tz.e3, az));
-                    f = fma(cpre, xc * (8.0 - xc) * sv, 2.0 * k.a0 * sv);
-                }
-                fw[c] = c_w5[qp] * f;
-            }
-#endif
             const int q0 = 16 * a + 4 * bb;
             b3 = fma(fw[2], c_l3[q0 + 2], fma(fw[0], c_l3[q0], b3));
             b3o = fma(fw[3], c_l3[q0 + 3], fma(fw[1], c_l3[q0 + 1], b3o));
@@ -315,7 +270,6 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
                                              int32_t* __restrict__ slot_mrow, Dv& dv) {
     // elem_volume == local.volume (assembly.cpp:18, 47)
     double bt[4];
-#if PHG_STAGE
     __shared__ Stage stg;
     const int tid = threadIdx.x;
     {
@@ -362,33 +316,6 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     double area[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) area[q] = stg.area[q][tid];
-#else
-    {
-        const int4 e = ldtet(tets, t);
-        const V3 p0[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
-        const double det = vdot(vcross(vsub(p0[1], p0[0]), vsub(p0[2], p0[0])), vsub(p0[3], p0[0]));
-        if (det == 0.0) return 3;
-        load_vector<KIND>(p0, load_coef(prob, t), dq(fabs(det), kDiv6), bt);
-    }
-    // coordinates and coefficients again (L1/L2 hits) rather than keeping
-    // them live through the load vector's Taylor coefficients
-    V3 p[4];
-    {
-        const int4 e = ld_fresh(reinterpret_cast<const int4*>(tets) + t);
-        p[0] = ldnode_fresh(coords, e.x);
-        p[1] = ldnode_fresh(coords, e.y);
-        p[2] = ldnode_fresh(coords, e.z);
-        p[3] = ldnode_fresh(coords, e.w);
-    }
-    const Coef k = load_coef_fresh(prob, t);
-    // the face-side gathers only now, after the fp64-heavy load vector (the
-    // other warps of the SM cover their latency)
-    Slots sl;
-    load_slots(t, fin.face_of_slot, fin.slot_mate, fin.face_mrow, sl);
-    double area[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) area[q] = __ldg(fin.face_area + sl.face[q]);
-#endif
     // boundary data (boundary_terms_k): Neumann terms (assembly.cpp:81-94;
     // this element's Neumann faces in face order == local slot order) and
     // Dirichlet traces b_D = |F| u_D(centroid) (assembly.cpp:96-104)
@@ -398,11 +325,7 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     for (int q = 0; q < 4; ++q) {
         bdv[q] = 0.0;
         if (!sl.bnd[q]) continue;
-#if PHG_STAGE
         const double v = stg.bval[q][tid];
-#else
-        const double v = __ldg(fin.face_bval + sl.face[q]);
-#endif
         if (sl.row[q] >= 0) {
             bdv[q] = v;
             continue;

@@ -122,16 +122,6 @@ __device__ __forceinline__ double ld_fresh(const double* p) {
     asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ int4 ld_fresh(const int4* p) {
-    int4 v;
-    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ V3 ldnode_fresh(const double* __restrict__ c, int32_t n) {
-    const double* p = c + 3 * (int64_t)n;
-    return {ld_fresh(p), ld_fresh(p + 1), ld_fresh(p + 2)};
-}
-
 __device__ __forceinline__ int4 ldtet(const int32_t* __restrict__ tets, int64_t t) {
     return __ldg(reinterpret_cast<const int4*>(tets) + t);
 }
