@@ -440,15 +440,20 @@ def main():
     barrier()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
+    # at least 20 steps: the first step's upload has nothing to overlap with
+    # and is charged in full to the timed region
+    n_e2e = max(args.steps, 20)
     e2.record(stream)
     t_wall = time.perf_counter()
-    cts = e2e_steps(args.steps)
+    cts = e2e_steps(n_e2e)
     e3.record(stream)
     e3.synchronize()
-    wall = (time.perf_counter() - t_wall) / args.steps
-    e2e_ms = max(e2.elapsed_time(e3) / args.steps, wall * 1e3)
+    wall = (time.perf_counter() - t_wall) / n_e2e
+    e2e_ms = max(e2.elapsed_time(e3) / n_e2e, wall * 1e3)
     e2e = {"value": job_throughput(world, ne, max_over_ranks(dist, e2e_ms, "cuda")), "unit": "tets/s",
-           "overlap": "double-buffered uploads on the copy engine (create_from_arrays_async)",
+           "overlap": "double-buffered uploads on the copy engine (create_from_arrays_async); "
+                      "the first step's upload is not overlapped",
+           "steps": n_e2e, "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(cts.nbytes + 7 * 8)}
 

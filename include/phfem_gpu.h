@@ -76,6 +76,12 @@ int phfem_gpu_split_counts(const int32_t* packed, int32_t* dir, int32_t* neu, in
 int phfem_gpu_check_indices(const int32_t* a, int64_t n, int64_t nc, unsigned long long* first_bad,
                             void* stream);
 
+/* small device-to-host reads without the copy engine: word i of dst (host
+ * memory mapped into the device address space) = *src[i], i < n <= 16.  A
+ * cudaMemcpyAsync D2H queues behind a running H2D upload on the copy
+ * engine; this kernel does not. */
+int phfem_gpu_gather_words(const unsigned long long* const* src, int n, unsigned long long* dst, void* stream);
+
 /* max element diameter (mesh.cpp:90-106); out: one double (device) */
 int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, double* out,
                        double* partials, void* stream);

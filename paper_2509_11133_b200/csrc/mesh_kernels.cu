@@ -227,6 +227,28 @@ extern "C" int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned lo
     return (int)cudaGetLastError();
 }
 
+namespace {
+struct WordPtrs {
+    const unsigned long long* p[16];
+};
+__global__ void gather_words_k(WordPtrs s, int n, unsigned long long* dst) {
+    const int i = threadIdx.x;
+    if (i < n) dst[i] = *s.p[i];
+    __threadfence_system();
+}
+}  // namespace
+
+extern "C" int phfem_gpu_gather_words(const unsigned long long* const* src, int n, unsigned long long* dst,
+                                      void* stream) {
+    if (n <= 0) return 0;
+    if (n > 16) return (int)cudaErrorInvalidValue;
+    WordPtrs w{};
+    for (int i = 0; i < n; ++i) w.p[i] = src[i];
+    gather_words_k<<<1, 32, 0, (cudaStream_t)stream>>>(w, n, dst);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int phfem_gpu_check_indices(const int32_t* a, int64_t n, int64_t nc, unsigned long long* first_bad,
                                        void* stream) {
     if (n <= 0) return 0;

@@ -21,16 +21,16 @@ void reset_err(Work& w) {
     w.err.fill_bytes(0xff);
 }
 
-// read several device scalars with one synchronisation
+// read several device scalars with one synchronisation (read_words)
 template <class T, size_t N>
 std::array<T, N> read_many(const std::array<const T*, N>& src) {
-    static thread_local T* pinned = nullptr;
-    if (!pinned) check(cudaMallocHost(reinterpret_cast<void**>(&pinned), 64 * sizeof(T)), "pinned alloc");
-    for (size_t i = 0; i < N; ++i)
-        check(cudaMemcpyAsync(pinned + i, src[i], sizeof(T), cudaMemcpyDeviceToHost, S()), "D2H");
-    sync();
+    static_assert(sizeof(T) == 8 && N <= 16, "8-byte words, at most 16");
+    const unsigned long long* p[N];
+    for (size_t i = 0; i < N; ++i) p[i] = reinterpret_cast<const unsigned long long*>(src[i]);
+    unsigned long long w[N];
+    read_words(p, (int)N, w);
     std::array<T, N> out;
-    for (size_t i = 0; i < N; ++i) out[i] = pinned[i];
+    for (size_t i = 0; i < N; ++i) std::memcpy(&out[i], &w[i], sizeof(T));
     return out;
 }
 

@@ -84,21 +84,40 @@ cudaEvent_t Stages::mark() {
 void Stages::span(double* field, cudaEvent_t from) { pending_.emplace_back(field, from, mark()); }
 void Stages::span(double* field, cudaEvent_t from, cudaEvent_t to) { pending_.emplace_back(field, from, to); }
 namespace {
-// page-locked slots for deferred error reads (allocated once: cudaMallocHost
-// synchronises the device)
-unsigned long long* err_slot(size_t i) {
-    constexpr size_t kSlots = 16;
+// host memory mapped into the device address space, written by
+// phfem_gpu_gather_words (allocated once per thread: cudaHostAlloc
+// synchronises the device): slot 0 for read_words, 1.. for deferred error
+// reads
+constexpr size_t kWordSlots = 17;
+unsigned long long* word_slot(size_t i) {
     static thread_local unsigned long long* base = nullptr;
-    if (!base) check(cudaMallocHost(reinterpret_cast<void**>(&base), kSlots * 8 * sizeof(unsigned long long)), "pinned");
-    if (i >= kSlots) throw MeshError("too many deferred error checks");
-    return base + 8 * i;
+    if (!base)
+        check(cudaHostAlloc(reinterpret_cast<void**>(&base), kWordSlots * 16 * sizeof(unsigned long long),
+                            cudaHostAllocMapped | cudaHostAllocPortable),
+              "mapped alloc");
+    if (i >= kWordSlots) throw MeshError("too many deferred error checks");
+    return base + 16 * i;
+}
+void gather_to(const unsigned long long* const* src, int n, unsigned long long* h) {
+    unsigned long long* d = nullptr;
+    check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0), "mapped pointer");
+    check(phfem_gpu_gather_words(src, n, d, S()), "gather words");
 }
 }  // namespace
 
+void read_words(const unsigned long long* const* src, int n, unsigned long long* out) {
+    if (n > 16) throw MeshError("read_words: at most 16 words");
+    volatile unsigned long long* h = word_slot(0);
+    gather_to(src, n, const_cast<unsigned long long*>(h));
+    sync();
+    for (int i = 0; i < n; ++i) out[i] = h[i];
+}
+
 void Stages::defer_errors(const unsigned long long* dev_err, std::function<void(const unsigned long long*)> f) {
-    unsigned long long* h = err_slot(checks_.size());
-    check(cudaMemcpyAsync(h, dev_err, PHG_ERR_COUNT * sizeof(unsigned long long), cudaMemcpyDeviceToHost, S()),
-          "D2H");
+    unsigned long long* h = word_slot(1 + checks_.size());
+    const unsigned long long* src[PHG_ERR_COUNT];
+    for (int i = 0; i < PHG_ERR_COUNT; ++i) src[i] = dev_err + i;
+    gather_to(src, PHG_ERR_COUNT, h);
     checks_.emplace_back(h, std::move(f));
 }
 

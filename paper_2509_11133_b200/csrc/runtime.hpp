@@ -3,6 +3,7 @@
 // orchestration that calls the kernels through phfem_gpu.h.
 #pragma once
 
+#include <cstring>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -120,11 +121,19 @@ struct DBuf {
     }
 };
 
+// n <= 16 device words to the host in one synchronisation, through host
+// memory mapped into the device (phfem_gpu_gather_words): no copy-engine
+// transfer, so the read does not wait behind an upload in flight
+void read_words(const unsigned long long* const* src, int n, unsigned long long* out);
+
 template <class T>
 T read_scalar(const T* dptr) {
-    T v{};
-    check(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, S()), "D2H");
-    sync();
+    static_assert(sizeof(T) == 8, "read_scalar reads one 8-byte word");
+    const unsigned long long* src[1] = {reinterpret_cast<const unsigned long long*>(dptr)};
+    unsigned long long w;
+    read_words(src, 1, &w);
+    T v;
+    std::memcpy(&v, &w, sizeof(T));
     return v;
 }
 

@@ -21,3 +21,17 @@ for i in range(5):
 for i in range(3):
     t1 = time.perf_counter(); st, _ = m.pipeline(cfg.problem, True); t2 = time.perf_counter()
     print(f"resident pipeline {1e3*(t2-t1):.2f} ms (device {st['total']:.2f})")
+# double-buffered e2e loop as in bench.py, per-step wall and device totals
+nxt = ph.Mesh.from_arrays_async(hc, ht, hd, hn)
+for k in range(6):
+    t0 = time.perf_counter()
+    cur = nxt
+    nxt = ph.Mesh.from_arrays_async(hc, ht, hd, hn)
+    t1 = time.perf_counter()
+    st, _ = cur.pipeline(cfg.problem, True)
+    t2 = time.perf_counter()
+    del cur
+    t3 = time.perf_counter()
+    print(f"e2e step: enqueue upload {1e3*(t1-t0):.2f} ms  pipeline {1e3*(t2-t1):.2f} ms (device {st['total']:.2f}: "
+          + " ".join(f"{n} {st[n]:.2f}" for n in ('star', 'groups', 'number', 'classify', 'assemble', 'refine'))
+          + f")  destroy {1e3*(t3-t2):.2f} ms")
