@@ -211,7 +211,8 @@ int phfem_gpu_assemble_grid(int64_t ne);
 typedef struct phg_cg_state {
     double rz, pq, alpha, beta, rnorm, bnorm, stop, rel_residual;
     long long it, max_iter;
-    int done, converged, not_spd, pad;
+    int done, converged, not_spd;
+    int x_pending; /* set with done by the stop test: cg_pdir still adds alpha p to x */
     unsigned int counter[4];
 } phg_cg_state;
 

@@ -2,9 +2,12 @@
 // sparse.cpp:163-212, with the stopping rule of inner_cg_options,
 // solver.cpp:78-86).  Three kernels per iteration:
 //   spmv   q = S p, partial p.q; last block: alpha = rz / pq
-//   update x += alpha p, r -= alpha q, z = d r, partials r.r, r.z;
+//   update r -= alpha q, z = d r, partials r.r, r.z;
 //          last block: stop test, beta = rz'/rz
-//   pdir   p = d r + beta p
+//   pdir   x += alpha p, p = d r + beta p
+// The reference's x += alpha p (before the stop test) runs in pdir, which
+// reads p anyway: one vector pass fewer per iteration, the same arithmetic
+// (on the stopping iteration pdir updates x only).
 // Scalars live in device memory (phg_cg_state); kernels become no-ops once
 // `done` is set, so the host can enqueue batches of iterations (captured in
 // a CUDA graph) and poll rarely.  Every reduction is a fixed-shape tree over
@@ -124,7 +127,11 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     cg_spmv(int64_t l, const int32_t* __restrict__ sell_col, const double* __restrict__ sell_val,
             const double* __restrict__ p, double* __restrict__ q, phg_cg_state* st, double* partials) {
-    if (st->done) return;
+    if (st->done) {
+        // the stopping iteration's pdir has run: nothing pending for x
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->x_pending = 0;
+        return;
+    }
     double acc[1] = {0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t base = (i >> 5) * (PHG_SELL_C * PHG_SELL_W) + (i & 31);
@@ -154,22 +161,17 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 __global__ void __launch_bounds__(kThreads)
-    cg_update(int64_t l, double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-              const double* __restrict__ q, const double* __restrict__ d, phg_cg_state* st, double* partials) {
+    cg_update(int64_t l, double* __restrict__ r, const double* __restrict__ q, const double* __restrict__ d,
+              phg_cg_state* st, double* partials) {
     if (st->done) return;
     const double alpha = st->alpha;
     double acc[2] = {0.0, 0.0};
     // two rows per thread and step (16 B accesses: twice the bytes in flight)
     const int64_t l2 = l / 2;
-    const double2 *p2 = reinterpret_cast<const double2*>(p), *q2 = reinterpret_cast<const double2*>(q),
-                  *d2 = reinterpret_cast<const double2*>(d);
-    double2 *x2 = reinterpret_cast<double2*>(x), *r2 = reinterpret_cast<double2*>(r);
+    const double2 *q2 = reinterpret_cast<const double2*>(q), *d2 = reinterpret_cast<const double2*>(d);
+    double2* r2 = reinterpret_cast<double2*>(r);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 pi = p2[i], qi = q2[i], di = d2[i], ri = r2[i];
-        double2 xi = x2[i];
-        xi.x += alpha * pi.x;
-        xi.y += alpha * pi.y;
-        x2[i] = xi;
+        const double2 qi = q2[i], di = d2[i], ri = r2[i];
         const double ra = ri.x - alpha * qi.x, rb = ri.y - alpha * qi.y;
         r2[i] = make_double2(ra, rb);
         acc[0] += ra * ra;
@@ -179,7 +181,6 @@ __global__ void __launch_bounds__(kThreads)
     }
     if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail row
         const int64_t i = l - 1;
-        x[i] += alpha * p[i];
         const double ri = r[i] - alpha * q[i];
         r[i] = ri;
         acc[0] += ri * ri;
@@ -196,8 +197,10 @@ __global__ void __launch_bounds__(kThreads)
         if (rnorm <= st->stop) {
             st->converged = 1;
             st->done = 1;
+            st->x_pending = 1;
         } else if (it >= st->max_iter) {
             st->done = 1;
+            st->x_pending = 1;
         } else {
             st->beta = tot[1] / st->rz;
             st->rz = tot[1];
@@ -206,18 +209,30 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 __global__ void __launch_bounds__(kThreads)
-    cg_pdir(int64_t l, const double* __restrict__ r, double* __restrict__ p, const double* __restrict__ d,
-            const phg_cg_state* st) {
-    if (st->done) return;
-    const double beta = st->beta;
+    cg_pdir(int64_t l, double* __restrict__ x, const double* __restrict__ r, double* __restrict__ p,
+            const double* __restrict__ d, const phg_cg_state* st) {
+    if (st->done && !st->x_pending) return;
+    const bool last = st->done;  // the stopping iteration: x only
+    const double alpha = st->alpha, beta = st->beta;
     const int64_t l2 = l / 2;
     const double2 *r2 = reinterpret_cast<const double2*>(r), *d2 = reinterpret_cast<const double2*>(d);
-    double2* p2 = reinterpret_cast<double2*>(p);
+    double2 *p2 = reinterpret_cast<double2*>(p), *x2 = reinterpret_cast<double2*>(x);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
-        const double2 ri = r2[i], di = d2[i], pi = p2[i];
-        p2[i] = make_double2(di.x * ri.x + beta * pi.x, di.y * ri.y + beta * pi.y);
+        const double2 pi = p2[i];
+        double2 xi = x2[i];
+        xi.x += alpha * pi.x;
+        xi.y += alpha * pi.y;
+        x2[i] = xi;
+        if (!last) {
+            const double2 ri = r2[i], di = d2[i];
+            p2[i] = make_double2(di.x * ri.x + beta * pi.x, di.y * ri.y + beta * pi.y);
+        }
     }
-    if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[l - 1] = d[l - 1] * r[l - 1] + beta * p[l - 1];
+    if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const int64_t i = l - 1;
+        x[i] += alpha * p[i];
+        if (!last) p[i] = d[i] * r[i] + beta * p[i];
+    }
 }
 
 }  // namespace
@@ -239,8 +254,8 @@ extern "C" int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col
     const int g = cg_grid(l);
     for (int i = 0; i < n; ++i) {
         cg_spmv<<<g, kThreads, 0, s>>>(l, sell_col, sell_val, p, q, st, partials); phg::count_launches(1);
-        cg_update<<<g, kThreads, 0, s>>>(l, x, r, p, q, d, st, partials); phg::count_launches(1);
-        cg_pdir<<<g, kThreads, 0, s>>>(l, r, p, d, st); phg::count_launches(1);
+        cg_update<<<g, kThreads, 0, s>>>(l, r, q, d, st, partials); phg::count_launches(1);
+        cg_pdir<<<g, kThreads, 0, s>>>(l, x, r, p, d, st); phg::count_launches(1);
     }
     return (int)cudaGetLastError();
 }
