@@ -1,6 +1,7 @@
 """Full BASELINE.json sizes on the GPU, checked through size-independent
-properties (the oracle is too slow at these sizes; tests/test_gpu_parity.py
-covers the same code paths bit for bit at scaled sizes):
+properties (tests/test_gpu_fullsize_parity.py compares configs 3-5 at full
+size with the oracle element for element; the refined 151M-tet mesh and the
+full-size solves are beyond what the serial oracle finishes in a test):
 
 * config 4 (Kuhn 128^3 x 6 = 12.6M tets): closed-form vertex / edge counts,
   Euler characteristic V - E + F - T = 1 of a ball, boundary face counts by
