@@ -11,11 +11,14 @@ connectivity and the condensed system:
 * element blocks A_T, C_T coefficients and rows, the SELL-32 Schur matrix S
   bit-exact; load vectors B_T, rhs_neg and b_D within 1e-12 relative (max
   norm) for the transcendental data (libdevice vs libm, economised series);
-* one red refinement of the full mesh bit-exact (configs 3 and 5).
+* one red refinement of the full mesh bit-exact (configs 3 and 5);
+* config 2's ladder: the refined meshes of levels 6 and 7 (215M tets) and
+  the connectivity of level 6 bit for bit.
 
 The face solve itself is compared at scaled sizes in test_gpu_parity.py
-(the oracle's serial CG would take tens of minutes here).  Oracle time is
-~10 s per 1.6M-tet config and ~90 s for config 4 on one host core.
+(the oracle's serial CG would take tens of minutes here).  The module
+takes ~2.5 min on the GPU box (oracle on one host core; ~20 GB of host
+memory at config 4).
 """
 import numpy as np
 import pytest
@@ -60,3 +63,29 @@ def test_full_size_config4_connectivity_system(oracle):
     k = cfg.coefficients(m.ne)
     fo = check_connectivity(g, m, oracle)
     check_system(g, m, fo, oracle, cfg.problem, cfg.c, k["a_elem"], k["a_diag"])
+
+
+def test_config2_levels_6_and_7(oracle):
+    """Config 2's ladder (one cube -> 6 Kuhn tets, red refinement) past the
+    level-5 check of test_gpu_parity.py: the refined meshes of levels 6
+    (17.9M tets) and 7 (215M tets, the first level with >= 2e7 tets) bit for
+    bit, and the full edge and face tables of level 6 (the
+    oracle holds level 7's mesh but not its connectivity in a test)."""
+    m = oracle.kuhn(1, 1, 1, dmask=0x3F)
+    g = ph.Mesh.kuhn(1, 1, 1, dirichlet_mask=0x3F)
+    for _ in range(6):
+        m = oracle.refine(m)[0]
+        g.refine()
+    assert m.ne == 17915904
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(m, k)), k
+    del mg
+    check_connectivity(g, m, oracle)
+    m7 = oracle.refine(m)[0]
+    del m
+    g.refine()
+    assert m7.ne == 214990848
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(m7, k)), k
