@@ -822,13 +822,12 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 // classes staged in shared memory (striped in, blocked for the scan), rows
-// and the compacted row -> face list staged again and written out striped
+// staged again and written out striped, with the row -> face list
 __global__ void __launch_bounds__(kScanThreads)
     face_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, const long long* __restrict__ tile_off,
                 int32_t* __restrict__ face_mrow, int32_t* __restrict__ row_face) {
     __shared__ __align__(16) uint8_t s_cls[kScanTile];
     __shared__ int32_t s_row[kScanTile + kScanTile / 32];
-    __shared__ int32_t s_rf[kScanTile];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
     const int nt = (int)(nf - base < kScanTile ? nf - base : kScanTile);
     if (nt == kScanTile) {
@@ -842,8 +841,7 @@ __global__ void __launch_bounds__(kScanThreads)
     int n = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) n += ((w[i / 4] >> (8 * (i % 4))) & 0xffu) != 2;
-    long long tot;
-    int r = (int)block_excl_scan_ll<kScanThreads>(n, &tot);
+    int r = (int)block_excl_scan_ll<kScanThreads>(n);
     const long long off = tile_off[blockIdx.x];
     // local index i of the tile lives at s_row[i + i / 32] (one pad word per
     // 32: blocked writes of 16 consecutive words stay conflict-light)
@@ -852,7 +850,7 @@ __global__ void __launch_bounds__(kScanThreads)
         const int li = threadIdx.x * kScanItems + i;
         const bool row = ((w[i / 4] >> (8 * (i % 4))) & 0xffu) != 2;
         s_row[li + (li >> 5)] = row ? (int32_t)(off + r) : -1;
-        if (row) s_rf[r++] = (int32_t)(base + li);
+        r += row;
     }
     __syncthreads();
     if (nt == kScanTile) {
@@ -866,7 +864,12 @@ __global__ void __launch_bounds__(kScanThreads)
     } else {
         for (int i = threadIdx.x; i < nt; i += kScanThreads) face_mrow[base + i] = s_row[i + (i >> 5)];
     }
-    for (int j = threadIdx.x; j < (int)tot; j += kScanThreads) row_face[off + j] = s_rf[j];
+    // the inverse map, striped over the tile: a warp's rows are consecutive
+    // apart from the Neumann faces it skips
+    for (int i = threadIdx.x; i < nt; i += kScanThreads) {
+        const int32_t row = s_row[i + (i >> 5)];
+        if (row >= 0) row_face[row] = (int32_t)(base + i);
+    }
 }
 
 inline int grid_cap(int64_t n, int block) {
