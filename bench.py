@@ -469,9 +469,19 @@ def main():
                  "converged": r["converged"], "accepted_by_verify": r["accepted"], "residual": r["residual"],
                  "ms_per_iteration": r["ms_per_iteration"], "gbs_per_iteration": gbs,
                  "hbm_frac": gbs / hbm if gbs else None, "tol": cfg.tol}
+        # verify_solution's three tests (solver.cpp:68-69) with their values
+        t = cfg.tol
+        checks = {"combined": [r["residual"], t],
+                  "primal ||AU-C'L-B||/||B||": [r["r1"] / max(r["norm_rhs"], 1e-300), t],
+                  "constraint ||CU-b_D||/(1+||b_D||)": [r["r2"] / (1.0 + r["norm_bd"]), t]}
+        solve["verify"] = {k: {"value": float(v), "limit": lim, "pass": bool(v <= lim)} for k, (v, lim) in checks.items()}
+        solve["norm_bd"] = r["norm_bd"]
+        solve["norm_rhs"] = r["norm_rhs"]
         if not r["accepted"]:
-            solve["note"] = ("verify_solution refuses this converged solve, as the reference does "
-                             "(b_D = 0 here; SURVEY finding 8)")
+            failed = [k for k, c in solve["verify"].items() if not c["pass"]]
+            solve["note"] = (f"verify_solution refuses this converged solve (failed: {', '.join(failed)}; "
+                             f"||b_D|| = {r['norm_bd']:.3e}, ||B|| = {r['norm_rhs']:.3e}); the CPU oracle's "
+                             f"verdict on the same system is in tests/golden/solution_cfg*.npz (SURVEY finding 8)")
 
     fp64_peak = measure_fp64_peak(ph, torch, stream)
     if "fp64" in roofline:

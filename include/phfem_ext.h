@@ -99,6 +99,15 @@ int phfem_solve_ex(const phfem_mesh* mesh, int problem, double tol, int64_t max_
  * lambda [L] host output; out: [iterations, rel_residual, converged]. */
 int phfem_mesh_solve_faces(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
                            double* lambda, double out[3]);
+/* The whole Schur path (face solve, recovery, verify_solution's residuals,
+ * error norms) without raising on verify_solution's refusal of a converged
+ * solve (SURVEY finding 8), for parity checks of U and Lambda where the
+ * reference itself refuses.  u [4 nE], lambda [L] host outputs (may be
+ * NULL).  out: [iterations, residual, constraint_residual, converged,
+ * accepted, ||AU - C'L - B||, ||CU - b_D||, ||B||, ||b_D||, CG rel_residual,
+ * y-norm error, multiplier h-norm error, L2 error] */
+int phfem_mesh_solve_unverified(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
+                                double* u, double* lambda, double out[13]);
 /* out: [iterations, residual, constraint_residual, seconds] */
 int phfem_solution_stats(const phfem_solution* sol, double out[4]);
 /* out: [broken Y-norm error, multiplier h-norm error, L2 error] */
@@ -137,9 +146,10 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
  * recovery and verify_solution; a verify refusal (SURVEY finding 8) is
  * reported, not raised.  out: [iterations, cg_ms, ms_per_iteration,
  * converged, total_s (CG + recovery + verify wall time), accepted,
- * residual, constraint_residual] */
+ * residual, constraint_residual]; verify_terms (may be NULL): [||AU - C'L - B||,
+ * ||CU - b_D||, ||B||, ||b_D||] (verify_solution, solver.cpp:44-76) */
 int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter,
-                      double out[8]);
+                      double out[8], double* verify_terms);
 
 #ifdef __cplusplus
 }

@@ -1110,6 +1110,97 @@ int or_pcg(int64_t n, const int64_t* rowptr, const int32_t* col, const double* v
 /* ------------------------------------------------------------------------ */
 /* solve_schur_parallel (solver.cpp:149-186) + verify_solution (44-76)       */
 
+/* Componentwise magnitudes for per-entry parity of the load data (TEST
+ * INFRASTRUCTURE; no reference counterpart).  The GPU and the reference
+ * evaluate sin/cos/exp differently (libdevice / series vs glibc libm), so an
+ * entry of B_T or rhs_neg that is a cancelling sum cannot agree to 1e-12 of
+ * its own size; it agrees to 1e-12 of the magnitude its summands carry:
+ *   rhs_scale[4t+v] = sum_q |V w_q f(x_q)| lambda_v + sum |Neumann terms|
+ *                    (the summands of assembly.cpp:75 and :91),
+ *   rhsneg_scale[R] = |b_D[R]| + sum_T sum_p |c_r[p]| (|A_T^-1| rhs_scale_T)_p
+ *                    (first-order propagation of B_T through
+ *                    r_T = C A^-1 B, solver.cpp:111-119, 133-138). */
+int or_entry_scales(int64_t nc, int64_t ne, const double* coords, const int32_t* tets, int64_t nf,
+                    const int32_t* faces, const int32_t* face_of_slot, const int8_t* sigma,
+                    const int64_t* face_slots, const uint8_t* face_class, const int32_t* mrow,
+                    const double* area, int64_t l, const or_problem* prob, double* rhs_scale,
+                    double* rhsneg_scale) {
+    (void)nc;
+    const int kind = prob ? prob->kind : 0;
+    const double cc = prob ? prob->c : 1.0;
+    int rc = 0;
+    double lam[4 * 64], w[64];
+    or_tet_rule(5, lam, w);
+    for (int64_t i = 0; i < 4 * ne; ++i) rhs_scale[i] = 0.0;
+    for (int64_t t = 0; t < ne; ++t) {
+        const int32_t* e = tets + 4 * t;
+        const v3 p[4] = {node(coords, e[0]), node(coords, e[1]), node(coords, e[2]), node(coords, e[3])};
+        const double vol = fabs(vdot(vcross(vsub(p[1], p[0]), vsub(p[2], p[0])), vsub(p[3], p[0]))) / 6.0;
+        double Ac[3];
+        coef_of(prob, t, Ac);
+        for (int q = 0; q < 64; ++q) {
+            const double* L = lam + 4 * q;
+            const v3 x = vadd(vadd(vadd(vmul(p[0], L[0]), vmul(p[1], L[1])), vmul(p[2], L[2])), vmul(p[3], L[3]));
+            const double fw = fabs(vol * w[q] * orp_f(kind, x.x, x.y, x.z, Ac, cc));
+            for (int v = 0; v < 4; ++v) rhs_scale[4 * t + v] += fw * L[v];
+        }
+    }
+    for (int64_t f = 0; f < nf && !rc; ++f) {
+        if (face_class[f] != 2) continue;
+        const int64_t slot = face_slots[2 * f];
+        const int64_t t = slot / 4;
+        const int k = (int)(slot % 4);
+        double ar;
+        v3 un;
+        rc = face_geom(coords, faces + 3 * f, &ar, &un);
+        if (rc) break;
+        const v3 cen = face_centroid(coords, faces + 3 * f);
+        double Ac[3];
+        coef_of(prob, t, Ac);
+        const double nn[3] = {un.x, un.y, un.z};
+        const double gc = orp_g(kind, cen.x, cen.y, cen.z, nn, Ac);
+        for (int v = 0; v < 3; ++v) rhs_scale[4 * t + kFaceVerts[k][v]] += fabs(ar * gc / 3.0);
+    }
+    if (rc) return rc;
+    for (int64_t r = 0; r < l; ++r) rhsneg_scale[r] = 0.0;
+    for (int64_t f = 0; f < nf; ++f) {
+        if (face_class[f] != 1) continue;
+        const v3 cen = face_centroid(coords, faces + 3 * f);
+        rhsneg_scale[mrow[f]] = fabs(area[f] * orp_u(kind, cen.x, cen.y, cen.z));
+    }
+    for (int64_t t = 0; t < ne && !rc; ++t) {
+        double Ac[3];
+        coef_of(prob, t, Ac);
+        local_mats lm;
+        rc = local_stiffness_mass(coords, tets + 4 * t, t, Ac, cc, &lm);
+        if (rc) break;
+        lu4 lu;
+        lu_factor(lm.a, &lu);
+        if (lu.singular) continue;
+        double ainv[4][4]; /* columns of A^-1 */
+        for (int j = 0; j < 4; ++j) {
+            double ej[4] = {0.0, 0.0, 0.0, 0.0};
+            ej[j] = 1.0;
+            lu_solve(&lu, ej, ainv[j]);
+        }
+        double prop[4];
+        for (int pp = 0; pp < 4; ++pp) {
+            prop[pp] = 0.0;
+            for (int j = 0; j < 4; ++j) prop[pp] += fabs(ainv[j][pp]) * rhs_scale[4 * t + j];
+        }
+        for (int r = 0; r < 4; ++r) {
+            const int64_t slot = 4 * t + r;
+            const int32_t R = mrow[face_of_slot[slot]];
+            if (R < 0) continue;
+            const double cf = fabs((double)sigma[slot] * area[face_of_slot[slot]] / 3.0);
+            double s = 0.0;
+            for (int v = 0; v < 3; ++v) s += cf * prop[kFaceVerts[r][v]];
+            rhsneg_scale[R] += s;
+        }
+    }
+    return rc;
+}
+
 int or_solve_schur(int64_t nc, int64_t ne, const double* coords, const int32_t* tets,
                    const or_problem* prob, int64_t l, const double* slot_coef,
                    const int32_t* slot_mrow, const double* rhs, const double* bd,

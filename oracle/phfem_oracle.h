@@ -92,6 +92,15 @@ int or_assemble_condense(int64_t nc, int64_t ne, const double* coords, const int
                          int32_t* c_col, double* c_val, int64_t* s_rowptr, int32_t* s_col,
                          double* s_val, double* rhs_neg, int64_t* s_nnz);
 
+/* Componentwise magnitudes for per-entry parity of B_T (rhs_scale [4 nE])
+ * and rhs_neg (rhsneg_scale [L]): the summed magnitudes of their summands
+ * (test infrastructure, see phfem_oracle.c). */
+int or_entry_scales(int64_t nc, int64_t ne, const double* coords, const int32_t* tets, int64_t nf,
+                    const int32_t* faces, const int32_t* face_of_slot, const int8_t* sigma,
+                    const int64_t* face_slots, const uint8_t* face_class, const int32_t* mrow,
+                    const double* area, int64_t l, const or_problem* prob, double* rhs_scale,
+                    double* rhsneg_scale);
+
 /* pcg_jacobi (sparse.cpp:163-212).  res out: [iterations, rel_residual,
  * converged]. */
 int or_pcg(int64_t n, const int64_t* rowptr, const int32_t* col, const double* val,

@@ -30,6 +30,7 @@ __constant__ double c_w5[64];
 __constant__ double c_l1[4];
 __constant__ double c_l2[16];
 __constant__ double c_l3[64];
+__constant__ double c_l0[64];  // lambda0 of each point, as the rule stores it
 }  // namespace phg
 
 extern "C" int phfem_gpu_set_rules_errors(const double* lam9, const double* w9);
@@ -99,8 +100,9 @@ struct Stage {
 //       A(a, b) = fma(lambda2, e2, fma(lambda1, e1, em)) once per (a, b): the
 //       same operations as the per-point fma chain, a third of the cost;
 //   b1 = sum_a lambda1(a) T_a, b2 = sum_ab lambda2(a, b) U_ab with the
-//       partial sums U_ab = sum_c w f, T_a = sum_b U_ab, b3 per point, and
-//       b0 = S - b1 - b2 - b3 (lambda0 = 1 - lambda1 - lambda2 - lambda3).
+//       partial sums U_ab = sum_c w f, T_a = sum_b U_ab, b3 and b0 per point
+//       (b0 accumulates w f lambda0 itself, as assembly.cpp:75 does: forming
+//       it as S - b1 - b2 - b3 cancels where f changes sign in the element).
 template <int N>
 __device__ __forceinline__ double horner(const AxisTaylor<N>& t, double z) {
     double r = t.k[N];
@@ -121,9 +123,10 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
     const double c0 = KIND == 4 ? p[0].z : p[0].x;
     const double d1 = (KIND == 4 ? p[1].z : p[1].x) - c0, d2 = (KIND == 4 ? p[2].z : p[2].x) - c0,
                  d3 = (KIND == 4 ? p[3].z : p[3].x) - c0;
-    // two b3 accumulators and a pairwise U keep the per-(a, b) dependency
-    // chains at depth 2 (the loop is short of independent work otherwise)
-    double S = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0, b3o = 0.0;
+    // two b3 / b0 accumulators and a pairwise U keep the per-(a, b)
+    // dependency chains at depth 2 (the loop is short of independent work
+    // otherwise)
+    double b0 = 0.0, b0o = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0, b3o = 0.0;
     for (int a = 0; a < 4; ++a) {
         const double l1 = c_l1[a];
         double T = 0.0;
@@ -177,16 +180,18 @@ __device__ __forceinline__ void load_taylor(const V3 p[4], double cpre, const Co
             const int q0 = 16 * a + 4 * bb;
             b3 = fma(fw[2], c_l3[q0 + 2], fma(fw[0], c_l3[q0], b3));
             b3o = fma(fw[3], c_l3[q0 + 3], fma(fw[1], c_l3[q0 + 1], b3o));
+            b0 = fma(fw[2], c_l0[q0 + 2], fma(fw[0], c_l0[q0], b0));
+            b0o = fma(fw[3], c_l0[q0 + 3], fma(fw[1], c_l0[q0 + 1], b0o));
             const double U = (fw[0] + fw[1]) + (fw[2] + fw[3]);
             T += U;
             b2 = fma(U, l2, b2);
         }
-        S += T;
         b1 = fma(T, l1, b1);
     }
     b3 += b3o;
+    b0 += b0o;
     const double sc = KIND == 3 ? vol * cpre : vol;
-    b[0] = (((S - b1) - b2) - b3) * sc;
+    b[0] = b0 * sc;
     b[1] = b1 * sc;
     b[2] = b2 * sc;
     b[3] = b3 * sc;
@@ -365,7 +370,9 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
         }
         lu_factor(L.a, lu, dv);  // local Schur complement (solver.cpp:101-127)
     }
-    if (lu.singular) return 2;
+    // only the exact pass may call a block singular: FastDiv pivots outside
+    // the exact window are not trusted (-> redo)
+    if (lu.singular) return dv.good() ? 2 : 1;
     // local C rows c[r][v] = coef_r on the face's vertices, 0 on the
     // opposite one and on Neumann faces (local_c_rows, solver.cpp:33-40)
     auto cr = [&](int r, int v) -> double {
@@ -602,7 +609,7 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
     cudaMemcpyToSymbol(phg::c_lam5, lam5, sizeof(double) * 4 * 64);
     cudaMemcpyToSymbol(phg::c_w5, w5, sizeof(double) * 64);
     // collapsed-product structure of the degree-5 rule (4 x 4 x 4 points)
-    double l1[4], l2[16], l3[64];
+    double l0[64], l1[4], l2[16], l3[64];
     for (int a = 0; a < 4; ++a) {
         l1[a] = lam5[4 * (16 * a) + 1];
         for (int b = 0; b < 4; ++b) {
@@ -610,6 +617,7 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
             for (int c = 0; c < 4; ++c) {
                 const int q = 16 * a + 4 * b + c;
                 l3[q] = lam5[4 * q + 3];
+                l0[q] = lam5[4 * q];
                 if (lam5[4 * q + 1] != l1[a] || lam5[4 * q + 2] != l2[4 * a + b]) return (int)cudaErrorInvalidValue;
             }
         }
@@ -617,6 +625,7 @@ extern "C" int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5,
     cudaMemcpyToSymbol(phg::c_l1, l1, sizeof(l1));
     cudaMemcpyToSymbol(phg::c_l2, l2, sizeof(l2));
     cudaMemcpyToSymbol(phg::c_l3, l3, sizeof(l3));
+    cudaMemcpyToSymbol(phg::c_l0, l0, sizeof(l0));
     const int rc = (int)cudaGetLastError();
     return rc ? rc : phfem_gpu_set_rules_errors(lam9, w9);
 }

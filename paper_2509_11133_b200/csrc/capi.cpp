@@ -288,7 +288,8 @@ int phfem_mesh_refine(phfem_mesh* mesh, phfem_refine_times* times) {
     });
 }
 
-int phfem_mesh_level(const phfem_mesh* mesh) { return mesh ? mesh->data()->level : -1; }
+// the level is known when the handle is made: no upload wait, no throw
+int phfem_mesh_level(const phfem_mesh* mesh) { return mesh && mesh->data_ ? mesh->data_->level : -1; }
 
 int phfem_mesh_counts(const phfem_mesh* mesh, int64_t* n_elems, int64_t* n_nodes, int64_t* n_edges,
                       int64_t* n_faces, phfem_refine_times* times) {
@@ -793,6 +794,27 @@ int phfem_mesh_solve_faces(const phfem_mesh* mesh, int problem, double tol, int6
     });
 }
 
+int phfem_mesh_solve_unverified(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter, double* u,
+                                double* lambda, double out[13]) {
+    return guarded([&] {
+        if (!mesh || !out) throw InvalidArgument("null argument");
+        if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
+        auto* m = const_cast<phfem_mesh*>(mesh);
+        const System& sys = m->system(problem, false);
+        SolveResult r;
+        solve_schur(*m->data(), *m->coef, *m->conn, sys, problem, tol > 0.0 ? tol : 1e-10, max_iter, "schur", r, false,
+                    false);
+        double e[3];
+        error_norms(*m->data(), *m->coef, *m->conn, problem, r.u.p, r.lambda.p, e);
+        if (u) r.u.download_to(u, 4 * m->data()->ne);
+        if (lambda) r.lambda.download_to(lambda, sys.l);
+        phb::sync();
+        const double v[13] = {(double)r.iterations, r.residual, r.constraint_residual, r.converged ? 1.0 : 0.0,
+                              r.accepted ? 1.0 : 0.0, r.r1, r.r2, r.nrm_rhs, r.nrm_bd, r.rel_residual, e[0], e[1], e[2]};
+        for (int i = 0; i < 13; ++i) out[i] = v[i];
+    });
+}
+
 int phfem_solution_stats(const phfem_solution* sol, double out[4]) {
     return guarded([&] {
         if (!sol || !out) throw InvalidArgument("null argument");
@@ -873,7 +895,8 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
     });
 }
 
-int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter, double out[8]) {
+int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter, double out[8],
+                      double* out8) {
     return guarded([&] {
         if (!mesh || !out) throw InvalidArgument("null argument");
         auto* m = const_cast<phfem_mesh*>(mesh);
@@ -896,6 +919,10 @@ int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t m
         out[5] = accepted ? 1.0 : 0.0;
         out[6] = r.residual;
         out[7] = r.constraint_residual;
+        if (out8) {
+            const double v[4] = {r.r1, r.r2, r.nrm_rhs, r.nrm_bd};
+            for (int i = 0; i < 4; ++i) out8[i] = v[i];
+        }
     });
 }
 

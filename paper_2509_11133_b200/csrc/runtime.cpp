@@ -284,12 +284,18 @@ MeshData::~MeshData() {
 void finish_upload(MeshData& m) {
     if (!m.pending) return;
     PendingUpload& pu = *m.pending;
+    // an invalid mesh stays pending: every later use fails the same way,
+    // from the saved message (the caller's arrays need only live until the
+    // first use, phfem_ext.h)
+    if (!pu.error.empty()) throw InvalidArgument(pu.error);
     check(cudaEventSynchronize(pu.ready), "upload");
-    // an invalid mesh stays pending: every later use fails the same way
     for (int i = 0; i < 3; ++i)
-        if (pu.flags[i] != ~0ull)
-            throw InvalidArgument("node index " + std::to_string((long long)pu.src[i][pu.flags[i]] + 1) +
-                                  " out of range 1.." + std::to_string(m.nc));
+        if (pu.flags[i] != ~0ull) {
+            pu.error = "node index " + std::to_string((long long)pu.src[i][pu.flags[i]] + 1) + " out of range 1.." +
+                       std::to_string(m.nc);
+            pu.src[0] = pu.src[1] = pu.src[2] = nullptr;
+            throw InvalidArgument(pu.error);
+        }
     check(cudaStreamWaitEvent(S(), pu.ready, 0), "wait upload");
     m.pending.reset();
 }
@@ -349,7 +355,8 @@ void System::norms(double& sum_rhs2, double& sum_bd2) const {
 }
 
 void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const System& sys, int problem,
-                 double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only) {
+                 double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only,
+                 bool refuse_throws) {
     const auto t0 = std::chrono::steady_clock::now();
     const int64_t l = sys.l;
     double sum_rhs2, sum_bd2;
@@ -436,7 +443,12 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
     out.constraint_residual = s2[1] / (1.0 + s2[2]);
     const bool ok = out.residual <= tol && r1 <= tol * std::max(nrm_rhs, 1e-300) && r2 <= tol * (1.0 + nrm_bd);
     out.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    if (!ok) {
+    out.r1 = r1;
+    out.r2 = r2;
+    out.nrm_rhs = nrm_rhs;
+    out.nrm_bd = nrm_bd;
+    out.accepted = ok;
+    if (!ok && refuse_throws) {
         char buf[200];
         std::snprintf(buf, sizeof buf, "solver '%s' missed the residual target: %g > %g", method.c_str(),
                       out.residual, tol);

@@ -154,7 +154,8 @@ struct PendingUpload {
     cudaEvent_t ready = nullptr;
     unsigned long long* flags = nullptr;  // pinned [3]: first bad index per array
     DBuf<unsigned long long> dflags;
-    const int32_t* src[3] = {nullptr, nullptr, nullptr};  // caller's arrays (messages)
+    const int32_t* src[3] = {nullptr, nullptr, nullptr};  // caller's arrays, read once for the message
+    std::string error;  // set by the first failed check; later uses rethrow it
     ~PendingUpload();
 };
 
@@ -294,11 +295,15 @@ struct SolveResult {
     DBuf<double> u, lambda;
     int64_t iterations = 0;
     double residual = 0.0, constraint_residual = 0.0, seconds = 0.0, cg_ms = 0.0, rel_residual = 0.0;
-    bool converged = false;
+    // verify_solution's terms (solver.cpp:44-76): ||AU - C'L - B||, ||CU - b_D||, ||B||, ||b_D||
+    double r1 = 0.0, r2 = 0.0, nrm_rhs = 0.0, nrm_bd = 0.0;
+    bool converged = false, accepted = false;
 };
-// Jacobi-PCG on S, then (unless cg_only) recovery and verify_solution.
+// Jacobi-PCG on S, then (unless cg_only) recovery and verify_solution;
+// with refuse_throws = false a verify refusal only clears `accepted`.
 void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const System& sys, int problem,
-                 double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only = false);
+                 double tol, int64_t max_iter, const std::string& method, SolveResult& out, bool cg_only = false,
+                 bool refuse_throws = true);
 
 double mesh_diameter(const MeshData& m);
 // [y-norm, kappa-norm, L2]

@@ -112,8 +112,9 @@ def lib():
         "phfem_solution_stats": [P, P],
         "phfem_solution_errors_ex": [P, P],
         "phfem_pipeline": [P, C.c_int, C.c_int, P, P],
-        "phfem_solve_timed": [P, C.c_int, C.c_double, I64, P],
+        "phfem_solve_timed": [P, C.c_int, C.c_double, I64, P, P],
         "phfem_mesh_solve_faces": [P, C.c_int, C.c_double, I64, P, P],
+        "phfem_mesh_solve_unverified": [P, C.c_int, C.c_double, I64, P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -141,7 +142,7 @@ EXPORTED = [
     "phfem_mesh_set_coefficients", "phfem_mesh_connectivity", "phfem_mesh_get_edges", "phfem_mesh_get_faces",
     "phfem_mesh_refinement_map", "phfem_mesh_assemble", "phfem_mesh_get_system", "phfem_solve_ex",
     "phfem_solution_stats", "phfem_solution_errors_ex", "phfem_stream", "phfem_pipeline", "phfem_solve_timed",
-    "phfem_mesh_solve_faces",
+    "phfem_mesh_solve_faces", "phfem_mesh_solve_unverified",
 ]
 
 
@@ -369,9 +370,29 @@ class Mesh:
         """Schur solve with timings: CG on the device, then recovery + verify
         (a verify refusal is reported as accepted=False, not raised)."""
         out = np.zeros(8)
-        _check(lib().phfem_solve_timed(self._h, problem, tol, max_iter, _ptr(out)))
+        vt = np.zeros(4)
+        _check(lib().phfem_solve_timed(self._h, problem, tol, max_iter, _ptr(out), _ptr(vt)))
         return dict(iterations=int(out[0]), cg_ms=out[1], ms_per_iteration=out[2], converged=bool(out[3]),
-                    total_s=out[4], accepted=bool(out[5]), residual=out[6], constraint_residual=out[7])
+                    total_s=out[4], accepted=bool(out[5]), residual=out[6], constraint_residual=out[7],
+                    r1=vt[0], r2=vt[1], norm_rhs=vt[2], norm_bd=vt[3])
+
+    def solve_unverified(self, problem, tol=1e-10, max_iter=-1):
+        """The whole Schur path (face solve + recovery + verify terms + error
+        norms) without raising on verify_solution's refusal; returns U,
+        Lambda and the stats."""
+        n = 4 * self.sizes()[1]
+        l = self.connectivity()["l"]
+        u = np.zeros(n)
+        lam = np.zeros(l)
+        out = np.zeros(13)
+        _check(lib().phfem_mesh_solve_unverified(self._h, problem, tol, max_iter, _ptr(u), _ptr(lam), _ptr(out)))
+        keys = ("iterations", "residual", "constraint_residual", "converged", "accepted", "r1", "r2", "norm_rhs",
+                "norm_bd", "cg_rel_residual", "err_y", "err_kappa", "err_l2")
+        st = dict(zip(keys, (float(v) for v in out)))
+        st["iterations"] = int(st["iterations"])
+        st["converged"] = bool(st["converged"])
+        st["accepted"] = bool(st["accepted"])
+        return u, lam, st
 
 
 class Solution:

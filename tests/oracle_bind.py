@@ -101,6 +101,7 @@ class Oracle:
         L.or_face_table.argtypes = [I64, I64, P, P, I64, P, I64, P, P, P, P, P, P, P, P, P]
         L.or_refine.argtypes = [I64, I64, P, P, I64, P, I64, P, P, P, P, P, P, P]
         L.or_assemble_condense.argtypes = [I64, I64, P, P, I64, P, P, P, P, P, P, P, I64, P] + [P] * 13
+        L.or_entry_scales.argtypes = [I64, I64, P, P, I64, P, P, P, P, P, P, P, I64, P, P, P]
         L.or_pcg.argtypes = [I64, P, P, P, P, P, C.c_double, C.c_double, I64, P]
         L.or_solve_schur.argtypes = [I64, I64, P, P, P, I64] + [P] * 11 + [C.c_double, I64, P, P, P]
         L.or_errors.argtypes = [I64, I64, P, P, P, P, P, P, P, P, P]
@@ -229,6 +230,35 @@ class Oracle:
             _ptr(sys["c_col"]), _ptr(sys["c_val"]), _ptr(sys["s_rowptr"]), _ptr(sys["s_col"]),
             _ptr(sys["s_val"]), _ptr(sys["rhs_neg"]), tol, max_iter, _ptr(u), _ptr(lam), _ptr(st)))
         return u, lam, dict(iterations=int(st[0]), residual=st[1], constraint_residual=st[2])
+
+    def entry_scales(self, m: MeshArrays, ft: dict, kind=0, c=1.0, a_elem=None, a_diag=None):
+        """componentwise magnitudes of B_T and rhs_neg (or_entry_scales)"""
+        pr = self._prob(kind, c, a_elem, a_diag)
+        rs = np.zeros(4 * m.ne)
+        ns = np.zeros(ft["l"])
+        self._check(self.L.or_entry_scales(
+            m.nc, m.ne, _ptr(m.coords), _ptr(m.tets), ft["nf"], _ptr(ft["faces"]), _ptr(ft["face_of_slot"]),
+            _ptr(ft["sigma"]), _ptr(ft["face_slots"]), _ptr(ft["face_class"]), _ptr(ft["mrow"]),
+            _ptr(ft["area"]), ft["l"], C.byref(pr), _ptr(rs), _ptr(ns)))
+        return rs, ns
+
+    def solve_raw(self, m: MeshArrays, sys: dict, kind=0, c=1.0, a_elem=None, a_diag=None, tol=1e-10,
+                  max_iter=-1):
+        """or_solve_schur without raising: U, Lambda and the stats are filled
+        before verify_solution decides (solver.cpp:44-76), so a refused solve
+        still yields its iterates.  Returns (u, lambda, stats, rc, message)."""
+        pr = self._prob(kind, c, a_elem, a_diag)
+        l = len(sys["bd"])
+        u = np.zeros(4 * m.ne)
+        lam = np.zeros(l)
+        st = np.zeros(3)
+        rc = self.L.or_solve_schur(
+            m.nc, m.ne, _ptr(m.coords), _ptr(m.tets), C.byref(pr), l, _ptr(sys["slot_coef"]),
+            _ptr(sys["slot_mrow"]), _ptr(sys["rhs"]), _ptr(sys["bd"]), _ptr(sys["c_rowptr"]),
+            _ptr(sys["c_col"]), _ptr(sys["c_val"]), _ptr(sys["s_rowptr"]), _ptr(sys["s_col"]),
+            _ptr(sys["s_val"]), _ptr(sys["rhs_neg"]), tol, max_iter, _ptr(u), _ptr(lam), _ptr(st))
+        msg = self.L.or_last_error().decode() if rc else ""
+        return u, lam, dict(iterations=int(st[0]), residual=st[1], constraint_residual=st[2]), rc, msg
 
     def pcg(self, sys: dict, tol=1e-10, abs_tol=0.0, max_iter=-1):
         l = len(sys["rhs_neg"])

@@ -31,9 +31,21 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
-def rel_max(a, b):
-    s = np.abs(b).max() if b.size else 0.0
-    return np.abs(a - b).max() / (s if s > 0 else 1.0) if a.size else 0.0
+def componentwise(a, b, scale):
+    """max_i |a_i - b_i| / max(scale_i, |b_i|): per-entry error relative to
+    the magnitude the entry's summands carry (oracle.entry_scales)"""
+    if not a.size:
+        return 0.0
+    den = np.maximum(np.maximum(scale, np.abs(b)), 1e-300)
+    return float((np.abs(a - b) / den).max())
+
+
+def per_entry(a, b):
+    """max_i |a_i - b_i| / max(|b_i|, 1e-12 ||b||_inf)"""
+    if not a.size:
+        return 0.0
+    fl = max(1e-12 * float(np.abs(b).max()), 1e-300)
+    return float((np.abs(a - b) / np.maximum(np.abs(b), fl)).max())
 
 
 def to_gpu(m: MeshArrays) -> "ph.Mesh":
@@ -60,17 +72,24 @@ def check_connectivity(g, m, oracle):
 
 
 def check_system(g, m, fo, oracle, kind, c=1.0, a_elem=None, a_diag=None):
+    """A_T, C_T, S bit-exact.  Polynomial data: B_T, rhs_neg, b_D bit-exact.
+    Transcendental data (glibc libm in the oracle vs libdevice / series on
+    the GPU): b_D <= 1e-12 per entry; B_T and rhs_neg <= 1e-12 per entry
+    relative to the magnitude of the entry's summands (or_entry_scales:
+    sum_q |V w f| lambda_v, and its propagation through C A^-1), which is
+    the accuracy the reference itself has on a cancelling entry."""
     so = oracle.assemble(m, fo, kind, c, a_elem, a_diag)
     sg = g.assemble(kind)
-    for k in ("a_blocks", "slot_coef", "slot_mrow", "s_rowptr", "s_col", "s_val", "bd"):
-        if kind in TRANSCENDENTAL and k == "bd":
-            assert rel_max(sg[k], so[k]) <= 1e-12, k
-        else:
-            assert np.array_equal(sg[k], so[k]), k
-    for k in ("rhs", "rhs_neg"):
-        if kind in TRANSCENDENTAL:
-            assert rel_max(sg[k], so[k]) <= 1e-12, (k, rel_max(sg[k], so[k]))
-        else:
+    for k in ("a_blocks", "slot_coef", "slot_mrow", "s_rowptr", "s_col", "s_val"):
+        assert np.array_equal(sg[k], so[k]), k
+    if kind in TRANSCENDENTAL:
+        assert per_entry(sg["bd"], so["bd"]) <= 1e-12, per_entry(sg["bd"], so["bd"])
+        rs, ns = oracle.entry_scales(m, fo, kind, c, a_elem, a_diag)
+        for k, sc in (("rhs", rs), ("rhs_neg", ns)):
+            err = componentwise(sg[k], so[k], sc)
+            assert err <= 1e-12, (k, err)
+    else:
+        for k in ("bd", "rhs", "rhs_neg"):
             assert np.array_equal(sg[k], so[k]), k
     return so
 
@@ -228,28 +247,29 @@ def test_config_parity(oracle, cid, factor):
     assert rel_l2(lg_cg, lo_cg) <= 1e-9, rel_l2(lg_cg, lo_cg)
     assert abs(st_g["iterations"] - res[0]) <= max(3, 0.02 * res[0])
     assert n_ == len(so["rhs"])
-    # the full solve; the reference may refuse a converged solve through
-    # verify_solution (SURVEY finding 8): then the GPU path must refuse too,
-    # and a tighter tolerance is tried
-    for tol in (cfg.tol, 1e-11, 1e-12):
-        try:
-            uo, lo, st_o = oracle.solve(m, so, cfg.problem, cfg.c, k["a_elem"], k["a_diag"], tol=tol)
-            break
-        except Exception as e:  # noqa: BLE001
-            with pytest.raises(ph.SolverError, match="missed the residual target"):
-                g.solve_ex(cfg.problem, tol=tol)
-            last = e
-    else:
-        pytest.skip(f"the reference refuses at every tolerance (finding 8): {last}; face solves matched")
-    sol = g.solve_ex(cfg.problem, tol=tol)
-    ug, lg = sol.values()
+    # the full solve (recovery + verify_solution + error norms).  The
+    # reference may refuse a converged solve through verify_solution (SURVEY
+    # finding 8); U and Lambda are compared either way, and the GPU path
+    # must reach the same verdict (and raise the same error through
+    # phfem_solve_ex when the reference refuses)
+    uo, lo, st_o, rc_o, msg_o = oracle.solve_raw(m, so, cfg.problem, cfg.c, k["a_elem"], k["a_diag"], tol=cfg.tol)
+    ug, lg, st_g = g.solve_unverified(cfg.problem, tol=cfg.tol)
     assert rel_l2(ug, uo) <= 1e-9, rel_l2(ug, uo)
     assert rel_l2(lg, lo) <= 1e-9, rel_l2(lg, lo)
     eo = oracle.errors(m, fo, uo, lo, cfg.problem, cfg.c, k["a_elem"], k["a_diag"])
-    eg = np.array(sol.errors_ex())
+    eg = np.array([st_g["err_y"], st_g["err_kappa"], st_g["err_l2"]])
     assert np.all(np.abs(eg - eo) <= 5e-4 * np.abs(eo)), (eg, eo)  # 3 significant digits
-    st = sol.stats()
-    assert abs(st["iterations"] - st_o["iterations"]) <= max(3, 0.02 * st_o["iterations"])
+    assert abs(st_g["iterations"] - st_o["iterations"]) <= max(3, 0.02 * st_o["iterations"])
+    assert rc_o in (0, 3), msg_o
+    assert st_g["accepted"] == (rc_o == 0), (st_g, st_o, msg_o)
+    if rc_o:
+        assert "missed the residual target" in msg_o
+        with pytest.raises(ph.SolverError, match="missed the residual target"):
+            g.solve_ex(cfg.problem, tol=cfg.tol)
+    else:
+        sol = g.solve_ex(cfg.problem, tol=cfg.tol)
+        u2, l2 = sol.values()
+        assert rel_l2(u2, uo) <= 1e-9 and rel_l2(l2, lo) <= 1e-9
 
 
 def test_solve_through_reference_c_abi(oracle, goldens):
