@@ -265,6 +265,159 @@ int phfem_gpu_division_selftest(int64_t n, uint64_t seed, unsigned long long* mi
  * launch; time it between ev_begin / ev_end (cudaEvent_t, may be NULL) */
 int phfem_gpu_fp64_peak(int iters, double* sink, void* ev_begin, void* ev_end, double* flops, void* stream);
 
+/* ------------------------------------------------- C++ API support (api.cu)
+ * Kernels behind the value-returning C++ API (include/phfem_cxx), whose
+ * inputs are host structs (LinearSystem, CsrMatrix, Triplets, FaceTable).
+ * Every sequential sum the reference defines is owned by one thread and
+ * replayed in the reference's order. */
+
+/* group n items by seg[i] in [0, nseg) and sort each group by
+ * (minor[i], i): seg_ptr [nseg+1] (exclusive offsets), perm [n] (item ids in
+ * sorted order).  Scratch: cnt [nseg], tmp [n], scan_scratch
+ * (phfem_gpu_scan_scratch(nseg)). */
+int phfem_gpu_seg_sort(int64_t n, int64_t nseg, const int64_t* seg, const int64_t* minor,
+                       int64_t* seg_ptr, int64_t* perm, int32_t* cnt, int64_t* tmp, void* scan_scratch,
+                       void* stream);
+/* items already grouped by seg_ptr: perm = identity, then sorted per group */
+int phfem_gpu_sort_within(int64_t n, int64_t nseg, const int64_t* seg_ptr, const int64_t* minor,
+                          int64_t* perm, int64_t* tmp, void* stream);
+
+/* edge_pairs_to_elems (connectivity.cpp:46-70): entry 12 m + 3 k + j of
+ * element m (from, to) edge pairs; after seg_sort by `from` with minor `to`,
+ * e2t_finish writes the sorted keys (from * ned + to) / elements and
+ * atomicMin's the first position j whose key equals key j-1. */
+int phfem_gpu_e2t_entries(int64_t ne, const int32_t* edge_of_slot, int64_t* from, int64_t* to,
+                          void* stream);
+int phfem_gpu_e2t_finish(int64_t n, int64_t ned, const int64_t* perm, const int64_t* from,
+                         const int64_t* to, unsigned long long* key, int32_t* elem,
+                         unsigned long long* first_dup, void* stream);
+
+int phfem_gpu_widen(int64_t n, const int32_t* a, int64_t* b, void* stream);
+/* from_triplets (sparse.cpp:12-44) after seg_sort by row with minor col:
+ * distinct columns per row, then the CSR with duplicates summed in
+ * insertion order */
+int phfem_gpu_csr_unique(int64_t rows, const int64_t* ptr, const int64_t* perm, const int64_t* col,
+                         int32_t* cnt, void* stream);
+int phfem_gpu_csr_write(int64_t rows, const int64_t* ptr, const int64_t* perm, const int64_t* col,
+                        const double* val, const int64_t* out_ptr, int32_t* out_col, double* out_val,
+                        void* stream);
+/* y = A x (sparse.cpp:46-52), diagonal (60-66) */
+int phfem_gpu_csr_spmv(int64_t rows, const int64_t* ptr, const int32_t* col, const double* val,
+                       const double* x, double* y, void* stream);
+int phfem_gpu_csr_diag(int64_t rows, const int64_t* ptr, const int32_t* col, const double* val,
+                       double* d, void* stream);
+/* transpose (sparse.cpp:68-87): rowof [nnz] = row of each entry; after
+ * seg_sort by column with minor = entry index, tcol/tval from perm */
+int phfem_gpu_csr_rowof(int64_t rows, const int64_t* ptr, int64_t* rowof, void* stream);
+int phfem_gpu_csr_transpose(int64_t nnz, const int64_t* perm, const int64_t* rowof, const double* val,
+                            int32_t* tcol, double* tval, void* stream);
+/* spgemm (sparse.cpp:122-149): products per row of A (count, fill in the
+ * accumulation order), sort_within by column, then per column
+ * acc = 0.0; acc += product in that order */
+int phfem_gpu_spgemm_count(int64_t rows, const int64_t* aptr, const int32_t* acol, const int64_t* bptr,
+                           int32_t* cnt, void* stream);
+int phfem_gpu_spgemm_fill(int64_t rows, const int64_t* aptr, const int32_t* acol, const double* aval,
+                          const int64_t* bptr, const int32_t* bcol, const double* bval,
+                          const int64_t* pptr, int64_t* pcol, double* pval, void* stream);
+int phfem_gpu_spgemm_write(int64_t rows, const int64_t* pptr, const int64_t* perm, const int64_t* pcol,
+                           const double* pval, const int64_t* out_ptr, int32_t* out_col,
+                           double* out_val, void* stream);
+
+/* build_schur's element part (solver.cpp:101-127) from given blocks:
+ * lu [16 nE], perm [4 nE], singular [nE], s_loc [16 nE], r_loc [4 nE];
+ * *first_singular = min singular element (init ULLONG_MAX) */
+int phfem_gpu_condense_blocks(int64_t ne, const double* a_blocks, const double* coef, const int32_t* mrow,
+                              const double* rhs, double* lu, int32_t* perm, uint8_t* singular,
+                              double* s_loc, double* r_loc, unsigned long long* first_singular,
+                              void* stream);
+/* per element: S triplets nr^2, rhs_neg terms nr (nr = non-Neumann rows) */
+int phfem_gpu_schur_counts(int64_t ne, const int32_t* mrow, int32_t* cs, int32_t* cr, void* stream);
+/* the reference's triplet stream (solver.cpp:131-145) at offsets os / orr */
+int phfem_gpu_schur_triplets(int64_t ne, const int32_t* mrow, const double* s_loc, const double* r_loc,
+                             const int64_t* os, const int64_t* orr, int64_t* trow, int64_t* tcol,
+                             double* tval, int64_t* rrow, double* rval, void* stream);
+/* rhs_neg[r] = ((b_D[r] - t0) - t1) over row r's terms in stream order */
+int phfem_gpu_rhs_neg(int64_t l, const int64_t* ptr, const int64_t* perm, const double* rval,
+                      const double* bd, double* out, void* stream);
+/* recovery (solver.cpp:168-181) + r1 = A U - B per element (44-50) */
+int phfem_gpu_recover_blocks(int64_t ne, const double* a_blocks, const double* coef, const int32_t* mrow,
+                             const double* rhs, const double* lambda, double* u, double* r1, void* stream);
+int phfem_gpu_sub_inplace(int64_t n, double* a, const double* b, void* stream);
+/* out (device) [sum x^2, max |x|], deterministic; partials
+ * [2 phfem_gpu_sumsq_max_partials()] */
+int phfem_gpu_sumsq_max_partials(void);
+int phfem_gpu_sumsq_max(int64_t n, const double* x, double* partials, double* out, void* stream);
+
+/* tabulated problem data (assembly.cpp:46-104): rule 0 = Gauss (nq points
+ * lam [4 nq], w [nq]), 1 = face centroids (4 per element).  load_points:
+ * vol [nE], pts [3 nq nE]; load_tab: b [4 nE] from f values fv [nq nE]. */
+int phfem_gpu_load_points(int64_t ne, const double* coords, const int32_t* tets, int rule, int nq,
+                          const double* lam, double* vol, double* pts, void* stream);
+int phfem_gpu_load_tab(int64_t ne, int rule, int nq, const double* lam, const double* w,
+                       const double* vol, const double* fv, double* b, void* stream);
+/* face_area_and_normal + face_centroid (mesh.cpp:76-88) of faces ids[i]
+ * (ids NULL: 0..n-1): out [7 n] = area, unit normal, centroid; *bad = first
+ * degenerate position (init ULLONG_MAX) */
+int phfem_gpu_face_geom(int64_t n, const int32_t* ids, const int32_t* faces, const double* coords,
+                        double* out, unsigned long long* bad, void* stream);
+/* neumann_vector (assembly.cpp:81-94) from g values gv [per geometry row];
+ * geo_of_face maps a face to its face_geom row */
+int phfem_gpu_neumann_tab(int64_t ne, const int32_t* slot_to_face, const uint8_t* face_class,
+                          const int64_t* face_slots, const int32_t* geo_of_face, const double* geo,
+                          const double* gv, double* ln, void* stream);
+/* y_norm_error (analysis.cpp:51-76): points [3 nq nE]; per-element sums
+ * from ex [4 nq nE] = (u, grad u) at the points */
+int phfem_gpu_ynorm_points(int64_t ne, const double* coords, const int32_t* tets, int nq,
+                           const double* lam, double* pts, void* stream);
+int phfem_gpu_ynorm_elem(int64_t ne, const double* coords, const int32_t* tets, const double* u, int nq,
+                         const double* lam, const double* w, const double* ex, double inv_h2,
+                         double* acc, void* stream);
+/* multiplier_norm_error (analysis.cpp:78-105): points [36 nE] (3 edge
+ * midpoints of each oriented face); per-element sums from grad u [36 nE] */
+int phfem_gpu_kappa_points(int64_t ne, const double* coords, const int32_t* tets, double* pts,
+                           void* stream);
+int phfem_gpu_kappa_elem(int64_t ne, const double* coords, const int32_t* tets,
+                         const int32_t* slot_to_face, const double* sigma, const uint8_t* face_class,
+                         const int32_t* mult, const double* lambda, const double* gr, double h,
+                         double* acc, void* stream);
+/* assemble_system's element part (assembly.cpp:115-130) from a given face
+ * table: a [16 nE] = K + M, coef [4 nE] = (sigma |F|) / 3, mrow [4 nE];
+ * *bad = first zero-volume element (init ULLONG_MAX) */
+int phfem_gpu_element_blocks(int64_t ne, const double* coords, const int32_t* tets,
+                             const int32_t* slot_to_face, const double* sigma, const double* area,
+                             const int32_t* mult, double* a, double* coef, int32_t* mrow,
+                             unsigned long long* bad, void* stream);
+/* C triplets in the reference's order at offsets 3 orr[t] (orr = exclusive
+ * scan of the non-Neumann slot counts) */
+int phfem_gpu_c_triplets(int64_t ne, const int32_t* mrow, const double* coef, const int64_t* orr,
+                         int64_t* trow, int64_t* tcol, double* tval, void* stream);
+/* solve_direct (solver.cpp:192-244): block inverses inv [16 nE] with the
+ * block pattern (4t+i, 4t+j); block solves; r1 = A U - B */
+int phfem_gpu_block_inverses(int64_t ne, const double* a, double* inv, unsigned long long* first_singular,
+                             void* stream);
+int phfem_gpu_block_pattern(int64_t ne, int64_t* row, int64_t* col, void* stream);
+int phfem_gpu_block_solve(int64_t ne, const double* a, const double* b, double* u, void* stream);
+int phfem_gpu_block_residual(int64_t ne, const double* a, const double* u, const double* rhs, double* r1,
+                             void* stream);
+/* a += b; a = b - a; out (device) = sum x (deterministic, partials as
+ * phfem_gpu_sumsq_max) */
+int phfem_gpu_add_inplace(int64_t n, double* a, const double* b, void* stream);
+int phfem_gpu_rsub_inplace(int64_t n, double* a, const double* b, void* stream);
+int phfem_gpu_sum(int64_t n, const double* x, double* partials, double* out, void* stream);
+/* refine_boundary_faces' split (refine.cpp:88-94): in [3 nf], the
+ * midpoint ids mid [3 nf] = (m12, m23, m13) per face, out [12 nf] */
+int phfem_gpu_split_boundary(int64_t nf, const int32_t* in, const int32_t* mid, int32_t* out, void* stream);
+/* RefinementMap::parent_elem [12 nE] (refine.cpp:58-68) */
+int phfem_gpu_refine_parents(int64_t ne, int32_t* parent, void* stream);
+/* Jacobi-PCG on a general CSR matrix (the C++ API's pcg_jacobi) */
+int phfem_gpu_cgcsr_init(int64_t l, const int64_t* ptr, const int32_t* col, const double* val,
+                         const double* b, double* x, double* r, double* p, double* d, double tol,
+                         double abs_tol, long long max_iter, phg_cg_state* st, double* partials,
+                         void* stream);
+int phfem_gpu_cgcsr_iterations(int n, int64_t l, const int64_t* ptr, const int32_t* col,
+                               const double* val, double* x, double* r, double* p, double* q,
+                               const double* d, phg_cg_state* st, double* partials, void* stream);
+
 /* kernels launched by this library since load (benchmark accounting) */
 long long phfem_gpu_launch_count(void);
 

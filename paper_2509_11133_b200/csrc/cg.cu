@@ -83,13 +83,32 @@ __device__ __forceinline__ bool finish(const double (&v)[NV], double* partials, 
     return true;
 }
 
+// the diagonal of S: SELL position 0, or the CSR row's entries on the
+// diagonal summed in storage order (CsrMatrix::diagonal, sparse.cpp:60-66)
+struct SellDiag {
+    const double* sell_val;
+    __device__ __forceinline__ double operator()(int64_t i) const { return sell_val[sell_idx(i, 0)]; }
+};
+struct CsrDiag {
+    const int64_t* ptr;
+    const int32_t* col;
+    const double* val;
+    __device__ __forceinline__ double operator()(int64_t i) const {
+        double s = 0.0;
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k)
+            if (col[k] == i) s = __dadd_rn(s, val[k]);
+        return s;
+    }
+};
+
+template <class Diag>
 __global__ void __launch_bounds__(kThreads)
-    cg_init(int64_t l, const double* __restrict__ sell_val, const double* __restrict__ b, double* __restrict__ x,
+    cg_init(int64_t l, Diag diag_of, const double* __restrict__ b, double* __restrict__ x,
             double* __restrict__ r, double* __restrict__ p, double* __restrict__ d, double tol, double abs_tol,
             long long max_iter, phg_cg_state* st, double* partials) {
     double acc[2] = {0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
-        const double diag = sell_val[sell_idx(i, 0)];
+        const double diag = diag_of(i);
         const double di = diag != 0.0 ? 1.0 / diag : 1.0;
         const double bi = b[i];
         d[i] = di;
@@ -152,6 +171,36 @@ __global__ void __launch_bounds__(kThreads)
     if (threadIdx.x == 0) {
         st->pq = tot[0];
         if (tot[0] <= 0.0) {  // sparse.cpp:185
+            st->not_spd = 1;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / tot[0];
+        }
+    }
+}
+
+// q = A p for a general CSR matrix (the C++ API's pcg_jacobi on a host
+// CsrMatrix): one row per thread, entries in storage order
+__global__ void __launch_bounds__(kThreads)
+    cg_spmv_csr(int64_t l, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                const double* __restrict__ val, const double* __restrict__ p, double* __restrict__ q,
+                phg_cg_state* st, double* partials) {
+    if (st->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->x_pending = 0;
+        return;
+    }
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) s += val[k] * __ldg(p + col[k]);
+        q[i] = s;
+        acc[0] += p[i] * s;
+    }
+    double tot[1];
+    if (!finish<1>(acc, partials, &st->counter[1], tot)) return;
+    if (threadIdx.x == 0) {
+        st->pq = tot[0];
+        if (tot[0] <= 0.0) {
             st->not_spd = 1;
             st->done = 1;
         } else {
@@ -243,7 +292,34 @@ extern "C" int phfem_gpu_cg_init(int64_t l, const int32_t* sell_col, const doubl
     (void)sell_col;
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(st, 0, sizeof(phg_cg_state), s);
-    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, sell_val, b, x, r, p, d, tol, abs_tol, max_iter, st, partials); phg::count_launches(1);
+    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, SellDiag{sell_val}, b, x, r, p, d, tol, abs_tol, max_iter, st, partials);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_cgcsr_init(int64_t l, const int64_t* ptr, const int32_t* col, const double* val,
+                                    const double* b, double* x, double* r, double* p, double* d, double tol,
+                                    double abs_tol, long long max_iter, phg_cg_state* st, double* partials,
+                                    void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(st, 0, sizeof(phg_cg_state), s);
+    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, CsrDiag{ptr, col, val}, b, x, r, p, d, tol, abs_tol, max_iter, st,
+                                            partials);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_cgcsr_iterations(int n, int64_t l, const int64_t* ptr, const int32_t* col, const double* val,
+                                          double* x, double* r, double* p, double* q, const double* d,
+                                          phg_cg_state* st, double* partials, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = cg_grid(l);
+    for (int i = 0; i < n; ++i) {
+        cg_spmv_csr<<<g, kThreads, 0, s>>>(l, ptr, col, val, p, q, st, partials);
+        cg_update<<<g, kThreads, 0, s>>>(l, r, q, d, st, partials);
+        cg_pdir<<<g, kThreads, 0, s>>>(l, x, r, p, d, st);
+    }
+    phg::count_launches(3 * n);
     return (int)cudaGetLastError();
 }
 

@@ -43,16 +43,22 @@ void fetch_tri(const int32_t* dev, int64_t i, int32_t out[3]) {
     sync();
 }
 
-// connectivity.cpp:62-68, 156-194 and mesh.cpp:80-82, in that order
-void replay_connectivity_errors(const std::vector<unsigned long long>& e, const MeshData& m, const Connectivity& c) {
+// connectivity.cpp:62-68, 156-194 and mesh.cpp:80-82, in that order; `upto`
+// stops after the checks the stage that ran owns (1: edges, which the
+// reference's num_edges never fails; 2: + the E2T duplicate-orientation
+// check; 3: everything)
+void replay_connectivity_errors(const std::vector<unsigned long long>& e, const MeshData& m, const Connectivity& c,
+                                int upto = 3) {
     if (e[PHG_ERR_VALENCE] != kNone)
         throw MeshError("vertex " + std::to_string(e[PHG_ERR_VALENCE] + 1) +
                         " is shared by more elements than the connectivity kernels support");
+    if (upto < 2) return;
     if (e[PHG_ERR_DUP_ORIENT] != kNone) {
         const unsigned long long k = e[PHG_ERR_DUP_ORIENT];
         throw MeshError("inconsistent mesh: elements " + std::to_string((k >> 32) + 1) + " and " +
                         std::to_string((k & 0xffffffffull) + 1) + " claim the same oriented face");
     }
+    if (upto < 3) return;
     if (e[PHG_ERR_CLASSIFY] != kNone) {
         const int64_t i = (int64_t)(e[PHG_ERR_CLASSIFY] >> 2);
         const int kind = (int)(e[PHG_ERR_CLASSIFY] & 3);
@@ -79,7 +85,7 @@ void replay_connectivity_errors(const std::vector<unsigned long long>& e, const 
 
 // ------------------------------------------------------------ connectivity
 
-void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st) {
+void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st, bool classify) {
     const int64_t nc = m.nc, ne = m.ne;
     Work& w = c.w;
     cudaEvent_t t0 = nullptr;
@@ -142,8 +148,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     c.has_edges = true;
     c.has_faces = false;
     c.t_edges = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
-    if (!faces) {
-        replay_connectivity_errors(w.err.download(), m, c);
+    if (!faces || !classify) {
+        replay_connectivity_errors(w.err.download(), m, c, faces ? 2 : 1);
         return;
     }
     // 4. boundary classification and multiplier rows

@@ -146,7 +146,7 @@ double Timer::stop_ms() {
 // gauss_legendre / tet_rule, quadrature.cpp:9-62 (the host builds the
 // tables exactly like the reference; the device receives them verbatim).
 
-static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
     x.assign(n, 0.0);
     w.assign(n, 0.0);
     for (int i = 0; i < n; ++i) {

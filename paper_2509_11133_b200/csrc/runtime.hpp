@@ -14,24 +14,18 @@
 #include <tuple>
 #include <vector>
 
+#include "phfem_cxx/errors.hpp"
 #include "phfem_gpu.h"
 
 namespace phb {
 
-// Error taxonomy of the reference (errors.hpp:9-27), mapped 1:1 onto the C
-// status codes by the C ABI wrapper.
-struct InvalidArgument : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct MeshError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct SolverError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-struct IoError : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
+// Error taxonomy of the reference (errors.hpp:9-27): the C++ API's own
+// classes, so errors raised here reach C++ callers with the reference's type;
+// the C ABI wrapper maps them 1:1 onto the status codes.
+using phfem::InvalidArgument;
+using phfem::IoError;
+using phfem::MeshError;
+using phfem::SolverError;
 
 void check(cudaError_t e, const char* what);
 inline void check(int e, const char* what) { check(static_cast<cudaError_t>(e), what); }
@@ -282,7 +276,9 @@ std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly
                                     uint64_t seed, uint32_t mask);
 
 // star + edges (+ faces, classification and multiplier rows)
-void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st = nullptr);
+// (classify = false: the face numbering alone, as faces_up gives it, without
+// the boundary classification and multiplier rows)
+void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st = nullptr, bool classify = true);
 // red refinement; needs edges.  `into` (optional) is reused for the child.
 std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st = nullptr,
                                       std::shared_ptr<MeshData> into = nullptr);
@@ -312,6 +308,7 @@ void error_norms(const MeshData& m, const Coefs& k, const Connectivity& c, int p
 
 // host helpers
 std::string format_double(double v);
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w);
 void tet_rule(int degree, std::vector<double>& lam, std::vector<double>& w);
 
 }  // namespace phb

@@ -1,12 +1,15 @@
 // Minimal doctest-compatible shim (the real doctest is not vendored in the
-// reference tree).  Enough for the reference's C-ABI suite
-// (/root/reference/proj/tests/test_capi.cpp): TEST_CASE, SUBCASE (run
-// inline), CHECK/REQUIRE and friends, doctest::Approx, and a main().
+// reference tree).  Enough for the reference's suites
+// (/root/reference/proj/tests/test_*.cpp): TEST_CASE, SUBCASE (run inline,
+// in order), CHECK/REQUIRE and friends, CHECK_THROWS_AS / CHECK_NOTHROW /
+// REQUIRE_NOTHROW, doctest::Approx, and a main().
 #pragma once
 
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <limits>
 #include <functional>
 #include <sstream>
 #include <string>
@@ -74,6 +77,36 @@ inline void fail(const char* file, int line, const char* expr, bool fatal) {
 #define CHECK_FALSE(...) DT_CHECK_IMPL(!(__VA_ARGS__), false)
 #define CHECK_MESSAGE(cond, ...) DT_CHECK_IMPL((cond), false)
 #define FAIL(...) doctest::detail::fail(__FILE__, __LINE__, "FAIL", true)
+#define DT_THROWS_IMPL(expr, T, fatal)                                                        \
+    do {                                                                                      \
+        ++doctest::detail::checks();                                                          \
+        bool dt_ok = false;                                                                   \
+        try {                                                                                 \
+            (void)(expr);                                                                     \
+        } catch (const T&) {                                                                  \
+            dt_ok = true;                                                                     \
+        } catch (...) {                                                                       \
+        }                                                                                     \
+        if (!dt_ok) doctest::detail::fail(__FILE__, __LINE__, #expr " throws " #T, fatal);    \
+    } while (0)
+#define CHECK_THROWS_AS(expr, ...) DT_THROWS_IMPL(expr, __VA_ARGS__, false)
+#define REQUIRE_THROWS_AS(expr, ...) DT_THROWS_IMPL(expr, __VA_ARGS__, true)
+#define DT_NOTHROW_IMPL(expr, fatal)                                                          \
+    do {                                                                                      \
+        ++doctest::detail::checks();                                                          \
+        bool dt_ok = true;                                                                    \
+        try {                                                                                 \
+            (void)(expr);                                                                     \
+        } catch (const std::exception& e) {                                                   \
+            dt_ok = false;                                                                    \
+            std::fprintf(stderr, "  threw: %s\n", e.what());                                  \
+        } catch (...) {                                                                       \
+            dt_ok = false;                                                                    \
+        }                                                                                     \
+        if (!dt_ok) doctest::detail::fail(__FILE__, __LINE__, #expr " does not throw", fatal); \
+    } while (0)
+#define CHECK_NOTHROW(expr) DT_NOTHROW_IMPL(expr, false)
+#define REQUIRE_NOTHROW(expr) DT_NOTHROW_IMPL(expr, true)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main() {
