@@ -1276,6 +1276,216 @@ int or_solve_schur(int64_t nc, int64_t ne, const double* coords, const int32_t* 
 }
 
 /* ------------------------------------------------------------------------ */
+/* Streaming connectivity digests (TEST INFRASTRUCTURE).  Config 2's level 7
+ * (215M tets) does not fit the full oracle tables in host memory (the E2T
+ * alone is 41 GB, SURVEY.md 8(c) "Limits"), so its connectivity is checked
+ * through SHA-256 digests of the arrays the reference defines, computed here
+ * in one element-order pass with the same first-occurrence rules:
+ *   edges: num_edges (connectivity.cpp:22-37), ids in first-occurrence order;
+ *   faces: a face is first seen at its owner slot (the lower element, the
+ *          slot faces_up emits, connectivity.cpp:72-86), whose oriented
+ *          tuple is stored; face ids in that order; the second slot gets
+ *          sigma from same_cycle (connectivity.cpp:104-108, 145);
+ *          face_area from face_area_and_normal (mesh.cpp:76-84);
+ *          class 1 (Dirichlet) for faces with one slot (config 2 lists every
+ *          boundary face as Dirichlet), multiplier row = face id.
+ * SHA-256 is FIPS 180-4, restated here. */
+
+typedef struct {
+    uint32_t h[8];
+    uint64_t len;
+    uint8_t buf[64];
+    int nbuf;
+} sha256;
+
+static const uint32_t kSha[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+    0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+    0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+    0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+    0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+    0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+    0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+
+static uint32_t rotr(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+
+static void sha_init(sha256* s) {
+    static const uint32_t h0[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                                   0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    memcpy(s->h, h0, sizeof h0);
+    s->len = 0;
+    s->nbuf = 0;
+}
+
+static void sha_block(sha256* s, const uint8_t* p) {
+    uint32_t w[64];
+    for (int i = 0; i < 16; ++i)
+        w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 | p[4 * i + 3];
+    for (int i = 16; i < 64; ++i) {
+        const uint32_t s0 = rotr(w[i - 15], 7) ^ rotr(w[i - 15], 18) ^ (w[i - 15] >> 3);
+        const uint32_t s1 = rotr(w[i - 2], 17) ^ rotr(w[i - 2], 19) ^ (w[i - 2] >> 10);
+        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    uint32_t a = s->h[0], b = s->h[1], c = s->h[2], d = s->h[3], e = s->h[4], f = s->h[5], g = s->h[6],
+             h = s->h[7];
+    for (int i = 0; i < 64; ++i) {
+        const uint32_t t1 = h + (rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25)) + ((e & f) ^ (~e & g)) + kSha[i] + w[i];
+        const uint32_t t2 = (rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+        h = g;
+        g = f;
+        f = e;
+        e = d + t1;
+        d = c;
+        c = b;
+        b = a;
+        a = t1 + t2;
+    }
+    s->h[0] += a; s->h[1] += b; s->h[2] += c; s->h[3] += d;
+    s->h[4] += e; s->h[5] += f; s->h[6] += g; s->h[7] += h;
+}
+
+static void sha_update(sha256* s, const void* data, size_t n) {
+    const uint8_t* p = (const uint8_t*)data;
+    s->len += n;
+    while (n) {
+        if (s->nbuf == 0 && n >= 64) {
+            sha_block(s, p);
+            p += 64;
+            n -= 64;
+            continue;
+        }
+        const size_t k = (size_t)(64 - s->nbuf) < n ? (size_t)(64 - s->nbuf) : n;
+        memcpy(s->buf + s->nbuf, p, k);
+        s->nbuf += (int)k;
+        p += k;
+        n -= k;
+        if (s->nbuf == 64) {
+            sha_block(s, s->buf);
+            s->nbuf = 0;
+        }
+    }
+}
+
+static void sha_final(sha256* s, uint8_t out[32]) {
+    const uint64_t bits = s->len * 8;
+    const uint8_t one = 0x80, zero = 0;
+    sha_update(s, &one, 1);
+    while (s->nbuf != 56) sha_update(s, &zero, 1);
+    uint8_t lb[8];
+    for (int i = 0; i < 8; ++i) lb[i] = (uint8_t)(bits >> (56 - 8 * i));
+    sha_update(s, lb, 8);
+    for (int i = 0; i < 8; ++i) {
+        out[4 * i] = (uint8_t)(s->h[i] >> 24);
+        out[4 * i + 1] = (uint8_t)(s->h[i] >> 16);
+        out[4 * i + 2] = (uint8_t)(s->h[i] >> 8);
+        out[4 * i + 3] = (uint8_t)s->h[i];
+    }
+}
+
+void or_sha256(const void* data, int64_t n, uint8_t out[32]) {
+    sha256 s;
+    sha_init(&s);
+    sha_update(&s, data, (size_t)n);
+    sha_final(&s, out);
+}
+
+static int same_cycle3(const int32_t a[3], const int32_t b[3]) {
+    return (a[0] == b[0] && a[1] == b[1] && a[2] == b[2]) || (a[0] == b[1] && a[1] == b[2] && a[2] == b[0]) ||
+           (a[0] == b[2] && a[1] == b[0] && a[2] == b[1]);
+}
+
+int or_conn_digests(int64_t nc, int64_t ne, const int32_t* tets, const double* coords, uint8_t* digests,
+                    int64_t counts[2]) {
+    enum { D_EN, D_EOS, D_F, D_FOS, D_SIG, D_FS, D_AREA, D_CLS, D_MROW, ND };
+    sha256 sh[ND];
+    for (int i = 0; i < ND; ++i) sha_init(&sh[i]);
+    edge_table et;
+    et.nc = nc;
+    hmap fm;
+    if (hmap_init(&et.map, 2 * ne + 8) || hmap_init(&fm, 2 * ne + 8)) return fail(2, "out of memory");
+    /* per face: owner slot, second slot (filled later), the stored tuple
+     * for the sigma test of the second slot */
+    int64_t cap = 2 * ne + ne / 16 + 1024; /* nF ~ 2 nE + boundary / 2; grown on demand */
+    int32_t* owner = (int32_t*)malloc((size_t)cap * sizeof(int32_t));
+    int32_t* mate = (int32_t*)malloc((size_t)cap * sizeof(int32_t));
+    if (!owner || !mate) return fail(2, "out of memory");
+    int64_t ned = 0, nf = 0;
+    for (int64_t t = 0; t < ne; ++t) {
+        const int32_t* e = tets + 4 * t;
+        int32_t eos[6];
+        for (int k = 0; k < 6; ++k) {
+            int32_t a = e[kEdgeVerts[k][0]], b = e[kEdgeVerts[k][1]];
+            if (a > b) { const int32_t x = a; a = b; b = x; }
+            int ins;
+            eos[k] = hmap_try_emplace(&et.map, (uint64_t)a * (uint64_t)nc + (uint64_t)b, (int32_t)ned, &ins);
+            if (ins) {
+                const int32_t pr[2] = {a, b};
+                sha_update(&sh[D_EN], pr, sizeof pr);
+                ++ned;
+            }
+        }
+        sha_update(&sh[D_EOS], eos, sizeof eos);
+        int32_t fos[4];
+        int8_t sig[4];
+        for (int k = 0; k < 4; ++k) {
+            int32_t f[3];
+            oriented_face(e, k, f);
+            int32_t v[3] = {f[0], f[1], f[2]};
+            /* sorted node set -> (edge of the two smallest, largest) */
+            if (v[0] > v[1]) { const int32_t x = v[0]; v[0] = v[1]; v[1] = x; }
+            if (v[1] > v[2]) { const int32_t x = v[1]; v[1] = v[2]; v[2] = x; }
+            if (v[0] > v[1]) { const int32_t x = v[0]; v[0] = v[1]; v[1] = x; }
+            const int32_t e01 = pair_to_edge(&et, v[0], v[1]);
+            int ins;
+            const int32_t id = hmap_try_emplace(&fm, (uint64_t)e01 * (uint64_t)nc + (uint64_t)v[2], (int32_t)nf, &ins);
+            fos[k] = id;
+            if (ins) {
+                if (nf == cap) {
+                    cap *= 2;
+                    owner = (int32_t*)realloc(owner, (size_t)cap * sizeof(int32_t));
+                    mate = (int32_t*)realloc(mate, (size_t)cap * sizeof(int32_t));
+                    if (!owner || !mate) return fail(2, "out of memory");
+                }
+                owner[nf] = (int32_t)(4 * t + k);
+                mate[nf] = -1;
+                sha_update(&sh[D_F], f, sizeof f);
+                double ar;
+                v3 un;
+                if (face_geom(coords, f, &ar, &un)) ar = 0.0;
+                sha_update(&sh[D_AREA], &ar, sizeof ar);
+                sig[k] = 1;
+                ++nf;
+            } else {
+                mate[id] = (int32_t)(4 * t + k);
+                const int64_t os = owner[id];
+                int32_t g[3];
+                oriented_face(tets + 4 * (os / 4), (int)(os % 4), g);
+                sig[k] = same_cycle3(f, g) ? 1 : -1;
+            }
+        }
+        sha_update(&sh[D_FOS], fos, sizeof fos);
+        sha_update(&sh[D_SIG], sig, sizeof sig);
+    }
+    for (int64_t f = 0; f < nf; ++f) {
+        const int64_t fs[2] = {owner[f], mate[f]};
+        sha_update(&sh[D_FS], fs, sizeof fs);
+        const uint8_t cls = mate[f] < 0 ? 1 : 0;
+        sha_update(&sh[D_CLS], &cls, 1);
+        const int32_t row = (int32_t)f;
+        sha_update(&sh[D_MROW], &row, sizeof row);
+    }
+    for (int i = 0; i < ND; ++i) sha_final(&sh[i], digests + 32 * i);
+    counts[0] = ned;
+    counts[1] = nf;
+    free(owner);
+    free(mate);
+    hmap_free(&et.map);
+    hmap_free(&fm);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* error norms, analysis.cpp:51-105 (+ L2 extension)                        */
 
 double or_mesh_diameter(int64_t nc, int64_t ne, const double* coords, const int32_t* tets) {

@@ -124,6 +124,17 @@ int or_errors(int64_t nc, int64_t ne, const double* coords, const int32_t* tets,
               const int32_t* face_of_slot, const int8_t* sigma, const int32_t* mrow,
               const or_problem* prob, const double* u, const double* lambda, double out[3]);
 
+/* SHA-256 (FIPS 180-4) of n bytes */
+void or_sha256(const void* data, int64_t n, uint8_t out[32]);
+/* Streaming connectivity digests for meshes whose full oracle tables do not
+ * fit host memory (config 2 level 7): digests [9 x 32] of edge_nodes int32
+ * [nEd][2], edge_of_slot int32 [nE][6], faces int32 [nF][3], face_of_slot
+ * int32 [4 nE], sigma int8 [4 nE], face_slots int64 [nF][2], face_area f64
+ * [nF], face_class u8 [nF], multiplier_index int32 [nF] of an all-Dirichlet
+ * mesh; counts [nEd, nF]. */
+int or_conn_digests(int64_t nc, int64_t ne, const int32_t* tets, const double* coords, uint8_t* digests,
+                    int64_t counts[2]);
+
 /* max element diameter (mesh.cpp:90-106) */
 double or_mesh_diameter(int64_t nc, int64_t ne, const double* coords, const int32_t* tets);
 

@@ -101,6 +101,8 @@ class Oracle:
         L.or_face_table.argtypes = [I64, I64, P, P, I64, P, I64, P, P, P, P, P, P, P, P, P]
         L.or_refine.argtypes = [I64, I64, P, P, I64, P, I64, P, P, P, P, P, P, P]
         L.or_assemble_condense.argtypes = [I64, I64, P, P, I64, P, P, P, P, P, P, P, I64, P] + [P] * 13
+        L.or_conn_digests.argtypes = [I64, I64, P, P, P, P]
+        L.or_sha256.argtypes = [P, I64, P]
         L.or_entry_scales.argtypes = [I64, I64, P, P, I64, P, P, P, P, P, P, P, I64, P, P, P]
         L.or_pcg.argtypes = [I64, P, P, P, P, P, C.c_double, C.c_double, I64, P]
         L.or_solve_schur.argtypes = [I64, I64, P, P, P, I64] + [P] * 11 + [C.c_double, I64, P, P, P]
@@ -230,6 +232,25 @@ class Oracle:
             _ptr(sys["c_col"]), _ptr(sys["c_val"]), _ptr(sys["s_rowptr"]), _ptr(sys["s_col"]),
             _ptr(sys["s_val"]), _ptr(sys["rhs_neg"]), tol, max_iter, _ptr(u), _ptr(lam), _ptr(st)))
         return u, lam, dict(iterations=int(st[0]), residual=st[1], constraint_residual=st[2])
+
+    DIGEST_KEYS = ("edge_nodes", "edge_of_slot", "faces", "face_of_slot", "sigma", "face_slots", "area",
+                   "face_class", "mrow")
+
+    def conn_digests(self, m: MeshArrays) -> dict:
+        """streaming SHA-256 digests of the connectivity arrays
+        (or_conn_digests; all-Dirichlet meshes)"""
+        d = np.zeros(32 * len(self.DIGEST_KEYS), dtype=np.uint8)
+        c = np.zeros(2, dtype=np.int64)
+        self._check(self.L.or_conn_digests(m.nc, m.ne, _ptr(m.tets), _ptr(m.coords), _ptr(d), _ptr(c)))
+        out = {k: bytes(d[32 * i:32 * i + 32]).hex() for i, k in enumerate(self.DIGEST_KEYS)}
+        out.update(ned=int(c[0]), nf=int(c[1]))
+        return out
+
+    def sha256(self, a: np.ndarray) -> str:
+        a = np.ascontiguousarray(a)
+        d = np.zeros(32, dtype=np.uint8)
+        self.L.or_sha256(_ptr(a), a.nbytes, _ptr(d))
+        return bytes(d).hex()
 
     def entry_scales(self, m: MeshArrays, ft: dict, kind=0, c=1.0, a_elem=None, a_diag=None):
         """componentwise magnitudes of B_T and rhs_neg (or_entry_scales)"""

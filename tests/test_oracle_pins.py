@@ -300,3 +300,24 @@ def test_kuhn_generator_properties(oracle):
     assert vol == pytest.approx(1.0, rel=1e-12)
     ft = oracle.faces(m)  # classification succeeds: boundary lists are complete and outward
     assert ft["n_dirichlet"] == len(m.db) and ft["n_neumann"] == len(m.nb)
+
+
+def test_streaming_digests_match_full_tables(oracle):
+    """or_conn_digests (the one-pass restatement used for config 2's level 7,
+    tools/gen_cfg2_digests.py) hashes exactly the arrays the full oracle
+    tables hold, levels 0-4 of the 6-Kuhn cube."""
+    import hashlib
+
+    m = oracle.kuhn(1, 1, 1, dmask=0x3F)
+    for _ in range(5):
+        d = oracle.conn_digests(m)
+        en, eos = oracle.edges(m)
+        f = oracle.faces(m)
+        arrs = dict(edge_nodes=en, edge_of_slot=eos, faces=f["faces"], face_of_slot=f["face_of_slot"],
+                    sigma=f["sigma"], face_slots=f["face_slots"], area=f["area"], face_class=f["face_class"],
+                    mrow=f["mrow"])
+        assert (d["ned"], d["nf"]) == (len(en), f["nf"])
+        for k, v in arrs.items():
+            assert hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() == d[k], k
+        assert oracle.sha256(en) == hashlib.sha256(en.tobytes()).hexdigest()
+        m = oracle.refine(m)[0]
