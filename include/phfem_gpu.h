@@ -103,12 +103,19 @@ int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr
  * connectivity.cpp:72-153).  slot_mate may be NULL (edges only).  Three
  * passes without host round trips: warps over stars <= 32, warps over the
  * deferred stars <= 64, blocks over anything larger (stars above 2730
- * incidences set PHG_ERR_VALENCE).  defer_list needs 2 nC entries,
- * defer_count 2. */
+ * incidences are listed for phfem_gpu_star_groups_global and set
+ * PHG_ERR_VALENCE, their slots hold in-bounds placeholders).  defer_list
+ * needs 3 nC entries, defer_count 3. */
 int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star,
                           const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
                           int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
                           void* stream);
+/* a star listed by star_groups as too large for shared memory (defer_list
+ * + 2 nC, count defer_count[2], PHG_ERR_VALENCE set): tables of capacity
+ * cap (power of two > 3 m) in global scratch [20 cap bytes] */
+int phfem_gpu_star_groups_global(int32_t v, const int64_t* star_ptr, const int32_t* star,
+                                 const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
+                                 void* scratch, unsigned cap, unsigned long long* err, void* stream);
 
 /* Per-element slot masks [ne] (bit k < 6: edge slot 6t+k is its edge's
  * first occurrence; bit 6+k: face slot 4t+k owns its face) and the exclusive

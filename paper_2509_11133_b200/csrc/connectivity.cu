@@ -475,7 +475,8 @@ __global__ void __launch_bounds__(256)
     star_groups_big(const int32_t* __restrict__ big_list, const int32_t* __restrict__ big_count,
                     const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
                     const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
-                    int32_t* __restrict__ slot_mate, unsigned cap, unsigned long long* err) {
+                    int32_t* __restrict__ slot_mate, unsigned cap, int32_t* __restrict__ huge_list,
+                    int32_t* __restrict__ huge_count, unsigned long long* err) {
     extern __shared__ __align__(16) unsigned char dsm[];
     const int32_t n = *big_count;
     for (int32_t it = blockIdx.x; it < n; it += gridDim.x) {
@@ -483,7 +484,33 @@ __global__ void __launch_bounds__(256)
         const int64_t beg = star_ptr[v];
         const int m = (int)(star_ptr[v + 1] - beg);
         if ((unsigned)(3 * m) >= cap) {
-            if (threadIdx.x == 0) report(err, PHG_ERR_VALENCE, (unsigned long long)v);
+            // too large for shared memory: placeholders that keep the
+            // numbering kernels in bounds (own slot as first occurrence, no
+            // mate), and the vertex goes to the global-memory pass the host
+            // runs when PHG_ERR_VALENCE is set (star_groups_global)
+            for (int e = threadIdx.x; e < m; e += blockDim.x) {
+                const int32_t inc = star[beg + e];
+                const int64_t t = inc >> 2;
+                const int lv = inc & 3;
+                const int4 tet = ldtet(tets, t);
+                for (int w = 0; w < 4; ++w) {
+                    if (w == lv || tv(tet, w) <= v) continue;
+                    if (edge_first) edge_first[6 * t + edge_index(lv, w)] = (int32_t)(6 * t + edge_index(lv, w));
+                }
+                if (!slot_mate) continue;
+                const int opp = opposite_face(lv);
+                for (int k = 0; k < 4; ++k) {
+                    if (k == opp) continue;
+                    int32_t x, y;
+                    face_other(tet, k, lv, x, y);
+                    if (x > v && y > v) slot_mate[4 * t + k] = -1;
+                }
+            }
+            if (threadIdx.x == 0) {
+                report(err, PHG_ERR_VALENCE, (unsigned long long)v);
+                huge_list[atomicAdd(huge_count, 1)] = v;
+            }
+            __syncthreads();
             continue;
         }
         int32_t* ekey = reinterpret_cast<int32_t*>(dsm);
@@ -497,6 +524,28 @@ __global__ void __launch_bounds__(256)
                           err, BlockSync{});
         __syncthreads();
     }
+}
+
+// Stars too large for the shared-memory tables (more than ~2730
+// incidences; the reference has no valence limit): one block, hash tables of
+// capacity `cap` (a power of two > 3 m) in global scratch memory.  Run by the
+// host only when star_groups_big listed such a vertex.
+__global__ void __launch_bounds__(256)
+    star_groups_global(int32_t v, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                       const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
+                       int32_t* __restrict__ slot_mate, unsigned char* __restrict__ scratch, unsigned cap,
+                       unsigned long long* err) {
+    const int64_t beg = star_ptr[v];
+    const int m = (int)(star_ptr[v + 1] - beg);
+    int32_t* ekey = reinterpret_cast<int32_t*>(scratch);
+    int32_t* eval = ekey + cap;
+    FaceTab ft;
+    ft.key = reinterpret_cast<unsigned long long*>(scratch);
+    ft.lo = reinterpret_cast<int32_t*>(scratch + (size_t)cap * 8);
+    ft.hi = ft.lo + cap;
+    ft.cnt = ft.hi + cap;
+    group_vertex<256>(v, beg, m, threadIdx.x, star, tets, edge_first, slot_mate, ekey, eval, ft, cap - 1, cap, err,
+                      BlockSync{});
 }
 
 // -------------------------------------------------------------- numbering
@@ -898,7 +947,7 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     // pass 2: deferred stars <= 64 (warp, two per lane)
     // pass 3: anything larger (block per vertex); counts stay on the device
     cudaStream_t s = (cudaStream_t)stream;
-    cudaMemsetAsync(defer_count, 0, 2 * sizeof(int32_t), s);
+    cudaMemsetAsync(defer_count, 0, 3 * sizeof(int32_t), s);
     // one full wave of resident blocks (grid-stride over the vertices)
     static int resident = 0;
     if (resident == 0) {
@@ -917,8 +966,17 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     const size_t bytes = (size_t)cap * 20;
     cudaFuncSetAttribute(star_groups_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     star_groups_big<<<kSMs, 256, bytes, s>>>(defer_list + nc, defer_count + 1, star_ptr, star, tets, edge_first,
-                                             slot_mate, cap, err);
+                                             slot_mate, cap, defer_list + 2 * nc, defer_count + 2, err);
     phg::count_launches(3);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_star_groups_global(int32_t v, const int64_t* star_ptr, const int32_t* star,
+                                            const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
+                                            void* scratch, unsigned cap, unsigned long long* err, void* stream) {
+    star_groups_global<<<1, 256, 0, (cudaStream_t)stream>>>(v, star_ptr, star, tets, edge_first, slot_mate,
+                                                           static_cast<unsigned char*>(scratch), cap, err);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

@@ -49,9 +49,7 @@ void fetch_tri(const int32_t* dev, int64_t i, int32_t out[3]) {
 // check; 3: everything)
 void replay_connectivity_errors(const std::vector<unsigned long long>& e, const MeshData& m, const Connectivity& c,
                                 int upto = 3) {
-    if (e[PHG_ERR_VALENCE] != kNone)
-        throw MeshError("vertex " + std::to_string(e[PHG_ERR_VALENCE] + 1) +
-                        " is shared by more elements than the connectivity kernels support");
+    // (PHG_ERR_VALENCE is not an error: those stars took the global path)
     if (upto < 2) return;
     if (e[PHG_ERR_DUP_ORIENT] != kNone) {
         const unsigned long long k = e[PHG_ERR_DUP_ORIENT];
@@ -81,6 +79,35 @@ void replay_connectivity_errors(const std::vector<unsigned long long>& e, const 
     }
 }
 
+// Stars above the shared-memory capacity of star_groups_big (listed at
+// big_list + 2 nC): grouped one by one with global-memory tables, then the
+// valence flag is cleared.  Rare (no such vertex in any config here), so the
+// host loop and its reads are off the normal path.
+void group_huge_stars(const MeshData& m, Connectivity& c, bool faces) {
+    Work& w = c.w;
+    const int64_t nc = m.nc;
+    int32_t n = 0;
+    check(cudaMemcpyAsync(&n, w.big_count.p + 2, sizeof n, cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    std::vector<int32_t> list(n);
+    if (n) check(cudaMemcpyAsync(list.data(), w.big_list.p + 2 * nc, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, S()),
+                 "D2H");
+    sync();
+    DBuf<unsigned char> scratch;
+    for (const int32_t v : list) {
+        int64_t se[2];
+        check(cudaMemcpyAsync(se, c.star_ptr.p + v, sizeof se, cudaMemcpyDeviceToHost, S()), "D2H");
+        sync();
+        unsigned cap = 16;
+        while (cap <= 3 * (uint64_t)(se[1] - se[0])) cap <<= 1;
+        scratch.alloc((int64_t)cap * 20);
+        check(phfem_gpu_star_groups_global(v, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                           faces ? c.slot_mate.p : nullptr, scratch.p, cap, w.err.p, SV()),
+              "star groups (global)");
+    }
+    check(cudaMemsetAsync(w.err.p + PHG_ERR_VALENCE, 0xff, sizeof(unsigned long long), S()), "memset");
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ connectivity
@@ -107,8 +134,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (st) t0 = st->mark();
     c.edge_first.alloc(6 * ne);
     if (faces) c.slot_mate.alloc(4 * ne);
-    w.big_list.alloc(2 * (nc > 0 ? nc : 1));
-    w.big_count.alloc(2);
+    w.big_list.alloc(3 * (nc > 0 ? nc : 1));
+    w.big_count.alloc(3);
     check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
                                 w.big_list.p, w.big_count.p, w.err.p, SV()),
           "star groups");
@@ -121,12 +148,19 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p, c.edge_off.p,
                                     faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
           "element offsets");
-    if (faces) {
-        const auto tot = read_many<int64_t, 2>({c.edge_off.p + ne, w.face_off.p + ne});
+    // the totals, and whether a star was too large for the shared-memory
+    // tables (the reference has no valence limit): then the global-memory
+    // pass groups those vertices and the offsets are redone
+    for (int pass = 0;; ++pass) {
+        const auto tot = read_many<int64_t, 3>({c.edge_off.p + ne, faces ? w.face_off.p + ne : c.edge_off.p + ne,
+                                                reinterpret_cast<const int64_t*>(w.err.p + PHG_ERR_VALENCE)});
         c.ned = tot[0];
-        c.nf = tot[1];
-    } else {
-        c.ned = read_scalar(c.edge_off.p + ne);
+        c.nf = faces ? tot[1] : 0;
+        if ((unsigned long long)tot[2] == kNone || pass > 0) break;
+        group_huge_stars(m, c, faces);
+        check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p,
+                                        c.edge_off.p, faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
+              "element offsets");
     }
     c.edge_of_slot.alloc(6 * ne);
     c.edge_nodes.alloc(2 * c.ned);

@@ -420,3 +420,39 @@ def test_config2_level5_bit_exact(oracle):
     for k in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, k), getattr(m, k)), k
     check_connectivity(g, m, oracle)
+
+
+def _fan(k: int) -> MeshArrays:
+    """A bipyramid fan: centre c, a ring of k nodes, apexes above and below;
+    2k tets share c (the reference has no valence limit)."""
+    th = 2.0 * np.pi * np.arange(k) / k
+    coords = np.zeros((k + 3, 3))
+    coords[1:k + 1, 0] = np.cos(th)
+    coords[1:k + 1, 1] = np.sin(th)
+    coords[k + 1] = (0.0, 0.0, 1.0)
+    coords[k + 2] = (0.0, 0.0, -1.0)
+    r = np.arange(1, k + 1, dtype=np.int32)
+    rn = np.roll(r, -1)
+    top, bot = k + 1, k + 2
+    up = np.stack([np.zeros(k, np.int32), r, rn, np.full(k, top, np.int32)], axis=1)
+    lo = np.stack([np.zeros(k, np.int32), rn, r, np.full(k, bot, np.int32)], axis=1)
+    tets = np.ascontiguousarray(np.stack([up, lo], axis=1).reshape(-1, 4))
+    db = np.ascontiguousarray(np.stack([np.full(k, top, np.int32), rn, r], axis=1))
+    nb = np.ascontiguousarray(np.stack([np.full(k, bot, np.int32), r, rn], axis=1))
+    return MeshArrays(coords, tets, db, nb, 0)
+
+
+@pytest.mark.parametrize("k", [700, 2000])
+def test_high_valence_star(oracle, k):
+    """stars above the shared-memory tables (2k = 4000 incidences at the
+    centre) go through the global-memory grouping; the numbering, system and
+    one refinement stay bit-exact"""
+    m = _fan(k)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, 0)
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for key in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
