@@ -209,10 +209,13 @@ int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, con
                                 int32_t* sell_col,
                                 double* sell_val,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
-                                double* slot_coef, int32_t* slot_mrow, double* norms,
-                                double* partials, int32_t* redo, unsigned long long* err, void* ev_begin,
-                                void* ev_end, void* stream);
+                                double* slot_coef, int32_t* slot_mrow, int32_t* redo,
+                                unsigned long long* err, void* ev_begin, void* ev_end, void* stream);
 int phfem_gpu_assemble_grid(int64_t ne);
+/* norms [2] (device) = ||rhs||^2 [n], ||bd||^2 [l], deterministic; partials
+ * [2 phfem_gpu_assemble_grid(n)] */
+int phfem_gpu_sumsq2(const double* rhs, int64_t n, const double* bd, int64_t l, double* partials,
+                     double* norms, void* stream);
 
 /* --------------------------------------------------------------- solver */
 typedef struct phg_cg_state {

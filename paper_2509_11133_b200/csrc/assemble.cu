@@ -649,9 +649,8 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            int32_t* sell_col,
                                            double* sell_val,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
-                                           double* slot_coef, int32_t* slot_mrow, double* norms, double* partials,
-                                           int32_t* redo, unsigned long long* err, void* ev_begin, void* ev_end,
-                                           void* stream) {
+                                           double* slot_coef, int32_t* slot_mrow, int32_t* redo,
+                                           unsigned long long* err, void* ev_begin, void* ev_end, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne == 0) return 0;
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
@@ -680,8 +679,17 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
         default: return (int)cudaErrorInvalidValue;
     }
 #undef PHG_ASM
-    sumsq2_k<<<kNormGrid, 256, 0, s>>>(rhs, 4 * ne, bd, l, partials);
+    phg::count_launches(4);
+    return (int)cudaGetLastError();
+}
+
+// ||B||^2, ||b_D||^2 for inner_cg_options (solver.cpp:78-86): computed when a
+// solve asks for them, as the reference does, not inside the assembly
+extern "C" int phfem_gpu_sumsq2(const double* rhs, int64_t n, const double* bd, int64_t l, double* partials,
+                                double* norms, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    sumsq2_k<<<kNormGrid, 256, 0, s>>>(rhs, n, bd, l, partials);
     reduce_pairs<<<1, 1024, 0, s>>>(partials, kNormGrid, norms);
-    phg::count_launches(6);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }

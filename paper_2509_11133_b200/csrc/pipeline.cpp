@@ -320,10 +320,7 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
         sys.slot_coef.release();
         sys.slot_mrow.release();
     }
-    const int grid = phfem_gpu_assemble_grid(m.ne);
     Work& w = sys.w;
-    w.partials.alloc(2 * (int64_t)grid);
-    w.norms.alloc(2);
     w.redo.alloc(m.ne + 1);
     reset_err(w);
     const phg_problem p = device_problem(k, problem);
@@ -335,8 +332,7 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
                                       w.face_bval.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
                                       sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
                                       debug_views ? sys.slot_coef.p : nullptr,
-                                      debug_views ? sys.slot_mrow.p : nullptr, w.norms.p, w.partials.p, w.redo.p,
-                                      w.err.p, ka, kb, SV()),
+                                      debug_views ? sys.slot_mrow.p : nullptr, w.redo.p, w.err.p, ka, kb, SV()),
           "assemble");
     if (st) {
         st->span(&st->assemble, t0);

@@ -347,8 +347,10 @@ std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly
 // ------------------------------------------------------------------- solve
 
 void System::norms(double& sum_rhs2, double& sum_bd2) const {
+    DBuf<double> partials(2 * (int64_t)phfem_gpu_assemble_grid(n / 4)), out(2);
+    check(phfem_gpu_sumsq2(rhs.p, n, bd.p, l, partials.p, out.p, SV()), "norms");
     double h[2];
-    check(cudaMemcpyAsync(h, w.norms.p, sizeof(h), cudaMemcpyDeviceToHost, S()), "D2H");
+    check(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, S()), "D2H");
     sync();
     sum_rhs2 = h[0];
     sum_bd2 = h[1];

@@ -220,8 +220,8 @@ struct System {
     int64_t n = 0, l = 0, nchunks = 0;
     DBuf<int32_t> sell_col;
     DBuf<double> sell_val, rhs_neg, bd, rhs;
-    // sum(B_T^2), sum(b_D^2): reduced on the device by the assembly, read
-    // to the host only when a solve needs them
+    // sum(B_T^2), sum(b_D^2) for inner_cg_options: reduced on the device
+    // when a solve asks (the reference computes them at solve time too)
     void norms(double& sum_rhs2, double& sum_bd2) const;
     // debug views (filled only on request)
     DBuf<double> a_blocks, slot_coef;
