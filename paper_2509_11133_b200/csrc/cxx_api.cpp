@@ -1489,3 +1489,34 @@ void export_multiplier_vtk(const std::string& path, const Mesh& mesh, const Face
 }
 
 }  // namespace phfem
+
+namespace phb {
+
+// The pair edge_pairs_to_elems names when two elements claim the same
+// oriented face (connectivity.cpp:62-68): the first repeated key of the
+// sorted E2T entries.  The pipeline never builds the E2T; on that error path
+// it is built once on the device to report the reference's exact pair.
+bool e2t_first_duplicate(const MeshData& m, const Connectivity& c, int32_t& a, int32_t& b) {
+    const int64_t ne = m.ne, n = 12 * ne, ned = c.ned;
+    if (!c.has_edges || n == 0) return false;
+    DBuf<int64_t> from(n), to(n), seg_ptr(ned + 1), perm(n), tmp(n);
+    DBuf<int32_t> cnt(ned > 0 ? ned : 1), elem(n);
+    DBuf<unsigned long long> key(n), dup(1);
+    DBuf<unsigned char> ss(phfem_gpu_scan_scratch(ned > 0 ? ned : 1));
+    dup.fill_bytes(0xff);
+    check(phfem_gpu_e2t_entries(ne, c.edge_of_slot.p, from.p, to.p, SV()), "e2t entries");
+    check(phfem_gpu_seg_sort(n, ned, from.p, to.p, seg_ptr.p, perm.p, cnt.p, tmp.p, ss.p, SV()), "e2t sort");
+    check(phfem_gpu_e2t_finish(n, ned, perm.p, from.p, to.p, key.p, elem.p, dup.p, SV()), "e2t finish");
+    unsigned long long j;
+    check(cudaMemcpyAsync(&j, dup.p, sizeof j, cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    if (j == ~0ull) return false;
+    int32_t pair[2];
+    check(cudaMemcpyAsync(pair, elem.p + j - 1, sizeof pair, cudaMemcpyDeviceToHost, S()), "D2H");
+    sync();
+    a = pair[0];
+    b = pair[1];
+    return true;
+}
+
+}  // namespace phb

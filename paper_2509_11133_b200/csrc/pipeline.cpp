@@ -52,9 +52,13 @@ void replay_connectivity_errors(const std::vector<unsigned long long>& e, const 
     // (PHG_ERR_VALENCE is not an error: those stars took the global path)
     if (upto < 2) return;
     if (e[PHG_ERR_DUP_ORIENT] != kNone) {
+        // the reference names the first repeated key of its sorted E2T
+        // entries: build that map on this error path to name the same pair
         const unsigned long long k = e[PHG_ERR_DUP_ORIENT];
-        throw MeshError("inconsistent mesh: elements " + std::to_string((k >> 32) + 1) + " and " +
-                        std::to_string((k & 0xffffffffull) + 1) + " claim the same oriented face");
+        int32_t a = (int32_t)(k >> 32), b = (int32_t)(k & 0xffffffffull);
+        e2t_first_duplicate(m, c, a, b);
+        throw MeshError("inconsistent mesh: elements " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
+                        " claim the same oriented face");
     }
     if (upto < 3) return;
     if (e[PHG_ERR_CLASSIFY] != kNone) {
@@ -136,8 +140,9 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(3 * (nc > 0 ? nc : 1));
     w.big_count.alloc(3);
-    check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
-                                w.big_list.p, w.big_count.p, w.err.p, SV()),
+    w.vstart.alloc((int64_t)phfem_gpu_star_groups_tiles(4 * ne) + 2);
+    check(phfem_gpu_star_groups(nc, 4 * ne, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.vstart.p, w.err.p, SV()),
           "star groups");
     if (st) st->span(&st->groups, t0);
     // 3. numbering: per-element counts, scans, ids, remaining slots

@@ -181,7 +181,7 @@ struct Coefs {
 // transient device buffers of one connectivity / refinement / assembly pass,
 // kept with their owner so repeated passes reuse them
 struct Work {
-    DBuf<int32_t> cnt, big_list, big_count, packed, redo;
+    DBuf<int32_t> cnt, big_list, big_count, packed, redo, vstart;
     DBuf<double> face_bval;  // boundary faces' b_D / Neumann terms (assembly)
     DBuf<int64_t> face_off;
     DBuf<unsigned char> scratch;
@@ -302,6 +302,8 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
                  bool refuse_throws = true);
 
 double mesh_diameter(const MeshData& m);
+// edge_pairs_to_elems' duplicate error pair (cxx_api.cpp), for the error path
+bool e2t_first_duplicate(const MeshData& m, const Connectivity& c, int32_t& a, int32_t& b);
 // [y-norm, kappa-norm, L2]
 void error_norms(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, const double* u,
                  const double* lambda, double out[3]);
