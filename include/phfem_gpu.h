@@ -100,21 +100,16 @@ int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr
  * vertex is v among the incident element slots: edge_first[6t+k] = smallest
  * slot of the edge (first occurrence, connectivity.cpp:22-37); slot_mate[4t+k]
  * = the other slot of the face or -1 (faces_up/full_face_table,
- * connectivity.cpp:72-153).  slot_mate may be NULL (edges only).  Passes
- * without host round trips: tiles of 256 incidences of the star (one thread
- * per incidence, one shared table pair per tile; stars <= 64), blocks over
- * larger stars (stars above 2730 incidences are listed for
- * phfem_gpu_star_groups_global and set PHG_ERR_VALENCE, their slots hold
- * in-bounds placeholders).  defer_list needs 3 nC entries, defer_count 3,
- * vstart phfem_gpu_star_groups_tiles(4 nE) + 1.  PHG_GROUPS=warp selects the
- * round-1 warp-per-vertex first pass (A/B measurement). */
-int phfem_gpu_star_groups(int64_t nc, int64_t ninc, const int64_t* star_ptr, const int32_t* star,
+ * connectivity.cpp:72-153).  slot_mate may be NULL (edges only).  Three
+ * passes without host round trips: warps over stars <= 32, warps over the
+ * deferred stars <= 64, blocks over anything larger (stars above 2730
+ * incidences are listed for phfem_gpu_star_groups_global and set
+ * PHG_ERR_VALENCE, their slots hold in-bounds placeholders).  defer_list
+ * needs 3 nC entries, defer_count 3. */
+int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star,
                           const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
-                          int32_t* defer_list, int32_t* defer_count, int32_t* vstart,
-                          unsigned long long* err, void* stream);
-/* tiles of the star pass (vstart needs tiles + 1 entries) for ninc = 4 nE
- * incidences */
-size_t phfem_gpu_star_groups_tiles(int64_t ninc);
+                          int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
+                          void* stream);
 /* a star listed by star_groups as too large for shared memory (defer_list
  * + 2 nC, count defer_count[2], PHG_ERR_VALENCE set): tables of capacity
  * cap (power of two > 3 m) in global scratch [20 cap bytes] */

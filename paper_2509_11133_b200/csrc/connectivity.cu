@@ -17,8 +17,6 @@
 // The directed edge-pair map (E2T) is never materialised; its only check
 // (two elements claiming the same oriented face) is the orientation test in 2.
 #include <climits>
-#include <cstdlib>
-#include <string>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -461,226 +459,6 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             I2[u] = I3[u];
             T1[u] = T2[u];
         }
-    }
-}
-
-// ------------------------------------- tile path: stars of <= kTileMaxStar
-
-// The star array cut into tiles of kTileC incidences: block b takes the
-// vertices whose star starts in its tile, [vstart[b], vstart[b+1]), and
-// groups all their candidates in ONE shared-memory table pair, one thread per
-// incidence (no per-vertex table set-up, list compaction or idle lanes: the
-// warp-per-vertex kernel spent ~390 warp instructions per vertex).
-//   edges:  key (v - V0) << 32 | b for b > v, value = min slot (first
-//           occurrence, connectivity.cpp:22-37);
-//   faces:  the face {v, lo, hi} (v < lo < hi) is keyed by the table slot of
-//           its edge (v, lo) -- an edge candidate of the same vertex, so
-//           inserted by this block -- and hi: (slot << 32 | hi); the two
-//           slots of the group pair up (slot_mate), same orientation twice
-//           is the reference's duplicate-orientation error.
-// At most 3 edge and 3 face keys per incidence and tiles of at most
-// kTileC + kTileMaxStar - 1 incidences: kTileCap > 3 (kTileC + kTileMaxStar)
-// can never fill.  Stars above kTileMaxStar go to the block-per-vertex pass.
-constexpr int kTileC = 256;
-constexpr int kTileMaxStar = 64;
-constexpr int kTileCap = 1024;
-constexpr int kTileThreads = 128;
-static_assert(kTileCap > 3 * (kTileC + kTileMaxStar), "tile tables must not fill");
-
-__global__ void tile_starts_k(int64_t nc, const int64_t* __restrict__ star_ptr, int64_t ntiles,
-                              int32_t* __restrict__ vstart) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; v <= nc;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = star_ptr[v - 1], q = star_ptr[v];
-        // tiles b with b C in (p, q] start at vertex v
-        for (int64_t b = p / kTileC + 1; b * kTileC <= q && b < ntiles; ++b) vstart[b] = (int32_t)v;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        vstart[0] = 0;
-        vstart[ntiles] = (int32_t)nc;
-    }
-}
-
-// One incidence of a tile: its element, local vertex, vertex and the other
-// three vertices in local order, as in star_groups_warp (the local edge of
-// neighbour i is 0xb15663088 >> 9 lv, 3 bits per i; the face of lv without
-// neighbour i is local face 0x9c72c9 >> 6 lv, 2 bits per i, and its vertex
-// following lv in the oriented cycle is neighbour i+1 for even lv, i+2 for
-// odd lv).  Edge / face table slots of its candidates are kept (10 bits each,
-// kTileCap = 1024) so no lookup is repeated.
-struct TileInc {
-    int32_t t, v, o[3];
-    int lv;
-    bool ok;
-    uint32_t eh, fh;  // 3 x 10-bit table slots (valid candidates only)
-};
-
-__device__ __forceinline__ void tile_load(TileInc& c, int64_t i, int64_t s1, const int64_t* __restrict__ star_ptr,
-                                          const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
-                                          int32_t* __restrict__ defer_list, int32_t* __restrict__ defer_count) {
-    c.ok = false;
-    if (i >= s1) return;
-    const int32_t inc = __ldg(star + i);
-    c.t = inc >> 2;
-    c.lv = inc & 3;
-    const int4 tet = ldtet(tets, c.t);
-    const int lv = c.lv;
-    c.v = lv == 0 ? tet.x : (lv == 1 ? tet.y : (lv == 2 ? tet.z : tet.w));
-    c.o[0] = lv == 0 ? tet.y : tet.x;
-    c.o[1] = lv <= 1 ? tet.z : tet.y;
-    c.o[2] = lv <= 2 ? tet.w : tet.z;
-    const int64_t a = __ldg(star_ptr + c.v);
-    if (__ldg(star_ptr + c.v + 1) - a > kTileMaxStar) {
-        if (i == a) defer_list[atomicAdd(defer_count, 1)] = c.v;  // the block-per-vertex pass
-        return;
-    }
-    c.ok = true;
-}
-
-__device__ __forceinline__ unsigned tile_insert64(unsigned long long* key_tab, unsigned long long key) {
-    constexpr unsigned mask = kTileCap - 1;
-    unsigned h = bucket(hash64(key), mask);
-    for (;;) {
-        const unsigned long long old = atomicCAS(key_tab + h, ~0ull, key);
-        if (old == ~0ull || old == key) return h;
-        h = (h + 1) & mask;
-    }
-}
-
-constexpr int kTileR = (kTileC + kTileMaxStar + kTileThreads - 1) / kTileThreads;  // rounds of a tile
-
-struct TileTabs {
-    unsigned long long ekey[kTileCap], fkey[kTileCap];
-    int32_t eval[kTileCap], fcnt[kTileCap];
-    int2 fsl[kTileCap];
-};
-
-__device__ __forceinline__ void tile_clear(TileTabs& T) {
-    for (int i = threadIdx.x; i < kTileCap; i += kTileThreads) {
-        T.ekey[i] = ~0ull;
-        T.fkey[i] = ~0ull;
-        T.eval[i] = INT_MAX;
-        T.fcnt[i] = 0;
-    }
-}
-
-// One pass over the incidences [lo, hi) (<= kTileR * kTileThreads, whole
-// stars only): edge inserts, face inserts, results.  Tables must be clear on
-// entry; the caller clears them again for a next pass.
-__device__ __forceinline__ void tile_pass(TileTabs& T, int64_t lo, int64_t hi, int32_t V0,
-                                          const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
-                                          const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
-                                          int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
-                                          int32_t* __restrict__ defer_count, unsigned long long* err) {
-    constexpr int R = kTileR;
-    const bool do_faces = slot_mate != nullptr;
-    TileInc c[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-        tile_load(c[r], lo + r * kTileThreads + threadIdx.x, hi, star_ptr, star, tets, defer_list, defer_count);
-    __syncthreads();
-    // edges: key (v - V0, b), value min slot
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        c[r].eh = 0;
-        if (!c[r].ok) continue;
-        const unsigned long long hi32 = (unsigned long long)(uint32_t)(c[r].v - V0) << 32;
-        const unsigned etab = (unsigned)(0xb15663088ull >> (9 * c[r].lv));
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-            const int32_t b = c[r].o[n];
-            if (b <= c[r].v) continue;
-            const unsigned h = tile_insert64(T.ekey, hi32 | (uint32_t)b);
-            atomicMin(T.eval + h, 6 * c[r].t + (int)((etab >> (3 * n)) & 7u));
-            c[r].eh |= h << (10 * n);
-        }
-    }
-    __syncthreads();
-    // faces {v, lo, hi}: key (edge slot of (v, lo), hi); two slots each
-    if (do_faces) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            c[r].fh = 0;
-            if (!c[r].ok) continue;
-            const unsigned ktab = (unsigned)(0x9c72c9u >> (6 * c[r].lv)) & 63u;
-#pragma unroll
-            for (int n = 0; n < 3; ++n) {
-                const int na = n == 2 ? 0 : n + 1, nb = n == 0 ? 2 : n - 1;  // (n+1)%3, (n+2)%3
-                const int32_t a = c[r].o[na], b = c[r].o[nb];
-                if (a <= c[r].v || b <= c[r].v) continue;
-                const int nlo = a < b ? na : nb;
-                const int32_t fhi = a < b ? b : a;
-                const unsigned he = (c[r].eh >> (10 * nlo)) & 1023u;
-                const unsigned h = tile_insert64(T.fkey, (unsigned long long)he << 32 | (uint32_t)fhi);
-                // count << 2 | orientation: the vertex following v is a (even
-                // lv) or b (odd lv); one slot of each orientation sums to 11
-                const bool xy = (c[r].lv & 1) ? b < a : a < b;
-                const int pos = atomicAdd(T.fcnt + h, xy ? 5 : 6) >> 2;
-                if (pos < 2)
-                    reinterpret_cast<int32_t*>(T.fsl)[2 * h + pos] = 4 * c[r].t + (int)((ktab >> (2 * n)) & 3u);
-                c[r].fh |= h << (10 * n);
-            }
-        }
-        __syncthreads();
-    }
-    // results to the slots
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-        if (!c[r].ok) continue;
-        const unsigned etab = (unsigned)(0xb15663088ull >> (9 * c[r].lv));
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-            if (c[r].o[n] <= c[r].v) continue;
-            edge_first[6 * (int64_t)c[r].t + ((etab >> (3 * n)) & 7u)] = T.eval[(c[r].eh >> (10 * n)) & 1023u];
-        }
-        if (!do_faces) continue;
-        const unsigned ktab = (unsigned)(0x9c72c9u >> (6 * c[r].lv)) & 63u;
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-            const int32_t a = c[r].o[n == 2 ? 0 : n + 1], b = c[r].o[n == 0 ? 2 : n - 1];
-            if (a <= c[r].v || b <= c[r].v) continue;
-            const unsigned h = (c[r].fh >> (10 * n)) & 1023u;
-            const int32_t slot = 4 * c[r].t + (int)((ktab >> (2 * n)) & 3u);
-            const int32_t cn = T.fcnt[h];
-            const int cnt = cn >> 2;
-            const int2 pr = T.fsl[h];
-            if (cnt > 2 || (cnt == 2 && cn != 11)) {
-                // same orientation twice: "elements A and B claim the same
-                // oriented face" (connectivity.cpp:62-68; the host names the
-                // reference's pair from the E2T map)
-                const int32_t ls = min(pr.x, pr.y), hs = max(pr.x, pr.y);
-                report(err, PHG_ERR_DUP_ORIENT, (unsigned long long)(ls >> 2) << 32 | (unsigned long long)(hs >> 2));
-            }
-            slot_mate[slot] = cnt >= 2 ? (slot == pr.x ? pr.y : pr.x) : -1;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kTileThreads)
-    star_groups_tile(const int32_t* __restrict__ vstart, const int64_t* __restrict__ star_ptr,
-                     const int32_t* __restrict__ star, const int32_t* __restrict__ tets,
-                     int32_t* __restrict__ edge_first, int32_t* __restrict__ slot_mate,
-                     int32_t* __restrict__ defer_list, int32_t* __restrict__ defer_count, unsigned long long* err) {
-    __shared__ TileTabs T;
-    tile_clear(T);
-    const int32_t V0 = vstart[blockIdx.x], V1 = vstart[blockIdx.x + 1];
-    const int64_t s0 = star_ptr[V0], s1 = star_ptr[V1];
-    if (s1 - s0 <= (int64_t)kTileR * kTileThreads) {
-        tile_pass(T, s0, s1, V0, star_ptr, star, tets, edge_first, slot_mate, defer_list, defer_count, err);
-        return;
-    }
-    // a star above kTileMaxStar inflated the tile: one pass per vertex (the
-    // long stars themselves go to the block-per-vertex pass)
-    for (int32_t v = V0; v < V1; ++v) {
-        const int64_t a = star_ptr[v], b = star_ptr[v + 1];
-        if (b - a > kTileMaxStar) {
-            if (threadIdx.x == 0) defer_list[atomicAdd(defer_count, 1)] = v;
-            continue;
-        }
-        if (b == a) continue;
-        tile_pass(T, a, b, V0, star_ptr, star, tets, edge_first, slot_mate, defer_list, defer_count, err);
-        __syncthreads();
-        tile_clear(T);
     }
 }
 
@@ -1162,49 +940,34 @@ extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_
     return (int)cudaGetLastError();
 }
 
-extern "C" size_t phfem_gpu_star_groups_tiles(int64_t ninc) { return (size_t)((ninc + kTileC - 1) / kTileC); }
-
-extern "C" int phfem_gpu_star_groups(int64_t nc, int64_t ninc, const int64_t* star_ptr, const int32_t* star,
-                                     const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
-                                     int32_t* defer_list, int32_t* defer_count, int32_t* vstart,
-                                     unsigned long long* err, void* stream) {
-    // tiles of the star (stars <= kTileMaxStar, one thread per incidence),
-    // then a block per vertex for larger stars (<= 2730 incidences, shared
-    // tables), then the host's global-memory pass for anything larger
+extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
+                                     int32_t* edge_first, int32_t* slot_mate, int32_t* defer_list,
+                                     int32_t* defer_count, unsigned long long* err, void* stream) {
+    // pass 1: all vertices, stars <= 32 (warp, one incidence per lane)
+    // pass 2: deferred stars <= 64 (warp, two per lane)
+    // pass 3: anything larger (block per vertex); counts stay on the device
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(defer_count, 0, 3 * sizeof(int32_t), s);
-    static const bool warp_path = getenv("PHG_GROUPS") && std::string(getenv("PHG_GROUPS")) == "warp";
-    if (!warp_path) {
-        const int64_t ntiles = (int64_t)phfem_gpu_star_groups_tiles(ninc);
-        if (ntiles > 0) {
-            tile_starts_k<<<grid_cap(nc, 256), 256, 0, s>>>(nc, star_ptr, ntiles, vstart);
-            star_groups_tile<<<(unsigned)ntiles, kTileThreads, 0, s>>>(vstart, star_ptr, star, tets, edge_first, slot_mate,
-                                                                       defer_list + nc, defer_count + 1, err);
-        }
-        phg::count_launches(2);
-    } else {
-        // warp per vertex (round 1): stars <= 32, then the deferred <= 64
-        static int resident = 0;
-        if (resident == 0) {
-            int per_sm = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, star_groups_warp<1>, 32 * kFastWarps, 0);
-            resident = (per_sm > 0 ? per_sm : 8) * kSMs;
-        }
-        const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
-        const int grid = (int)(blocks < resident ? blocks : resident);
-        star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
-                                                             slot_mate, defer_list, defer_count, err);
-        star_groups_warp<2><<<kSMs * 4, 32 * kFastWarps, 0, s>>>(0, defer_list, defer_count, star_ptr, star, tets,
-                                                                 edge_first, slot_mate, defer_list + nc,
-                                                                 defer_count + 1, err);
-        phg::count_launches(2);
+    // one full wave of resident blocks (grid-stride over the vertices)
+    static int resident = 0;
+    if (resident == 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, star_groups_warp<1>, 32 * kFastWarps, 0);
+        resident = (per_sm > 0 ? per_sm : 8) * kSMs;
     }
+    const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
+    const int grid = (int)(blocks < resident ? blocks : resident);
+    star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
+                                                         slot_mate, defer_list, defer_count, err);
+    star_groups_warp<2><<<kSMs * 4, 32 * kFastWarps, 0, s>>>(0, defer_list, defer_count, star_ptr, star, tets,
+                                                             edge_first, slot_mate, defer_list + nc,
+                                                             defer_count + 1, err);
     constexpr unsigned cap = 8192;  // stars up to 2730 incidences
     const size_t bytes = (size_t)cap * 20;
     cudaFuncSetAttribute(star_groups_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     star_groups_big<<<kSMs, 256, bytes, s>>>(defer_list + nc, defer_count + 1, star_ptr, star, tets, edge_first,
                                              slot_mate, cap, defer_list + 2 * nc, defer_count + 2, err);
-    phg::count_launches(1);
+    phg::count_launches(3);
     return (int)cudaGetLastError();
 }
 

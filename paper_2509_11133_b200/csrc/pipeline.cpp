@@ -140,9 +140,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(3 * (nc > 0 ? nc : 1));
     w.big_count.alloc(3);
-    w.vstart.alloc((int64_t)phfem_gpu_star_groups_tiles(4 * ne) + 2);
-    check(phfem_gpu_star_groups(nc, 4 * ne, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
-                                faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.vstart.p, w.err.p, SV()),
+    check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
+                                w.big_list.p, w.big_count.p, w.err.p, SV()),
           "star groups");
     if (st) st->span(&st->groups, t0);
     // 3. numbering: per-element counts, scans, ids, remaining slots

@@ -181,7 +181,7 @@ struct Coefs {
 // transient device buffers of one connectivity / refinement / assembly pass,
 // kept with their owner so repeated passes reuse them
 struct Work {
-    DBuf<int32_t> cnt, big_list, big_count, packed, redo, vstart;
+    DBuf<int32_t> cnt, big_list, big_count, packed, redo;
     DBuf<double> face_bval;  // boundary faces' b_D / Neumann terms (assembly)
     DBuf<int64_t> face_off;
     DBuf<unsigned char> scratch;
