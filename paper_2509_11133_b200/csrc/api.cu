@@ -41,7 +41,9 @@ __global__ void seg_scatter_k(int64_t n, const int64_t* __restrict__ seg, const 
                               int32_t* __restrict__ cursor, int64_t* __restrict__ perm) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = seg[i];
-        perm[ptr[s] + atomicAdd(cursor + s, 1)] = i;
+        const int32_t k = atomicAdd(cursor + s, 1);
+        PHG_CHECK(ptr[s] + k < ptr[s + 1]);
+        perm[ptr[s] + k] = i;
     }
 }
 

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int k = 1; k < PHG_SELL_W; ++k) {
             const int32_t c = __ldg(sell_col + base + k * PHG_SELL_C);
+            PHG_CHECK(c >= 0 && c < l);
             const double v = __ldg(sell_val + base + k * PHG_SELL_C);
             s += v * __ldg(p + c);
         }

@@ -10,6 +10,17 @@
 
 #include "phfem_gpu.h"
 
+// Checked builds (make EXTRA=-DPHG_CHECKS, tests/test_gpu_checked.py): device
+// asserts on the indices the kernels compute (star positions, hash probes,
+// first-occurrence slots, node / row ids).  compute-sanitizer is not
+// available on the GPU pool; these bounds checks stand in for its memcheck.
+#ifdef PHG_CHECKS
+#include <cassert>
+#define PHG_CHECK(cond) assert(cond)
+#else
+#define PHG_CHECK(cond) ((void)0)
+#endif
+
 namespace phg {
 
 // ---------------------------------------------------------------- exact fp64

@@ -44,6 +44,7 @@ __global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, const in
         const int32_t base = (int32_t)(4 * t);
         const int32_t c0 = atomicSub(count + e.x, 1), c1 = atomicSub(count + e.y, 1), c2 = atomicSub(count + e.z, 1),
                       c3 = atomicSub(count + e.w, 1);
+        PHG_CHECK(c0 >= 1 && c0 <= star_ptr[e.x + 1] - star_ptr[e.x] && c1 >= 1 && c2 >= 1 && c3 >= 1);
         star[__ldg(star_ptr + e.x) + c0 - 1] = base + 0;
         star[__ldg(star_ptr + e.y) + c1 - 1] = base + 1;
         star[__ldg(star_ptr + e.z) + c2 - 1] = base + 2;
@@ -73,7 +74,8 @@ __device__ __forceinline__ unsigned hash64(unsigned long long k) {
 
 __device__ __forceinline__ int edge_slot_insert(int32_t* key, unsigned mask, int32_t b) {
     unsigned h = bucket(hash32((uint32_t)b), mask);
-    for (;;) {
+    for (unsigned probe = 0;; ++probe) {
+        PHG_CHECK(probe <= mask);
         const int32_t old = atomicCAS(key + h, -1, b);
         if (old == -1 || old == b) return (int)h;
         h = (h + 1) & mask;
@@ -86,7 +88,8 @@ __device__ __forceinline__ int edge_slot_find(const int32_t* key, unsigned mask,
 }
 __device__ __forceinline__ int face_slot_insert(unsigned long long* key, unsigned mask, unsigned long long k) {
     unsigned h = bucket(hash64(k), mask);
-    for (;;) {
+    for (unsigned probe = 0;; ++probe) {
+        PHG_CHECK(probe <= mask);
         const unsigned long long old = atomicCAS(key + h, ~0ull, k);
         if (old == ~0ull || old == k) return (int)h;
         h = (h + 1) & mask;
@@ -388,7 +391,8 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             if (j < ne_l) {
                 const int2 c = el[j];
                 unsigned h = bucket(hash32((uint32_t)c.x), mask);
-                for (;;) {
+                for (unsigned probe = 0;; ++probe) {
+                    PHG_CHECK(probe <= mask);
                     const int32_t old = atomicCAS(ekey + h, -1, c.x);
                     if (old == -1 || old == c.x) break;
                     h = (h + 1) & mask;
@@ -400,7 +404,8 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                 const int4 c = fl[j];
                 const unsigned long long key = (unsigned long long)c.x << 32 | (uint32_t)c.y;
                 unsigned h = bucket(hash64(key), mask);
-                for (;;) {
+                for (unsigned probe = 0;; ++probe) {
+                    PHG_CHECK(probe <= mask);
                     const unsigned long long old = atomicCAS(fkey + h, ~0ull, key);
                     if (old == ~0ull || old == key) break;
                     h = (h + 1) & mask;
@@ -416,7 +421,10 @@ __global__ void __launch_bounds__(32 * kFastWarps)
         for (int r = 0; r < R; ++r) {
             if (E > 1 && 32 * r >= nl_max) break;  // warp-uniform: only the rounds in use
             const int j = lane + 32 * r;
-            if (eh[r] >= 0) edge_first[el[j].y] = eval[eh[r]];
+            if (eh[r] >= 0) {
+                PHG_CHECK(eval[eh[r]] <= el[j].y && eval[eh[r]] >= 0);  // the first occurrence is not later
+                edge_first[el[j].y] = eval[eh[r]];
+            }
             if (fh[r] >= 0) {
                 const int h = fh[r];
                 const int32_t slot = fl[j].z;
@@ -695,6 +703,7 @@ __global__ void __launch_bounds__(256)
                 ++id;
             } else {
                 // rank of slot f among the first-occurrence slots of its element
+                PHG_CHECK(f >= 0 && f < (int32_t)s);
                 const int64_t g = f / 6;
                 const uint32_t below = (1u << (f - 6 * g)) - 1u;
                 const unsigned long long w = (unsigned long long)__ldg(edge_off + g);
@@ -736,6 +745,7 @@ __global__ void __launch_bounds__(256)
                 // the owner is slot `mate` of an earlier element g: its rank
                 // among g's owned slots (sigma = -1: opposite orientation,
                 // checked in star_groups)
+                PHG_CHECK(mate >= 0 && mate < s);
                 const int64_t g = mate >> 2;
                 const uint32_t below = (1u << (mate & 3)) - 1u;
                 const unsigned long long w = (unsigned long long)__ldg(face_off + g);

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kRefBlock)
             const int32_t first = fs[k];
             const int32_t id = os[k];
             const int64_t node = nc + first / 6 + 1 + id;
+            PHG_CHECK(first >= 0 && first <= (int32_t)s && id >= 0 && node < nc + t + 1 + (uint32_t)edge_off[t] + 6);
             mid[k] = (int32_t)node;
             if (first == (int32_t)s) {
                 const int a = k < 3 ? 0 : (k < 5 ? 1 : 2);

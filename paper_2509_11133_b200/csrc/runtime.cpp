@@ -379,7 +379,10 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
     phg_cg_state hs{};
     phg_cg_state* pinned = nullptr;
     check(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(phg_cg_state)), "pinned alloc");
-    const int batch = l < 200000 ? 32 : 16;
+    // iterations per graph launch / host poll: a poll (D2H + stream sync +
+    // relaunch) costs ~20-30 us, so small systems batch more; iterations past
+    // convergence are no-op launches (a few us each)
+    const int batch = l < 200000 ? 64 : (l < 8000000 ? 32 : 16);
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     try {
