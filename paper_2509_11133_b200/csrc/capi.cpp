@@ -12,6 +12,7 @@
 #include <cstring>
 #include <fstream>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <sstream>
 #include <string>
@@ -19,6 +20,8 @@
 
 #include "phfem.h"
 #include "phfem_ext.h"
+#include "phfem_cxx/analysis.hpp"
+#include "phfem_cxx/solver.hpp"
 #include "runtime.hpp"
 
 using namespace phb;
@@ -141,8 +144,55 @@ std::string stats_json(const std::string& method, int64_t n, int64_t l, int64_t 
 
 }  // namespace
 
+// Workspaces (connectivity, system, refinement target) of destroyed mesh
+// handles, handed to the next handle's pipeline pass: a stream of meshes (the
+// end-to-end path, one handle per mesh) then allocates nothing per mesh in
+// the middle of a pass, like repeated passes on one handle.  All their device
+// work is ordered on the library stream, so reuse is safe.
+template <class T>
+struct Recycle {
+    std::mutex mu;
+    std::vector<std::shared_ptr<T>> spare;
+    std::shared_ptr<T> take() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (spare.empty()) return std::make_shared<T>();
+        auto p = std::move(spare.back());
+        spare.pop_back();
+        return p;
+    }
+    void give(std::shared_ptr<T>& p) {
+        if (p && p.use_count() == 1) {
+            std::lock_guard<std::mutex> lk(mu);
+            if (spare.empty()) spare.push_back(std::move(p));
+        }
+        p.reset();
+    }
+};
+Recycle<Connectivity>& conn_pool() {
+    static Recycle<Connectivity> r;
+    return r;
+}
+Recycle<System>& sys_pool() {
+    static Recycle<System> r;
+    return r;
+}
+Recycle<MeshData>& child_pool() {
+    static Recycle<MeshData> r;
+    return r;
+}
+
 // Mesh handle: device mesh + lazily built connectivity and system caches.
 struct phfem_mesh {
+    ~phfem_mesh() {
+        try {
+            if (conn) conn->has_edges = conn->has_faces = false;
+            if (sys) sys->problem = -1;
+            conn_pool().give(conn);
+            sys_pool().give(sys);
+            child_pool().give(scratch_child);
+        } catch (...) {
+        }
+    }
     // the mesh; an asynchronous upload completes on first access
     mutable std::shared_ptr<MeshData> data_;
     std::shared_ptr<MeshData>& data() const {
@@ -224,7 +274,38 @@ phfem_solution* do_solve(phfem_mesh* m, int problem, const std::string& method, 
     sol->n = sys.n;
     sol->l = sys.l;
     sol->peak_dim = peak_dim_override > 0 ? peak_dim_override : sys.l;
-    solve_schur(*m->data(), *m->coef, *snapshot_conn, sys, problem, tol, max_iter, method, sol->res);
+    if (method == "direct") {
+        // the reference's global route (solver.cpp:192-244) through the C++
+        // API: the builtin problem's host data, assemble_system, solve_direct
+        // (block inverses, device transpose and spgemms, CSR PCG)
+        const HostMesh h = to_host(*m->data());
+        phfem::Mesh hm;
+        hm.level = h.level;
+        for (size_t i = 0; i < h.coords.size(); i += 3)
+            hm.coords.emplace_back(h.coords[i], h.coords[i + 1], h.coords[i + 2]);
+        for (size_t i = 0; i < h.tets.size(); i += 4)
+            hm.tetra.push_back({h.tets[i], h.tets[i + 1], h.tets[i + 2], h.tets[i + 3]});
+        for (size_t i = 0; i < h.db.size(); i += 3) hm.dirichlet_faces.push_back({h.db[i], h.db[i + 1], h.db[i + 2]});
+        for (size_t i = 0; i < h.nb.size(); i += 3) hm.neumann_faces.push_back({h.nb[i], h.nb[i + 1], h.nb[i + 2]});
+        const phfem::ManufacturedProblem prob = problem == 0   ? phfem::manufactured_problem()
+                                                : problem == 1 ? phfem::linear_patch_problem()
+                                                               : phfem::zero_problem();
+        const phfem::FaceTable ft = phfem::build_face_table(hm);
+        const phfem::LinearSystem ls = phfem::assemble_system(hm, ft, prob.data);
+        phfem::SolverOptions opt;
+        opt.tol = tol;
+        opt.max_iter = max_iter;
+        const phfem::Solution hs = phfem::solve_direct(ls, opt);
+        sol->res.u.upload(hs.u.data(), (int64_t)hs.u.size());
+        sol->res.lambda.upload(hs.lambda.data(), (int64_t)hs.lambda.size());
+        sol->res.iterations = hs.stats.iterations;
+        sol->res.residual = hs.stats.residual;
+        sol->res.constraint_residual = hs.stats.constraint_residual;
+        sol->res.seconds = hs.stats.seconds;
+        sol->res.converged = sol->res.accepted = true;
+    } else {
+        solve_schur(*m->data(), *m->coef, *snapshot_conn, sys, problem, tol, max_iter, method, sol->res);
+    }
     sol->stats = stats_json(method, sol->n, sol->l, sol->res.iterations, sol->res.residual,
                             sol->res.constraint_residual, sol->res.seconds, workers, sol->peak_dim);
     return sol.release();
@@ -853,8 +934,8 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
         total.start();
         // rebuild everything; reuse the previous pass's device memory when no
         // solution snapshot shares it
-        auto c = (mesh->conn && mesh->conn.use_count() == 1) ? mesh->conn : std::make_shared<Connectivity>();
-        auto s = (mesh->sys && mesh->sys.use_count() == 1) ? mesh->sys : std::make_shared<System>();
+        auto c = (mesh->conn && mesh->conn.use_count() == 1) ? mesh->conn : conn_pool().take();
+        auto s = (mesh->sys && mesh->sys.use_count() == 1) ? mesh->sys : sys_pool().take();
         mesh->invalidate();
         build_connectivity(*mesh->data(), *c, true, &st);
         mesh->conn = c;
@@ -864,7 +945,7 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
         }
         int64_t ne_child = 0;
         if (do_refine) {
-            if (!mesh->scratch_child) mesh->scratch_child = std::make_shared<MeshData>();
+            if (!mesh->scratch_child) mesh->scratch_child = child_pool().take();
             auto child = refine_mesh(*mesh->data(), *c, nullptr, &st, mesh->scratch_child);
             ne_child = child->ne;
         }
