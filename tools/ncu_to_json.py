@@ -1,9 +1,11 @@
 """Extract per-kernel facts from ncu --set full captures into
 profiles/ncu_kernels.json (read by bench.py for roofline.traffic).
 
-usage: python tools/ncu_to_json.py OUT.json REP.ncu-rep[=profiles/summary.txt] ...
+usage: python tools/ncu_to_json.py OUT.json [--config=NAME] REP.ncu-rep[=profiles/summary.txt] ...
 Each kernel keeps its first launch in the capture; names are shortened to
-`name<T>` (namespace and argument list dropped).
+`name<T>` (namespace and argument list dropped).  --config tags the
+following captures with the workload they ran (bench.py only uses a flop
+count captured on its own config).
 """
 import csv
 import json
@@ -97,10 +99,16 @@ def main():
             data = json.load(f)
     except (OSError, ValueError):
         data = {}
+    config = None
     for arg in sys.argv[2:]:
+        if arg.startswith("--config="):
+            config = arg.split("=", 1)[1]
+            continue
         rep, _, src = arg.partition("=")
         for k, v in facts(rep).items():
             v["source"] = src or rep
+            if config:
+                v["config"] = config
             data[k] = v
     with open(out, "w") as f:
         json.dump(data, f, indent=1, sort_keys=True)
