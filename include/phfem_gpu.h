@@ -110,6 +110,13 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
                           const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
                           int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
                           void* stream);
+/* The child of a red refinement (refine_conn.cu): edge_first [6 x 12 n] and
+ * slot_mate [4 x 12 n] (may be NULL) of the child mesh in closed form from
+ * the parent's tets [4 n], edge_of_slot, edge_first, slot_mate and nEd;
+ * a0 is scratch [2 nEd]. */
+int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge_of_slot,
+                             const int32_t* edge_first, const int32_t* slot_mate, int64_t ned,
+                             int32_t* a0, int32_t* ef_out, int32_t* sm_out, void* stream);
 /* a star listed by star_groups as too large for shared memory (defer_list
  * + 2 nC, count defer_count[2], PHG_ERR_VALENCE set): tables of capacity
  * cap (power of two > 3 m) in global scratch [20 cap bytes] */

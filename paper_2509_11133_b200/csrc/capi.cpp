@@ -8,6 +8,7 @@
 // connectivity so they survive later refinement (capi.cpp:87-93, 202).  Here
 // the snapshot shares the immutable device buffers by reference count.
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -357,6 +358,14 @@ int phfem_mesh_refine(phfem_mesh* mesh, phfem_refine_times* times) {
         Connectivity& c = const_cast<Connectivity&>(mesh->edges());
         const int64_t ned = c.ned, ne = mesh->data()->ne;
         auto child = refine_mesh(*mesh->data(), c, &mesh->last_map);
+        if (c.has_faces && !std::getenv("PHG_NO_REFINED_CONN")) {
+            // keep the parent's tables for the child's closed-form grouping
+            // (its own parent link is no longer needed)
+            child->parent_mesh = mesh->data();
+            child->parent_conn = mesh->conn;
+            mesh->data()->parent_mesh.reset();
+            mesh->data()->parent_conn.reset();
+        }
         mesh->map_ned = ned;
         mesh->map_ne = ne;
         mesh->data() = child;

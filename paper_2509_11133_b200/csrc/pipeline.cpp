@@ -140,9 +140,22 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(3 * (nc > 0 ? nc : 1));
     w.big_count.alloc(3);
-    check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr,
-                                w.big_list.p, w.big_count.p, w.err.p, SV()),
-          "star groups");
+    // a child of a red refinement whose parent kept its full tables: the
+    // grouping in closed form (refine_conn.cu), else per-vertex hashing
+    const Connectivity* pc = m.parent_conn.get();
+    const bool refined = pc && m.parent_mesh && pc->has_faces && 12 * m.parent_mesh->ne == ne;
+    if (refined) {
+        w.a0.alloc(2 * pc->ned + 2);
+        check(phfem_gpu_refined_groups(m.parent_mesh->ne, m.parent_mesh->tets.p, pc->edge_of_slot.p, pc->edge_first.p,
+                                       pc->slot_mate.p, pc->ned, w.a0.p, c.edge_first.p,
+                                       faces ? c.slot_mate.p : nullptr, SV()),
+              "refined groups");
+        w.err.fill_bytes(0xff);
+    } else {
+        check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                    faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.err.p, SV()),
+              "star groups");
+    }
     if (st) st->span(&st->groups, t0);
     // 3. numbering: per-element counts, scans, ids, remaining slots
     if (st) t0 = st->mark();

@@ -1,0 +1,211 @@
+// Connectivity of a red-refined mesh in closed form from its parent's tables
+// (no vertex star, no hashing): the child's first-occurrence edge slots
+// (edge_first) and face mates (slot_mate), one thread per parent element
+// writing the 12 children's 72 edge and 48 face slots.  The rest of the
+// numbering (offsets, ids, classification) is the generic pipeline's.
+//
+// Children of parent t = (i, j, k, l) with midpoints m_ab and centroid c
+// (refine.cpp:58-61): C0 = (i ij ik il) at index t, C1..C11 at
+// nE + 11 t + q - 1.  Child edges are of three kinds:
+//   V  (a, m_ab): only in the corner children at a.  First occurrence: C0 of
+//      the first parent containing edge ab whose vertex 0 is a (A0 table),
+//      else the corner child at a of the first parent containing ab (the
+//      parent's first-occurrence element of ab);
+//   F  (m_ab, m_ac) inside parent face abc: C0 of the first of the face's
+//      (one or two) parents whose vertex 0 is a, else the corner child at a
+//      of the face's owner (lower) parent;
+//   C  (m_ab, c): only in t's centroid children, first in C4 / C5 / C6.
+// Child faces are either shared by two children of the same parent (fixed
+// table) or sub-triangles of a parent face, whose mate is the corresponding
+// child of the parent across that face (or none on the boundary).
+// tools/refined_conn_proto.py states the same rules in Python and checks
+// them against the generic path; the tables below were generated from it.
+#include <climits>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace {
+
+using namespace phg;
+
+// [q][kk] = {kind, a, b, c}: kind 0 V (corner a, other end b), 1 F (shared
+// corner a, other corners b, c), 2 C (first in child a, local edge b)
+__constant__ signed char kREdge[12][6][4] = {
+    {{0, 0, 1, 0}, {0, 0, 2, 0}, {0, 0, 3, 0}, {1, 0, 1, 2}, {1, 0, 1, 3}, {1, 0, 2, 3}},
+    {{0, 1, 2, 0}, {0, 1, 0, 0}, {0, 1, 3, 0}, {1, 1, 2, 0}, {1, 1, 2, 3}, {1, 1, 0, 3}},
+    {{0, 2, 0, 0}, {0, 2, 1, 0}, {0, 2, 3, 0}, {1, 2, 0, 1}, {1, 2, 0, 3}, {1, 2, 1, 3}},
+    {{0, 3, 2, 0}, {0, 3, 1, 0}, {0, 3, 0, 0}, {1, 3, 2, 1}, {1, 3, 2, 0}, {1, 3, 1, 0}},
+    {{1, 0, 1, 2}, {1, 0, 1, 3}, {2, 4, 2, 0}, {1, 0, 2, 3}, {2, 4, 4, 0}, {2, 4, 5, 0}},
+    {{1, 1, 2, 0}, {1, 1, 2, 3}, {2, 5, 2, 0}, {1, 1, 0, 3}, {2, 4, 2, 0}, {2, 5, 5, 0}},
+    {{1, 2, 0, 1}, {1, 2, 0, 3}, {2, 4, 4, 0}, {1, 2, 1, 3}, {2, 5, 2, 0}, {2, 6, 5, 0}},
+    {{1, 3, 2, 1}, {1, 3, 2, 0}, {2, 6, 5, 0}, {1, 3, 1, 0}, {2, 5, 5, 0}, {2, 4, 5, 0}},
+    {{1, 1, 0, 2}, {1, 0, 1, 2}, {2, 4, 2, 0}, {1, 2, 1, 0}, {2, 5, 2, 0}, {2, 4, 4, 0}},
+    {{1, 2, 0, 3}, {1, 0, 2, 3}, {2, 4, 4, 0}, {1, 3, 2, 0}, {2, 6, 5, 0}, {2, 4, 5, 0}},
+    {{1, 0, 1, 3}, {1, 1, 0, 3}, {2, 4, 2, 0}, {1, 3, 0, 1}, {2, 4, 5, 0}, {2, 5, 5, 0}},
+    {{1, 2, 3, 1}, {1, 3, 2, 1}, {2, 6, 5, 0}, {1, 1, 2, 3}, {2, 5, 2, 0}, {2, 5, 5, 0}}};
+
+// [q][kf] = {kind, a, b}: kind 0 shared inside the parent with child a,
+// local face b; 1 corner sub-triangle at corner a of parent face b; 2 middle
+// sub-triangle of parent face a
+__constant__ signed char kRFace[12][4][4] = {
+    {{1, 0, 0, 0}, {1, 0, 1, 0}, {1, 0, 2, 0}, {0, 4, 0, 0}},
+    {{1, 1, 0, 0}, {1, 1, 2, 0}, {1, 1, 3, 0}, {0, 5, 0, 0}},
+    {{1, 2, 0, 0}, {1, 2, 3, 0}, {1, 2, 1, 0}, {0, 6, 0, 0}},
+    {{1, 3, 3, 0}, {1, 3, 2, 0}, {1, 3, 1, 0}, {0, 7, 0, 0}},
+    {{0, 0, 3, 0}, {0, 10, 2, 0}, {0, 8, 1, 0}, {0, 9, 1, 0}},
+    {{0, 1, 3, 0}, {0, 11, 3, 0}, {0, 8, 2, 0}, {0, 10, 1, 0}},
+    {{0, 2, 3, 0}, {0, 9, 2, 0}, {0, 8, 3, 0}, {0, 11, 2, 0}},
+    {{0, 3, 3, 0}, {0, 9, 3, 0}, {0, 11, 1, 0}, {0, 10, 3, 0}},
+    {{2, 0, 0, 0}, {0, 4, 2, 0}, {0, 5, 2, 0}, {0, 6, 2, 0}},
+    {{2, 1, 0, 0}, {0, 4, 3, 0}, {0, 6, 1, 0}, {0, 7, 1, 0}},
+    {{2, 2, 0, 0}, {0, 5, 3, 0}, {0, 4, 1, 0}, {0, 7, 3, 0}},
+    {{2, 3, 0, 0}, {0, 7, 2, 0}, {0, 6, 3, 0}, {0, 5, 1, 0}}};
+
+// position of midpoint m_qx in corner child q (x != q)
+__constant__ signed char kRPos[4][4] = {{-1, 1, 2, 3}, {2, -1, 1, 3}, {1, 2, -1, 3}, {3, 2, 1, -1}};
+
+// local face k excludes local vertex kExcl[k]; the same map sends a vertex
+// to the face that excludes it
+__device__ __forceinline__ int excl(int k) { return k == 0 ? 3 : (k == 3 ? 0 : k); }
+
+// A0 entries start as 0x7f7f7f7f (byte memset): no parent with that vertex 0
+constexpr int32_t kNoParent = 0x7f7f7f7f;
+
+__device__ __forceinline__ int64_t child(int64_t t, int q, int64_t n) { return q == 0 ? t : n + 11 * t + q - 1; }
+
+__device__ __forceinline__ int idx_of(const int4& p, int32_t g) {
+    return p.x == g ? 0 : (p.y == g ? 1 : (p.z == g ? 2 : 3));
+}
+
+__device__ __forceinline__ int ledge(int a, int b) { return edge_index(a, b); }
+
+// A0[2e + w]: the first parent with vertex 0 = the smaller (w = 0) / larger
+// (w = 1) endpoint of edge e, from the slots (t, k < 3) whose local pair
+// contains vertex 0
+__global__ void a0_k(int64_t ne, const int32_t* __restrict__ tets, const int32_t* __restrict__ edge_of_slot,
+                     int32_t* __restrict__ a0) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 p = ldtet(tets, t);
+        const int32_t o[3] = {p.y, p.z, p.w};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int32_t e = edge_of_slot[6 * t + k];
+            atomicMin(a0 + 2 * (int64_t)e + (p.x < o[k] ? 0 : 1), (int32_t)t);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128)
+    refined_groups_k(int64_t n, const int32_t* __restrict__ tets, const int32_t* __restrict__ edge_of_slot,
+                     const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
+                     const int32_t* __restrict__ a0, int32_t* __restrict__ ef_out, int32_t* __restrict__ sm_out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int4 pt = ldtet(tets, t);
+    const int32_t pv[4] = {pt.x, pt.y, pt.z, pt.w};
+    int32_t eos[6], ef[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        eos[k] = __ldg(edge_of_slot + 6 * t + k);
+        ef[k] = __ldg(edge_first + 6 * t + k);
+    }
+    const int4 sm4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+    const int32_t sm[4] = {sm4.x, sm4.y, sm4.z, sm4.w};
+    // the parents across t's faces
+    int4 mt[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
+    for (int q = 0; q < 12; ++q) {
+        const int64_t cq = child(t, q, n);
+        int32_t out[6];
+#pragma unroll
+        for (int kk = 0; kk < 6; ++kk) {
+            const int kind = kREdge[q][kk][0], a = kREdge[q][kk][1], b = kREdge[q][kk][2], c = kREdge[q][kk][3];
+            int64_t first;
+            if (kind == 2) {
+                first = 6 * child(t, a, n) + b;
+            } else if (kind == 0) {
+                const int32_t ga = pv[a], gb = pv[b];
+                const int le = ledge(a, b);
+                const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
+                if (ts != kNoParent) {
+                    const int4 ps = ts == t ? pt : ldtet(tets, ts);
+                    first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
+                } else {
+                    const int64_t t1 = ef[le] / 6;
+                    const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
+                    const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
+                    first = 6 * child(t1, qa, n) + kRPos[qa][qb] - 1;
+                }
+            } else {
+                // parent face abc: the face of t that excludes the fourth
+                // corner, and the parent across it
+                const int d = 6 - a - b - c;
+                const int kF = excl(d);
+                const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
+                const int32_t ms = sm[kF];
+                const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
+                const int4 p2 = mt[kF];
+                const bool t_first = t2 < 0 || t < t2;
+                const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
+                const int4 plo = t_first ? pt : p2, phi = t_first ? p2 : pt;
+                if (plo.x == ga) {
+                    first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
+                } else if (hi >= 0 && phi.x == ga) {
+                    first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
+                } else {
+                    const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
+                    first = 6 * child(lo, qa, n) + ledge(kRPos[qa][qb], kRPos[qa][qc]);
+                }
+            }
+            out[kk] = (int32_t)first;
+        }
+        int2* o2 = reinterpret_cast<int2*>(ef_out + 6 * cq);
+        o2[0] = make_int2(out[0], out[1]);
+        o2[1] = make_int2(out[2], out[3]);
+        o2[2] = make_int2(out[4], out[5]);
+        if (!sm_out) continue;
+        int32_t fo[4];
+#pragma unroll
+        for (int kf = 0; kf < 4; ++kf) {
+            const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
+            int64_t mate;
+            if (kind == 0) {
+                mate = 4 * child(t, a, n) + b;
+            } else {
+                const int kF = kind == 1 ? b : a;
+                const int32_t ms = sm[kF];
+                if (ms < 0) {
+                    mate = -1;
+                } else {
+                    const int64_t t2 = ms >> 2;
+                    const int kF2 = ms & 3;
+                    if (kind == 2) {
+                        mate = 4 * child(t2, 8 + kF2, n);
+                    } else {
+                        const int a2 = idx_of(mt[kF], pv[a]);
+                        mate = 4 * child(t2, a2, n) + excl(kRPos[a2][excl(kF2)]);
+                    }
+                }
+            }
+            fo[kf] = (int32_t)mate;
+        }
+        reinterpret_cast<int4*>(sm_out)[cq] = make_int4(fo[0], fo[1], fo[2], fo[3]);
+    }
+}
+
+}  // namespace
+
+extern "C" int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge_of_slot,
+                                        const int32_t* edge_first, const int32_t* slot_mate, int64_t ned,
+                                        int32_t* a0, int32_t* ef_out, int32_t* sm_out, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) return 0;
+    cudaMemsetAsync(a0, 0x7f, sizeof(int32_t) * 2 * (size_t)(ned > 0 ? ned : 1), s);
+    a0_k<<<grid_for(n, 256), 256, 0, s>>>(n, tets, edge_of_slot, a0);
+    refined_groups_k<<<grid_for(n, 128), 128, 0, s>>>(n, tets, edge_of_slot, edge_first, slot_mate, a0, ef_out,
+                                                      sm_out);
+    phg::count_launches(2);
+    return (int)cudaGetLastError();
+}

@@ -153,9 +153,16 @@ struct PendingUpload {
     ~PendingUpload();
 };
 
+struct Connectivity;
+
 struct MeshData {
     int64_t nc = 0, ne = 0, nd = 0, nn = 0;
     int level = 0;
+    // the mesh this one was red-refined from, with its full connectivity:
+    // the child's edge / face grouping then follows in closed form
+    // (refine_conn.cu) instead of the vertex-star hashing
+    std::shared_ptr<MeshData> parent_mesh;
+    std::shared_ptr<Connectivity> parent_conn;
     DBuf<double> coords;  // [3 nC]
     DBuf<int32_t> tets;   // [4 nE]
     DBuf<int32_t> db, nb; // [3 nD], [3 nN]
@@ -181,7 +188,7 @@ struct Coefs {
 // transient device buffers of one connectivity / refinement / assembly pass,
 // kept with their owner so repeated passes reuse them
 struct Work {
-    DBuf<int32_t> cnt, big_list, big_count, packed, redo;
+    DBuf<int32_t> cnt, big_list, big_count, packed, redo, a0;
     DBuf<double> face_bval;  // boundary faces' b_D / Neumann terms (assembly)
     DBuf<int64_t> face_off;
     DBuf<unsigned char> scratch;
