@@ -117,6 +117,14 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
 int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge_of_slot,
                              const int32_t* edge_first, const int32_t* slot_mate, int64_t ned,
                              int32_t* a0, int32_t* ef_out, int32_t* sm_out, void* stream);
+/* classification (connectivity.cpp:120-160) of a refined mesh's lists: the
+ * child entries' faces from the parent's classification (nd, nn, db, nb,
+ * entry_face, face_slots, tets of the PARENT, n = parent nE), the child's
+ * face_of_slot / face_slots; claims and errors as phfem_gpu_classify */
+int phfem_gpu_refined_classify(int64_t nd, int64_t nn, const int32_t* db, const int32_t* nb,
+                               const int32_t* p_entry_face, const int32_t* p_face_slots, const int32_t* p_tets,
+                               int64_t n, const int32_t* face_of_slot, const int32_t* face_slots,
+                               uint32_t* claim, int32_t* entry_face, unsigned long long* err, void* stream);
 /* a star listed by star_groups as too large for shared memory (defer_list
  * + 2 nC, count defer_count[2], PHG_ERR_VALENCE set): tables of capacity
  * cap (power of two > 3 m) in global scratch [20 cap bytes] */
@@ -186,6 +194,12 @@ int phfem_gpu_refine_boundary(int64_t nf, const int32_t* faces, int64_t list_bas
                               const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                               const int32_t* edge_first, const int32_t* edge_of_slot,
                               int32_t* out, unsigned long long* err, void* stream);
+/* the same split for a classified mesh: midpoints through the owner slot of
+ * each entry's face (entry_face + list_base, face_slots), no star */
+int phfem_gpu_refine_boundary_owned(int64_t nf, const int32_t* faces, int64_t list_base, int64_t nc,
+                                    const int32_t* entry_face, const int32_t* face_slots, const int32_t* tets,
+                                    const int32_t* edge_first, const int32_t* edge_of_slot, int32_t* out,
+                                    void* stream);
 
 /* ------------------------------------------------- assembly + condensation */
 /* Upload tet_rule(5) and tet_rule(9) (quadrature.cpp:36-62), built on the

@@ -116,6 +116,21 @@ void group_huge_stars(const MeshData& m, Connectivity& c, bool faces) {
 
 // ------------------------------------------------------------ connectivity
 
+void build_star(const MeshData& m, Connectivity& c, Stages* st) {
+    Work& w = c.w;
+    cudaEvent_t t0 = st ? st->mark() : nullptr;
+    if (w.scratch.cap < (int64_t)phfem_gpu_scan_scratch(m.nc)) w.scratch.alloc((int64_t)phfem_gpu_scan_scratch(m.nc));
+    w.cnt.alloc(m.nc);
+    w.cnt.zero();
+    check(phfem_gpu_star_count(m.tets.p, m.ne, w.cnt.p, SV()), "star count");
+    c.star_ptr.alloc(m.nc + 1);
+    check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, m.nc, w.scratch.p, SV()), "star scan");
+    c.star.alloc(4 * m.ne);
+    check(phfem_gpu_star_fill(m.tets.p, m.ne, c.star_ptr.p, w.cnt.p, c.star.p, SV()), "star fill");
+    if (st) st->span(&st->star, t0);
+    c.has_star = true;
+}
+
 void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st, bool classify) {
     const int64_t nc = m.nc, ne = m.ne;
     Work& w = c.w;
@@ -124,26 +139,22 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     reset_err(w);
     w.scratch.alloc((int64_t)std::max(phfem_gpu_scan_scratch(std::max<int64_t>({nc, ne, 4 * ne})),
                                       phfem_gpu_element_offsets_scratch(ne)));
+    // a child of a red refinement whose parent kept its full tables: the
+    // grouping (and, with faces, the classification) in closed form
+    // (refine_conn.cu), else per-vertex hashing through the star
+    const Connectivity* pc = m.parent_conn.get();
+    const MeshData* pm = m.parent_mesh.get();
+    const bool refined = pc && pm && pc->has_faces && 12 * pm->ne == ne;
+    const bool refined_cls = refined && faces && classify && m.nd == 4 * pm->nd && m.nn == 4 * pm->nn;
     // 1. vertex star (CSR by vertex)
-    if (st) t0 = st->mark();
-    w.cnt.alloc(nc);
-    w.cnt.zero();
-    check(phfem_gpu_star_count(m.tets.p, ne, w.cnt.p, SV()), "star count");
-    c.star_ptr.alloc(nc + 1);
-    check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, nc, w.scratch.p, SV()), "star scan");
-    c.star.alloc(4 * ne);
-    check(phfem_gpu_star_fill(m.tets.p, ne, c.star_ptr.p, w.cnt.p, c.star.p, SV()), "star fill");
-    if (st) st->span(&st->star, t0);
+    c.has_star = false;
+    if (!refined_cls) build_star(m, c, st);
     // 2. per-vertex grouping of edges and faces
     if (st) t0 = st->mark();
     c.edge_first.alloc(6 * ne);
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(3 * (nc > 0 ? nc : 1));
     w.big_count.alloc(3);
-    // a child of a red refinement whose parent kept its full tables: the
-    // grouping in closed form (refine_conn.cu), else per-vertex hashing
-    const Connectivity* pc = m.parent_conn.get();
-    const bool refined = pc && m.parent_mesh && pc->has_faces && 12 * m.parent_mesh->ne == ne;
     if (refined) {
         w.a0.alloc(2 * pc->ned + 2);
         check(phfem_gpu_refined_groups(m.parent_mesh->ne, m.parent_mesh->tets.p, pc->edge_of_slot.p, pc->edge_first.p,
@@ -210,9 +221,16 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     w.claim.alloc(nf);
     w.claim.fill_bytes(0xff);
     c.entry_face.alloc(m.nd + m.nn);
-    check(phfem_gpu_classify(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
-                             c.face_slots.p, w.claim.p, c.entry_face.p, w.err.p, SV()),
-          "classify");
+    if (refined_cls) {
+        check(phfem_gpu_refined_classify(pm->nd, pm->nn, pm->db.p, pm->nb.p, pc->entry_face.p, pc->face_slots.p,
+                                         pm->tets.p, pm->ne, c.face_of_slot.p, c.face_slots.p, w.claim.p,
+                                         c.entry_face.p, w.err.p, SV()),
+              "refined classify");
+    } else {
+        check(phfem_gpu_classify(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
+                                 c.face_slots.p, w.claim.p, c.entry_face.p, w.err.p, SV()),
+              "classify");
+    }
     check(phfem_gpu_classify_check(m.nd, m.nn, c.entry_face.p, w.claim.p, w.err.p, SV()), "classify check");
     c.face_class.alloc(nf + 16);
     w.counts.alloc(4);
@@ -271,12 +289,23 @@ std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, Refine
                            out->coords.p, out->tets.p, map ? map->midpoint.p : nullptr,
                            map ? map->centroid.p : nullptr, SV()),
           "refine");
-    check(phfem_gpu_refine_boundary(m.nd, m.db.p, 0, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
-                                    c.edge_of_slot.p, out->db.p, w.err.p, SV()),
-          "refine boundary");
-    check(phfem_gpu_refine_boundary(m.nn, m.nb.p, m.nd, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
-                                    c.edge_of_slot.p, out->nb.p, w.err.p, SV()),
-          "refine boundary");
+    if (c.has_faces) {
+        // classified: each list entry's face and its owner element are known
+        check(phfem_gpu_refine_boundary_owned(m.nd, m.db.p, 0, m.nc, c.entry_face.p, c.face_slots.p, m.tets.p,
+                                              c.edge_first.p, c.edge_of_slot.p, out->db.p, SV()),
+              "refine boundary");
+        check(phfem_gpu_refine_boundary_owned(m.nn, m.nb.p, m.nd, m.nc, c.entry_face.p, c.face_slots.p, m.tets.p,
+                                              c.edge_first.p, c.edge_of_slot.p, out->nb.p, SV()),
+              "refine boundary");
+    } else {
+        if (!c.has_star) build_star(m, c, nullptr);
+        check(phfem_gpu_refine_boundary(m.nd, m.db.p, 0, m.nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
+                                        c.edge_of_slot.p, out->db.p, w.err.p, SV()),
+              "refine boundary");
+        check(phfem_gpu_refine_boundary(m.nn, m.nb.p, m.nd, m.nc, c.star_ptr.p, c.star.p, m.tets.p,
+                                        c.edge_first.p, c.edge_of_slot.p, out->nb.p, w.err.p, SV()),
+              "refine boundary");
+    }
     if (st) st->span(&st->refine, t0);
     auto replay = [&m](const unsigned long long* e) {
         if (e[PHG_ERR_BOUNDARY_EDGE] != kNone) {

@@ -137,6 +137,38 @@ __global__ void refine_boundary_k(int64_t nf, const int32_t* __restrict__ faces,
     }
 }
 
+
+// The same split for a mesh whose classification is done: each entry's face
+// is entry_face[list_base + f], owned by the slot (t, k), and the three
+// midpoints follow from t's edge slots (no star search).  The entries are
+// faces of the mesh, so no boundary-edge error can arise.
+__global__ void refine_boundary_owned_k(int64_t nf, const int32_t* __restrict__ faces, int64_t list_base,
+                                        int64_t nc, const int32_t* __restrict__ entry_face,
+                                        const int32_t* __restrict__ face_slots, const int32_t* __restrict__ tets,
+                                        const int32_t* __restrict__ edge_first,
+                                        const int32_t* __restrict__ edge_of_slot, int32_t* __restrict__ out) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t n1 = faces[3 * f], n2 = faces[3 * f + 1], n3 = faces[3 * f + 2];
+        const int32_t fid = __ldg(entry_face + list_base + f);
+        const int64_t t = __ldg(face_slots + 2 * (int64_t)fid) >> 2;
+        const int4 tet = ldtet(tets, t);
+        const int l1 = tet.x == n1 ? 0 : (tet.y == n1 ? 1 : (tet.z == n1 ? 2 : 3));
+        const int l2 = tet.x == n2 ? 0 : (tet.y == n2 ? 1 : (tet.z == n2 ? 2 : 3));
+        const int l3 = tet.x == n3 ? 0 : (tet.y == n3 ? 1 : (tet.z == n3 ? 2 : 3));
+        auto mid = [&](int a, int b) {
+            const int64_t s = 6 * t + edge_index(a, b);
+            return (int32_t)(nc + __ldg(edge_first + s) / 6 + 1 + __ldg(edge_of_slot + s));
+        };
+        const int32_t m12 = mid(l1, l2), m23 = mid(l2, l3), m13 = mid(l1, l3);
+        int32_t* o = out + 3 * f;
+        o[0] = n1; o[1] = m12; o[2] = m13;
+        o = out + 3 * (nf + 3 * f);
+        o[0] = n2; o[1] = m23; o[2] = m12;
+        o[3] = n3; o[4] = m13; o[5] = m23;
+        o[6] = m12; o[7] = m23; o[8] = m13;
+    }
+}
+
 }  // namespace
 
 extern "C" int phfem_gpu_refine(int64_t nc, int64_t ne, const double* coords, const int32_t* tets,
@@ -159,5 +191,16 @@ extern "C" int phfem_gpu_refine_boundary(int64_t nf, const int32_t* faces, int64
     if (nf == 0) return 0;
     refine_boundary_k<<<grid_for(nf, 128), 128, 0, (cudaStream_t)stream>>>(nf, faces, list_base, nc, star_ptr, star,
                                                                            tets, edge_first, edge_of_slot, out, err); phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_refine_boundary_owned(int64_t nf, const int32_t* faces, int64_t list_base, int64_t nc,
+                                               const int32_t* entry_face, const int32_t* face_slots,
+                                               const int32_t* tets, const int32_t* edge_first,
+                                               const int32_t* edge_of_slot, int32_t* out, void* stream) {
+    if (nf == 0) return 0;
+    refine_boundary_owned_k<<<grid_for(nf, 128), 128, 0, (cudaStream_t)stream>>>(
+        nf, faces, list_base, nc, entry_face, face_slots, tets, edge_first, edge_of_slot, out);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -96,102 +96,164 @@ __global__ void a0_k(int64_t ne, const int32_t* __restrict__ tets, const int32_t
     }
 }
 
-__global__ void __launch_bounds__(128)
+// The 12 children's rows are staged in shared memory and written out
+// coalesced: the block's C1..C11 rows are one contiguous range (nE + 11 t0
+// ...), its C0 rows another (t0 ...).  Row r of the stage is C(q) of local
+// parent lt at r = 11 lt + q - 1 (q >= 1) or 11 kRgBlock + lt (q = 0).
+constexpr int kRgBlock = 64;
+
+__device__ __forceinline__ int stage_row(int lt, int q) { return q == 0 ? 11 * kRgBlock + lt : 11 * lt + q - 1; }
+
+__global__ void __launch_bounds__(kRgBlock)
     refined_groups_k(int64_t n, const int32_t* __restrict__ tets, const int32_t* __restrict__ edge_of_slot,
                      const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
                      const int32_t* __restrict__ a0, int32_t* __restrict__ ef_out, int32_t* __restrict__ sm_out) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    const int4 pt = ldtet(tets, t);
-    const int32_t pv[4] = {pt.x, pt.y, pt.z, pt.w};
-    int32_t eos[6], ef[6];
+    __shared__ int2 s_ef[12 * kRgBlock * 3];
+    __shared__ int4 s_sm[12 * kRgBlock];
+    const int64_t t0 = (int64_t)blockIdx.x * kRgBlock;
+    const int lt = threadIdx.x;
+    const int64_t t = t0 + lt;
+    const int nb = (int)(n - t0 < kRgBlock ? n - t0 : kRgBlock);
+    if (lt < nb) {
+        const int4 pt = ldtet(tets, t);
+        const int32_t pv[4] = {pt.x, pt.y, pt.z, pt.w};
+        int32_t eos[6], ef[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) {
-        eos[k] = __ldg(edge_of_slot + 6 * t + k);
-        ef[k] = __ldg(edge_first + 6 * t + k);
-    }
-    const int4 sm4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
-    const int32_t sm[4] = {sm4.x, sm4.y, sm4.z, sm4.w};
-    // the parents across t's faces
-    int4 mt[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
-    for (int q = 0; q < 12; ++q) {
-        const int64_t cq = child(t, q, n);
-        int32_t out[6];
-#pragma unroll
-        for (int kk = 0; kk < 6; ++kk) {
-            const int kind = kREdge[q][kk][0], a = kREdge[q][kk][1], b = kREdge[q][kk][2], c = kREdge[q][kk][3];
-            int64_t first;
-            if (kind == 2) {
-                first = 6 * child(t, a, n) + b;
-            } else if (kind == 0) {
-                const int32_t ga = pv[a], gb = pv[b];
-                const int le = ledge(a, b);
-                const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
-                if (ts != kNoParent) {
-                    const int4 ps = ts == t ? pt : ldtet(tets, ts);
-                    first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
-                } else {
-                    const int64_t t1 = ef[le] / 6;
-                    const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
-                    const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
-                    first = 6 * child(t1, qa, n) + kRPos[qa][qb] - 1;
-                }
-            } else {
-                // parent face abc: the face of t that excludes the fourth
-                // corner, and the parent across it
-                const int d = 6 - a - b - c;
-                const int kF = excl(d);
-                const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
-                const int32_t ms = sm[kF];
-                const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
-                const int4 p2 = mt[kF];
-                const bool t_first = t2 < 0 || t < t2;
-                const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
-                const int4 plo = t_first ? pt : p2, phi = t_first ? p2 : pt;
-                if (plo.x == ga) {
-                    first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
-                } else if (hi >= 0 && phi.x == ga) {
-                    first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
-                } else {
-                    const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
-                    first = 6 * child(lo, qa, n) + ledge(kRPos[qa][qb], kRPos[qa][qc]);
-                }
-            }
-            out[kk] = (int32_t)first;
+        for (int k = 0; k < 6; ++k) {
+            eos[k] = __ldg(edge_of_slot + 6 * t + k);
+            ef[k] = __ldg(edge_first + 6 * t + k);
         }
-        int2* o2 = reinterpret_cast<int2*>(ef_out + 6 * cq);
-        o2[0] = make_int2(out[0], out[1]);
-        o2[1] = make_int2(out[2], out[3]);
-        o2[2] = make_int2(out[4], out[5]);
-        if (!sm_out) continue;
-        int32_t fo[4];
+        const int4 sm4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        const int32_t sm[4] = {sm4.x, sm4.y, sm4.z, sm4.w};
+        // the parents across t's faces
+        int4 mt[4];
 #pragma unroll
-        for (int kf = 0; kf < 4; ++kf) {
-            const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
-            int64_t mate;
-            if (kind == 0) {
-                mate = 4 * child(t, a, n) + b;
-            } else {
-                const int kF = kind == 1 ? b : a;
-                const int32_t ms = sm[kF];
-                if (ms < 0) {
-                    mate = -1;
-                } else {
-                    const int64_t t2 = ms >> 2;
-                    const int kF2 = ms & 3;
-                    if (kind == 2) {
-                        mate = 4 * child(t2, 8 + kF2, n);
+        for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
+        for (int q = 0; q < 12; ++q) {
+            int32_t out[6];
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) {
+                const int kind = kREdge[q][kk][0], a = kREdge[q][kk][1], b = kREdge[q][kk][2], c = kREdge[q][kk][3];
+                int64_t first;
+                if (kind == 2) {
+                    first = 6 * child(t, a, n) + b;
+                } else if (kind == 0) {
+                    const int32_t ga = pv[a], gb = pv[b];
+                    const int le = ledge(a, b);
+                    const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
+                    if (ts != kNoParent) {
+                        const int4 ps = ts == t ? pt : ldtet(tets, ts);
+                        first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
                     } else {
-                        const int a2 = idx_of(mt[kF], pv[a]);
-                        mate = 4 * child(t2, a2, n) + excl(kRPos[a2][excl(kF2)]);
+                        const int64_t t1 = ef[le] / 6;
+                        const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
+                        const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
+                        first = 6 * child(t1, qa, n) + kRPos[qa][qb] - 1;
+                    }
+                } else {
+                    // parent face abc: the face of t that excludes the fourth
+                    // corner, and the parent across it
+                    const int d = 6 - a - b - c;
+                    const int kF = excl(d);
+                    const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
+                    const int32_t ms = sm[kF];
+                    const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
+                    const int4 p2 = mt[kF];
+                    const bool t_first = t2 < 0 || t < t2;
+                    const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
+                    const int4 plo = t_first ? pt : p2, phi = t_first ? p2 : pt;
+                    if (plo.x == ga) {
+                        first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
+                    } else if (hi >= 0 && phi.x == ga) {
+                        first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
+                    } else {
+                        const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
+                        first = 6 * child(lo, qa, n) + ledge(kRPos[qa][qb], kRPos[qa][qc]);
                     }
                 }
+                out[kk] = (int32_t)first;
             }
-            fo[kf] = (int32_t)mate;
+            int2* o2 = s_ef + 3 * stage_row(lt, q);
+            o2[0] = make_int2(out[0], out[1]);
+            o2[1] = make_int2(out[2], out[3]);
+            o2[2] = make_int2(out[4], out[5]);
+            if (!sm_out) continue;
+            int32_t fo[4];
+#pragma unroll
+            for (int kf = 0; kf < 4; ++kf) {
+                const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
+                int64_t mate;
+                if (kind == 0) {
+                    mate = 4 * child(t, a, n) + b;
+                } else {
+                    const int kF = kind == 1 ? b : a;
+                    const int32_t ms = sm[kF];
+                    if (ms < 0) {
+                        mate = -1;
+                    } else {
+                        const int64_t t2 = ms >> 2;
+                        const int kF2 = ms & 3;
+                        if (kind == 2) {
+                            mate = 4 * child(t2, 8 + kF2, n);
+                        } else {
+                            const int a2 = idx_of(mt[kF], pv[a]);
+                            mate = 4 * child(t2, a2, n) + excl(kRPos[a2][excl(kF2)]);
+                        }
+                    }
+                }
+                fo[kf] = (int32_t)mate;
+            }
+            s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
         }
-        reinterpret_cast<int4*>(sm_out)[cq] = make_int4(fo[0], fo[1], fo[2], fo[3]);
+    }
+    __syncthreads();
+    // C1..C11: rows nE + 11 t0 + [0, 11 nb); C0: rows t0 + [0, nb)
+    int2* e1 = reinterpret_cast<int2*>(ef_out) + 3 * (n + 11 * t0);
+    for (int i = lt; i < 33 * nb; i += kRgBlock) e1[i] = s_ef[i];
+    int2* e0 = reinterpret_cast<int2*>(ef_out) + 3 * t0;
+    for (int i = lt; i < 3 * nb; i += kRgBlock) e0[i] = s_ef[33 * kRgBlock + i];
+    if (!sm_out) return;
+    int4* f1 = reinterpret_cast<int4*>(sm_out) + n + 11 * t0;
+    for (int i = lt; i < 11 * nb; i += kRgBlock) f1[i] = s_sm[i];
+    int4* f0 = reinterpret_cast<int4*>(sm_out) + t0;
+    for (int i = lt; i < nb; i += kRgBlock) f0[i] = s_sm[11 * kRgBlock + i];
+}
+
+// Classification of a refined mesh's boundary lists, which refine_mesh built
+// from the parent's (refine.cpp:88-94: row j = the corner triangle at n1,
+// rows nL + 3 j + 0/1/2 = the corner triangles at n2, n3 and the middle
+// one): parent entry j lies on the parent face entry_face[j], owned by the
+// parent slot (t, k); its four sub-triangles are faces of t's children at
+// fixed local faces (corner child a: the face without m_ad, d the vertex of t
+// off the face; middle: child 8 + k, face 0).  One thread per parent entry
+// writes the child entries' face ids and claims, as classify does.
+__global__ void refined_classify_k(int64_t nd, int64_t nn, const int32_t* __restrict__ db,
+                                   const int32_t* __restrict__ nb, const int32_t* __restrict__ p_entry_face,
+                                   const int32_t* __restrict__ p_face_slots, const int32_t* __restrict__ p_tets,
+                                   int64_t n, const int32_t* __restrict__ face_of_slot,
+                                   const int32_t* __restrict__ face_slots, uint32_t* __restrict__ claim,
+                                   int32_t* __restrict__ entry_face, unsigned long long* err) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nd + nn; j += (int64_t)gridDim.x * blockDim.x) {
+        const bool dir = j < nd;
+        const int64_t jl = dir ? j : j - nd, nl = dir ? nd : nn, base = dir ? 0 : 4 * nd;
+        const int32_t* tri = (dir ? db : nb) + 3 * jl;
+        const int32_t pf = __ldg(p_entry_face + j);
+        const int64_t t = __ldg(p_face_slots + 2 * (int64_t)pf) >> 2;
+        const int4 pt = ldtet(p_tets, t);
+        const int a1 = idx_of(pt, __ldg(tri)), a2 = idx_of(pt, __ldg(tri + 1)), a3 = idx_of(pt, __ldg(tri + 2));
+        const int d = 6 - a1 - a2 - a3;
+        const int64_t rows[4] = {base + jl, base + nl + 3 * jl, base + nl + 3 * jl + 1, base + nl + 3 * jl + 2};
+        const int64_t slots[4] = {4 * child(t, a1, n) + excl(kRPos[a1][d]), 4 * child(t, a2, n) + excl(kRPos[a2][d]),
+                                  4 * child(t, a3, n) + excl(kRPos[a3][d]), 4 * child(t, 8 + excl(d), n)};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int32_t f = __ldg(face_of_slot + slots[q]);
+            PHG_CHECK(f >= 0);
+            entry_face[rows[q]] = f;
+            atomicMin(claim + f, (uint32_t)rows[q]);
+            if (__ldg(face_slots + 2 * (int64_t)f + 1) >= 0)
+                report(err, PHG_ERR_CLASSIFY, (unsigned long long)rows[q] << 2 | 2);
+        }
     }
 }
 
@@ -204,8 +266,20 @@ extern "C" int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const in
     if (n == 0) return 0;
     cudaMemsetAsync(a0, 0x7f, sizeof(int32_t) * 2 * (size_t)(ned > 0 ? ned : 1), s);
     a0_k<<<grid_for(n, 256), 256, 0, s>>>(n, tets, edge_of_slot, a0);
-    refined_groups_k<<<grid_for(n, 128), 128, 0, s>>>(n, tets, edge_of_slot, edge_first, slot_mate, a0, ef_out,
+    refined_groups_k<<<grid_for(n, kRgBlock), kRgBlock, 0, s>>>(n, tets, edge_of_slot, edge_first, slot_mate, a0, ef_out,
                                                       sm_out);
     phg::count_launches(2);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_refined_classify(int64_t nd, int64_t nn, const int32_t* db, const int32_t* nb,
+                                          const int32_t* p_entry_face, const int32_t* p_face_slots,
+                                          const int32_t* p_tets, int64_t n, const int32_t* face_of_slot,
+                                          const int32_t* face_slots, uint32_t* claim, int32_t* entry_face,
+                                          unsigned long long* err, void* stream) {
+    if (nd + nn == 0) return 0;
+    refined_classify_k<<<grid_for(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(
+        nd, nn, db, nb, p_entry_face, p_face_slots, p_tets, n, face_of_slot, face_slots, claim, entry_face, err);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -203,6 +203,7 @@ struct Connectivity {
     // vertex star
     DBuf<int64_t> star_ptr;
     DBuf<int32_t> star;
+    bool has_star = false;  // skipped for a classified refined mesh
     // edges
     bool has_edges = false;
     int64_t ned = 0;

@@ -197,6 +197,28 @@ def test_refinement_bit_exact(oracle, goldens):
     assert c.tolist() == st["coords"] and (t + 1).tolist() == st["children"]
 
 
+@pytest.mark.parametrize("name", ["cube5", "kuhn322_mixed", "kuhn213_neumann"])
+def test_refined_chain_with_faces(oracle, name):
+    """A mesh whose faces were classified before each refinement: the child's
+    grouping, classification (refine_conn.cu) and boundary lists
+    (refine_boundary_owned) come from the parent's tables, not the star;
+    every level is compared with the oracle's generic tables."""
+    base = {"cube5": lambda: cube5(), "kuhn322_mixed": lambda: oracle.kuhn(3, 2, 2, jitter=0.2, dmask=0x5),
+            "kuhn213_neumann": lambda: oracle.kuhn(2, 1, 3, jitter=0.1, dmask=0x1)}[name]()
+    g = to_gpu(base)
+    m = base
+    for lv in range(4 if base.ne < 10 else 3):
+        check_connectivity(g, m, oracle)
+        mo = oracle.refine(m)[0]
+        g.refine()
+        mg = from_gpu(g)
+        for k in ("coords", "tets", "db", "nb"):
+            assert np.array_equal(getattr(mg, k), getattr(mo, k)), (lv, k)
+        m = mo
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, kind=0)
+
+
 def test_reference_golden_counts_levels_1_to_4(goldens):
     table = goldens["refine_counts_ne_nc_ned_nf"]["value"]
     dims = goldens["system_dims_n_l"]["value"]
