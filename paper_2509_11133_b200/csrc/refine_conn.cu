@@ -31,7 +31,7 @@ using namespace phg;
 
 // [q][kk] = {kind, a, b, c}: kind 0 V (corner a, other end b), 1 F (shared
 // corner a, other corners b, c), 2 C (first in child a, local edge b)
-__constant__ signed char kREdge[12][6][4] = {
+__device__ constexpr signed char kREdge[12][6][4] = {
     {{0, 0, 1, 0}, {0, 0, 2, 0}, {0, 0, 3, 0}, {1, 0, 1, 2}, {1, 0, 1, 3}, {1, 0, 2, 3}},
     {{0, 1, 2, 0}, {0, 1, 0, 0}, {0, 1, 3, 0}, {1, 1, 2, 0}, {1, 1, 2, 3}, {1, 1, 0, 3}},
     {{0, 2, 0, 0}, {0, 2, 1, 0}, {0, 2, 3, 0}, {1, 2, 0, 1}, {1, 2, 0, 3}, {1, 2, 1, 3}},
@@ -48,7 +48,7 @@ __constant__ signed char kREdge[12][6][4] = {
 // [q][kf] = {kind, a, b}: kind 0 shared inside the parent with child a,
 // local face b; 1 corner sub-triangle at corner a of parent face b; 2 middle
 // sub-triangle of parent face a
-__constant__ signed char kRFace[12][4][4] = {
+__device__ constexpr signed char kRFace[12][4][4] = {
     {{1, 0, 0, 0}, {1, 0, 1, 0}, {1, 0, 2, 0}, {0, 4, 0, 0}},
     {{1, 1, 0, 0}, {1, 1, 2, 0}, {1, 1, 3, 0}, {0, 5, 0, 0}},
     {{1, 2, 0, 0}, {1, 2, 3, 0}, {1, 2, 1, 0}, {0, 6, 0, 0}},
@@ -62,8 +62,12 @@ __constant__ signed char kRFace[12][4][4] = {
     {{2, 2, 0, 0}, {0, 5, 3, 0}, {0, 4, 1, 0}, {0, 7, 3, 0}},
     {{2, 3, 0, 0}, {0, 7, 2, 0}, {0, 6, 3, 0}, {0, 5, 1, 0}}};
 
-// position of midpoint m_qx in corner child q (x != q)
-__constant__ signed char kRPos[4][4] = {{-1, 1, 2, 3}, {2, -1, 1, 3}, {1, 2, -1, 3}, {3, 2, 1, -1}};
+// position of midpoint m_qx in corner child q (x != q):
+// {{-1, 1, 2, 3}, {2, -1, 1, 3}, {1, 2, -1, 3}, {3, 2, 1, -1}}, packed + 1 in
+// nibbles (runtime indices without a memory table)
+__device__ __forceinline__ int rpos(int q, int x) {
+    return (int)((0x234403242034320ull >> (4 * (4 * q + x))) & 0xFu) - 1;
+}
 
 // local face k excludes local vertex kExcl[k]; the same map sends a vertex
 // to the face that excludes it
@@ -129,81 +133,98 @@ __global__ void __launch_bounds__(kRgBlock)
         int4 mt[4];
 #pragma unroll
         for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
+        // The distinct child edges once each (the 72 slots repeat them):
+        // V[a][b] for the half-edge (a, m_ab), F[k][a] for the edge
+        // (m_ab, m_ac) inside parent face k at its corner a; the C edges are
+        // closed-form.  All table indices are compile-time constants after
+        // unrolling.
+        int32_t V[4][4], F[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                if (a == b) continue;
+                const int32_t ga = pv[a], gb = pv[b];
+                const int le = ledge(a, b);
+                const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
+                int64_t first;
+                if (ts != kNoParent) {
+                    const int4 ps = ts == t ? pt : ldtet(tets, ts);
+                    first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
+                } else {
+                    const int64_t t1 = ef[le] / 6;
+                    const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
+                    const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
+                    first = 6 * child(t1, qa, n) + rpos(qa, qb) - 1;
+                }
+                V[a][b] = (int32_t)first;
+            }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            // parent face k and the parent across it; lo = the lower of the two
+            const int32_t ms = sm[k];
+            const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
+            const bool t_first = t2 < 0 || t < t2;
+            const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
+            const int4 plo = t_first ? pt : mt[k], phi = t_first ? mt[k] : pt;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int a = face_vert(k, j), b = face_vert(k, (j + 1) % 3), c = face_vert(k, (j + 2) % 3);
+                const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
+                int64_t first;
+                if (plo.x == ga) {
+                    first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
+                } else if (hi >= 0 && phi.x == ga) {
+                    first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
+                } else {
+                    const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
+                    first = 6 * child(lo, qa, n) + ledge(rpos(qa, qb), rpos(qa, qc));
+                }
+                F[k][a] = (int32_t)first;
+            }
+        }
+#pragma unroll
         for (int q = 0; q < 12; ++q) {
             int32_t out[6];
 #pragma unroll
             for (int kk = 0; kk < 6; ++kk) {
                 const int kind = kREdge[q][kk][0], a = kREdge[q][kk][1], b = kREdge[q][kk][2], c = kREdge[q][kk][3];
-                int64_t first;
-                if (kind == 2) {
-                    first = 6 * child(t, a, n) + b;
-                } else if (kind == 0) {
-                    const int32_t ga = pv[a], gb = pv[b];
-                    const int le = ledge(a, b);
-                    const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
-                    if (ts != kNoParent) {
-                        const int4 ps = ts == t ? pt : ldtet(tets, ts);
-                        first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
-                    } else {
-                        const int64_t t1 = ef[le] / 6;
-                        const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
-                        const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
-                        first = 6 * child(t1, qa, n) + kRPos[qa][qb] - 1;
-                    }
-                } else {
-                    // parent face abc: the face of t that excludes the fourth
-                    // corner, and the parent across it
-                    const int d = 6 - a - b - c;
-                    const int kF = excl(d);
-                    const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
-                    const int32_t ms = sm[kF];
-                    const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
-                    const int4 p2 = mt[kF];
-                    const bool t_first = t2 < 0 || t < t2;
-                    const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
-                    const int4 plo = t_first ? pt : p2, phi = t_first ? p2 : pt;
-                    if (plo.x == ga) {
-                        first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
-                    } else if (hi >= 0 && phi.x == ga) {
-                        first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
-                    } else {
-                        const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
-                        first = 6 * child(lo, qa, n) + ledge(kRPos[qa][qb], kRPos[qa][qc]);
-                    }
-                }
-                out[kk] = (int32_t)first;
+                if (kind == 2) out[kk] = (int32_t)(6 * child(t, a, n) + b);
+                else if (kind == 0) out[kk] = V[a][b];
+                else out[kk] = F[excl(6 - a - b - c)][a];
             }
             int2* o2 = s_ef + 3 * stage_row(lt, q);
             o2[0] = make_int2(out[0], out[1]);
             o2[1] = make_int2(out[2], out[3]);
             o2[2] = make_int2(out[4], out[5]);
-            if (!sm_out) continue;
-            int32_t fo[4];
+        }
+        if (sm_out) {
+            // mates of the sub-triangles of parent face k: FM[k][a] at
+            // corner a, MM[k] the middle one
+            int32_t FM[4][4], MM[4];
 #pragma unroll
-            for (int kf = 0; kf < 4; ++kf) {
-                const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
-                int64_t mate;
-                if (kind == 0) {
-                    mate = 4 * child(t, a, n) + b;
-                } else {
-                    const int kF = kind == 1 ? b : a;
-                    const int32_t ms = sm[kF];
-                    if (ms < 0) {
-                        mate = -1;
-                    } else {
-                        const int64_t t2 = ms >> 2;
-                        const int kF2 = ms & 3;
-                        if (kind == 2) {
-                            mate = 4 * child(t2, 8 + kF2, n);
-                        } else {
-                            const int a2 = idx_of(mt[kF], pv[a]);
-                            mate = 4 * child(t2, a2, n) + excl(kRPos[a2][excl(kF2)]);
-                        }
-                    }
+            for (int k = 0; k < 4; ++k) {
+                const int32_t ms = sm[k];
+                const int64_t t2 = ms >> 2;
+                const int k2 = ms & 3;
+                MM[k] = ms < 0 ? -1 : (int32_t)(4 * child(t2, 8 + k2, n));
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int a = face_vert(k, j);
+                    const int a2 = idx_of(mt[k], pv[a]);
+                    FM[k][a] = ms < 0 ? -1 : (int32_t)(4 * child(t2, a2, n) + excl(rpos(a2, excl(k2))));
                 }
-                fo[kf] = (int32_t)mate;
             }
-            s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
+#pragma unroll
+            for (int q = 0; q < 12; ++q) {
+                int32_t fo[4];
+#pragma unroll
+                for (int kf = 0; kf < 4; ++kf) {
+                    const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
+                    fo[kf] = kind == 0 ? (int32_t)(4 * child(t, a, n) + b) : (kind == 1 ? FM[b][a] : MM[a]);
+                }
+                s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
+            }
         }
     }
     __syncthreads();
@@ -243,8 +264,8 @@ __global__ void refined_classify_k(int64_t nd, int64_t nn, const int32_t* __rest
         const int a1 = idx_of(pt, __ldg(tri)), a2 = idx_of(pt, __ldg(tri + 1)), a3 = idx_of(pt, __ldg(tri + 2));
         const int d = 6 - a1 - a2 - a3;
         const int64_t rows[4] = {base + jl, base + nl + 3 * jl, base + nl + 3 * jl + 1, base + nl + 3 * jl + 2};
-        const int64_t slots[4] = {4 * child(t, a1, n) + excl(kRPos[a1][d]), 4 * child(t, a2, n) + excl(kRPos[a2][d]),
-                                  4 * child(t, a3, n) + excl(kRPos[a3][d]), 4 * child(t, 8 + excl(d), n)};
+        const int64_t slots[4] = {4 * child(t, a1, n) + excl(rpos(a1, d)), 4 * child(t, a2, n) + excl(rpos(a2, d)),
+                                  4 * child(t, a3, n) + excl(rpos(a3, d)), 4 * child(t, 8 + excl(d), n)};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int32_t f = __ldg(face_of_slot + slots[q]);
