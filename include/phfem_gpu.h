@@ -113,10 +113,13 @@ int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* st
 /* The child of a red refinement (refine_conn.cu): edge_first [6 x 12 n] and
  * slot_mate [4 x 12 n] (may be NULL) of the child mesh in closed form from
  * the parent's tets [4 n], edge_of_slot, edge_first, slot_mate and nEd;
- * a0 is scratch [2 nEd]. */
+ * a0 is scratch [2 nEd].  Also the child's slot masks [12 n] and the tile
+ * sums of phfem_gpu_element_offsets in scratch (its layout), so that
+ * phfem_gpu_element_offsets_scan finishes the offsets. */
 int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge_of_slot,
                              const int32_t* edge_first, const int32_t* slot_mate, int64_t ned,
-                             int32_t* a0, int32_t* ef_out, int32_t* sm_out, void* stream);
+                             int32_t* a0, int32_t* ef_out, int32_t* sm_out, uint16_t* masks, void* scratch,
+                             void* stream);
 /* classification (connectivity.cpp:120-160) of a refined mesh's lists: the
  * child entries' faces from the parent's classification (nd, nn, db, nb,
  * entry_face, face_slots, tets of the PARENT, n = parent nE), the child's
@@ -142,6 +145,9 @@ int phfem_gpu_star_groups_global(int32_t v, const int64_t* star_ptr, const int32
 size_t phfem_gpu_element_offsets_scratch(int64_t ne);
 int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, const int32_t* slot_mate, uint16_t* masks,
                               int64_t* edge_off, int64_t* face_off, void* scratch, void* stream);
+/* the same from masks and tile sums already in scratch (refined_groups) */
+int phfem_gpu_element_offsets_scan(int64_t ne, const uint16_t* masks, bool faces, int64_t* edge_off,
+                                   int64_t* face_off, void* scratch, void* stream);
 
 /* Numbering from the exclusive offsets: edge ids = rank of the first slot,
  * face ids = rank of the owner slot (the faces_up order).  One thread per

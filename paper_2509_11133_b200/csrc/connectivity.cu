@@ -1015,6 +1015,20 @@ extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, 
     return (int)cudaGetLastError();
 }
 
+extern "C" int phfem_gpu_element_offsets_scan(int64_t ne, const uint16_t* masks, bool faces, int64_t* edge_off,
+                                              int64_t* face_off, void* scratch, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ne <= 0) return phfem_gpu_element_offsets(ne, nullptr, nullptr, nullptr, edge_off, face_off, scratch, stream);
+    const int64_t ntiles = scan_tiles(ne);
+    long long* sums = static_cast<long long*>(scratch);
+    int64_t* total = reinterpret_cast<int64_t*>(sums + ntiles);
+    scan_sums(sums, ntiles, total, s);
+    offsets_scan_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(ne, masks, sums, edge_off, faces ? face_off : nullptr);
+    offsets_total_k<<<1, 1, 0, s>>>(total, ne, edge_off, faces ? face_off : nullptr);
+    phg::count_launches(3);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int phfem_gpu_number(int64_t ne, const int32_t* tets, const double* coords, const int32_t* edge_first,
                                 const int64_t* edge_off, int32_t* edge_of_slot,
                                 int32_t* edge_nodes,

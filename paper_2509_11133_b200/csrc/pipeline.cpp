@@ -155,13 +155,17 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (faces) c.slot_mate.alloc(4 * ne);
     w.big_list.alloc(3 * (nc > 0 ? nc : 1));
     w.big_count.alloc(3);
+    c.edge_off.alloc(ne + 1);
+    if (faces) w.face_off.alloc(ne + 1);
+    w.masks.alloc(ne + 8);
     if (refined) {
+        // also the per-element masks and tile sums: the offsets need only
+        // their scan (no offsets_count_k pass over the slots)
         w.a0.alloc(2 * pc->ned + 2);
-        check(phfem_gpu_refined_groups(m.parent_mesh->ne, m.parent_mesh->tets.p, pc->edge_of_slot.p, pc->edge_first.p,
-                                       pc->slot_mate.p, pc->ned, w.a0.p, c.edge_first.p,
-                                       faces ? c.slot_mate.p : nullptr, SV()),
+        check(phfem_gpu_refined_groups(pm->ne, pm->tets.p, pc->edge_of_slot.p, pc->edge_first.p, pc->slot_mate.p,
+                                       pc->ned, w.a0.p, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p,
+                                       w.scratch.p, SV()),
               "refined groups");
-        w.err.fill_bytes(0xff);
     } else {
         check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
                                     faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.err.p, SV()),
@@ -170,12 +174,14 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     if (st) st->span(&st->groups, t0);
     // 3. numbering: per-element counts, scans, ids, remaining slots
     if (st) t0 = st->mark();
-    c.edge_off.alloc(ne + 1);
-    if (faces) w.face_off.alloc(ne + 1);
-    w.masks.alloc(ne + 8);
-    check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p, c.edge_off.p,
-                                    faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
-          "element offsets");
+    if (refined)
+        check(phfem_gpu_element_offsets_scan(ne, w.masks.p, faces, c.edge_off.p, faces ? w.face_off.p : nullptr,
+                                             w.scratch.p, SV()),
+              "element offsets");
+    else
+        check(phfem_gpu_element_offsets(ne, c.edge_first.p, faces ? c.slot_mate.p : nullptr, w.masks.p,
+                                        c.edge_off.p, faces ? w.face_off.p : nullptr, w.scratch.p, SV()),
+              "element offsets");
     // the totals, and whether a star was too large for the shared-memory
     // tables (the reference has no valence limit): then the global-memory
     // pass groups those vertices and the offsets are redone

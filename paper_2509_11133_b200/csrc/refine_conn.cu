@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include "common.cuh"
+#include "scan.cuh"
 
 namespace {
 
@@ -111,13 +112,20 @@ __device__ __forceinline__ int stage_row(int lt, int q) { return q == 0 ? 11 * k
 __global__ void __launch_bounds__(kRgBlock)
     refined_groups_k(int64_t n, const int32_t* __restrict__ tets, const int32_t* __restrict__ edge_of_slot,
                      const int32_t* __restrict__ edge_first, const int32_t* __restrict__ slot_mate,
-                     const int32_t* __restrict__ a0, int32_t* __restrict__ ef_out, int32_t* __restrict__ sm_out) {
-    __shared__ int2 s_ef[12 * kRgBlock * 3];
-    __shared__ int4 s_sm[12 * kRgBlock];
+                     const int32_t* __restrict__ a0, int32_t* __restrict__ ef_out, int32_t* __restrict__ sm_out,
+                     uint16_t* __restrict__ masks, long long* __restrict__ tile_sums) {
+    // one stage buffer, the edge rows then the face rows
+    __shared__ int4 s_buf[12 * kRgBlock * 6 / 4];
+    __shared__ uint16_t s_mask[12 * kRgBlock];
+    int2* s_ef = reinterpret_cast<int2*>(s_buf);
+    int4* s_sm = s_buf;
     const int64_t t0 = (int64_t)blockIdx.x * kRgBlock;
     const int lt = threadIdx.x;
     const int64_t t = t0 + lt;
     const int nb = (int)(n - t0 < kRgBlock ? n - t0 : kRgBlock);
+    // mates of the sub-triangles of parent face k: FM[k][a] at corner a,
+    // MM[k] the middle one (kept in registers across the edge-row stage)
+    int32_t FM[4][4], MM[4];
     if (lt < nb) {
         const int4 pt = ldtet(tets, t);
         const int32_t pv[4] = {pt.x, pt.y, pt.z, pt.w};
@@ -133,6 +141,19 @@ __global__ void __launch_bounds__(kRgBlock)
         int4 mt[4];
 #pragma unroll
         for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t ms = sm[k];
+            const int64_t t2 = ms >> 2;
+            const int k2 = ms & 3;
+            MM[k] = ms < 0 ? -1 : (int32_t)(4 * child(t2, 8 + k2, n));
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int a = face_vert(k, j);
+                const int a2 = idx_of(mt[k], pv[a]);
+                FM[k][a] = ms < 0 ? -1 : (int32_t)(4 * child(t2, a2, n) + excl(rpos(a2, excl(k2))));
+            }
+        }
         // The distinct child edges once each (the 72 slots repeat them):
         // V[a][b] for the half-edge (a, m_ab), F[k][a] for the edge
         // (m_ab, m_ac) inside parent face k at its corner a; the C edges are
@@ -197,24 +218,25 @@ __global__ void __launch_bounds__(kRgBlock)
             o2[0] = make_int2(out[0], out[1]);
             o2[1] = make_int2(out[2], out[3]);
             o2[2] = make_int2(out[4], out[5]);
+            // first-occurrence slots of the child (offsets_count_k's bits 0-5)
+            const int32_t base = (int32_t)(6 * child(t, q, n));
+            uint32_t m = 0;
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) m |= (uint32_t)(out[kk] == base + kk) << kk;
+            s_mask[stage_row(lt, q)] = (uint16_t)m;
         }
-        if (sm_out) {
-            // mates of the sub-triangles of parent face k: FM[k][a] at
-            // corner a, MM[k] the middle one
-            int32_t FM[4][4], MM[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int32_t ms = sm[k];
-                const int64_t t2 = ms >> 2;
-                const int k2 = ms & 3;
-                MM[k] = ms < 0 ? -1 : (int32_t)(4 * child(t2, 8 + k2, n));
-#pragma unroll
-                for (int j = 0; j < 3; ++j) {
-                    const int a = face_vert(k, j);
-                    const int a2 = idx_of(mt[k], pv[a]);
-                    FM[k][a] = ms < 0 ? -1 : (int32_t)(4 * child(t2, a2, n) + excl(rpos(a2, excl(k2))));
-                }
-            }
+    }
+    __syncthreads();
+    // C1..C11: rows nE + 11 t0 + [0, 11 nb); C0: rows t0 + [0, nb)
+    {
+        int2* e1 = reinterpret_cast<int2*>(ef_out) + 3 * (n + 11 * t0);
+        for (int i = lt; i < 33 * nb; i += kRgBlock) e1[i] = s_ef[i];
+        int2* e0 = reinterpret_cast<int2*>(ef_out) + 3 * t0;
+        for (int i = lt; i < 3 * nb; i += kRgBlock) e0[i] = s_ef[33 * kRgBlock + i];
+    }
+    if (sm_out) {
+        __syncthreads();
+        if (lt < nb) {
 #pragma unroll
             for (int q = 0; q < 12; ++q) {
                 int32_t fo[4];
@@ -224,20 +246,48 @@ __global__ void __launch_bounds__(kRgBlock)
                     fo[kf] = kind == 0 ? (int32_t)(4 * child(t, a, n) + b) : (kind == 1 ? FM[b][a] : MM[a]);
                 }
                 s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
+                // owned face slots (bits 6-9)
+                const int32_t sl = (int32_t)(4 * child(t, q, n));
+                uint32_t m = 0;
+#pragma unroll
+                for (int kf = 0; kf < 4; ++kf) m |= (uint32_t)(fo[kf] < 0 || fo[kf] > sl + kf) << (6 + kf);
+                s_mask[stage_row(lt, q)] |= (uint16_t)m;
             }
         }
+        __syncthreads();
+        int4* f1 = reinterpret_cast<int4*>(sm_out) + n + 11 * t0;
+        for (int i = lt; i < 11 * nb; i += kRgBlock) f1[i] = s_sm[i];
+        int4* f0 = reinterpret_cast<int4*>(sm_out) + t0;
+        for (int i = lt; i < nb; i += kRgBlock) f0[i] = s_sm[11 * kRgBlock + i];
     }
+    // the masks and this block's share of the offsets' tile sums (packed
+    // edges << 31 | faces, offsets_count_k's format): C0 rows lie in one
+    // tile, the C1..C11 range in at most two
+    const int64_t c1 = n + 11 * t0;
+    const int64_t tile1 = c1 / kScanTile;
+    long long s0 = 0, s1 = 0, s2 = 0;
+    for (int i = lt; i < 11 * nb; i += kRgBlock) {
+        const uint32_t m = s_mask[i];
+        masks[c1 + i] = (uint16_t)m;
+        const long long v = (long long)__popc(m & 63u) << 31 | __popc(m >> 6);
+        if ((c1 + i) / kScanTile == tile1) s1 += v;
+        else s2 += v;
+    }
+    if (lt < nb) {
+        const uint32_t m = s_mask[11 * kRgBlock + lt];
+        masks[t0 + lt] = (uint16_t)m;
+        s0 = (long long)__popc(m & 63u) << 31 | __popc(m >> 6);
+    }
+    s0 = block_sum_ll<kRgBlock>(s0);
     __syncthreads();
-    // C1..C11: rows nE + 11 t0 + [0, 11 nb); C0: rows t0 + [0, nb)
-    int2* e1 = reinterpret_cast<int2*>(ef_out) + 3 * (n + 11 * t0);
-    for (int i = lt; i < 33 * nb; i += kRgBlock) e1[i] = s_ef[i];
-    int2* e0 = reinterpret_cast<int2*>(ef_out) + 3 * t0;
-    for (int i = lt; i < 3 * nb; i += kRgBlock) e0[i] = s_ef[33 * kRgBlock + i];
-    if (!sm_out) return;
-    int4* f1 = reinterpret_cast<int4*>(sm_out) + n + 11 * t0;
-    for (int i = lt; i < 11 * nb; i += kRgBlock) f1[i] = s_sm[i];
-    int4* f0 = reinterpret_cast<int4*>(sm_out) + t0;
-    for (int i = lt; i < nb; i += kRgBlock) f0[i] = s_sm[11 * kRgBlock + i];
+    s1 = block_sum_ll<kRgBlock>(s1);
+    __syncthreads();
+    s2 = block_sum_ll<kRgBlock>(s2);
+    if (lt == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(tile_sums + t0 / kScanTile), (unsigned long long)s0);
+        atomicAdd(reinterpret_cast<unsigned long long*>(tile_sums + tile1), (unsigned long long)s1);
+        if (s2) atomicAdd(reinterpret_cast<unsigned long long*>(tile_sums + tile1 + 1), (unsigned long long)s2);
+    }
 }
 
 // Classification of a refined mesh's boundary lists, which refine_mesh built
@@ -282,13 +332,16 @@ __global__ void refined_classify_k(int64_t nd, int64_t nn, const int32_t* __rest
 
 extern "C" int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge_of_slot,
                                         const int32_t* edge_first, const int32_t* slot_mate, int64_t ned,
-                                        int32_t* a0, int32_t* ef_out, int32_t* sm_out, void* stream) {
+                                        int32_t* a0, int32_t* ef_out, int32_t* sm_out, uint16_t* masks,
+                                        void* scratch, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (n == 0) return 0;
+    long long* sums = static_cast<long long*>(scratch);
+    cudaMemsetAsync(sums, 0, sizeof(long long) * (size_t)scan_tiles(12 * n), s);
     cudaMemsetAsync(a0, 0x7f, sizeof(int32_t) * 2 * (size_t)(ned > 0 ? ned : 1), s);
     a0_k<<<grid_for(n, 256), 256, 0, s>>>(n, tets, edge_of_slot, a0);
-    refined_groups_k<<<grid_for(n, kRgBlock), kRgBlock, 0, s>>>(n, tets, edge_of_slot, edge_first, slot_mate, a0, ef_out,
-                                                      sm_out);
+    refined_groups_k<<<grid_for(n, kRgBlock), kRgBlock, 0, s>>>(n, tets, edge_of_slot, edge_first, slot_mate, a0,
+                                                                ef_out, sm_out, masks, sums);
     phg::count_launches(2);
     return (int)cudaGetLastError();
 }
