@@ -227,14 +227,16 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * face_bval [nf] is scratch: the boundary faces' Dirichlet traces / Neumann
  * terms, formed first by a pass over the nd + nn boundary entries
  * (entry_face of the classification, face_slots).  ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the
- * main kernel. */
+ * main kernel.  S goes to SELL-32 (sell_col, sell_val: the reference's rows,
+ * both triangles) or, when sell_col is NULL, element-major: st_val [10 ne]
+ * (S_T[r][q], r <= q, in 32-element chunks: (t/32)*320 + pair*32 + t%32),
+ * the rows slot_mrow [4 ne] (required) and the assembled diagonal diag [l]. */
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
                                 const double* face_area, int64_t nd, int64_t nn,
                                 const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
-                                int32_t* sell_col,
-                                double* sell_val,
+                                int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, int32_t* redo,
                                 unsigned long long* err, void* ev_begin, void* ev_end, void* stream);
@@ -264,6 +266,13 @@ int phfem_gpu_cg_init(int64_t l, const int32_t* sell_col, const double* sell_val
 int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col, const double* sell_val,
                             double* x, double* r, double* p, double* q, const double* d,
                             phg_cg_state* st, double* partials, void* stream);
+/* SELL-32 rows of an element-major S (phfem_gpu_assemble_condense with
+ * sell_col NULL): the layout the SELL assembly writes, S[r][q] = S[q][r] =
+ * the stored upper-triangle value, diagonal = diag; needs slot_mate for the
+ * owner / second-slot positions.  Once per solve (the CG streams rows). */
+int phfem_gpu_elem_to_sell(int64_t ne, int64_t l, const double* st_val, const int32_t* slot_mrow,
+                           const int32_t* slot_mate, const double* diag, int32_t* sell_col, double* sell_val,
+                           void* stream);
 
 /* Element-local recovery U_T = A_T^-1 (B_T + C_T' Lambda_T) (solver.cpp:168-181)
  * fused with the primal block residual of verify_solution (solver.cpp:44-53):

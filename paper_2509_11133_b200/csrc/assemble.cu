@@ -48,6 +48,23 @@ __device__ __forceinline__ int64_t sell_idx(int64_t row, int pos) {
     return (row >> 5) * (PHG_SELL_C * PHG_SELL_W) + pos * PHG_SELL_C + (row & 31);
 }
 
+// Where the condensed operator goes.  SELL (exports, the C++ API's S): the
+// reference's S row by row, both triangles as build_schur computes them.
+// Element-major (the solve path): per element the upper triangle of S_T,
+// S_T[r][q] for r <= q as solver.cpp:121-125 computes it (10 values,
+// 32-element AoSoA chunks), rows = slot_mrow, and the assembled diagonal
+// (two-term sums, so the atomics are order-free); S = sum_T S_T exactly as
+// from_triplets sums it, minus the lower triangle's last-bit differences.
+struct SchurOut {
+    int32_t* sell_col;
+    double* sell_val;
+    double* st_val;  // [10 x ne], element-major
+    double* diag;    // [l], element-major
+};
+__device__ __forceinline__ int64_t st_idx(int64_t t, int j) { return (t >> 5) * 320 + j * 32 + (t & 31); }
+// (r, q), r <= q -> 0..9: (0,0..3) 0-3, (1,1..3) 4-6, (2,2..3) 7-8, (3,3) 9
+__host__ __device__ constexpr int st_pair(int r, int q) { return r == 0 ? q : (r == 1 ? q + 3 : (r == 2 ? q + 5 : 9)); }
+
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -265,11 +282,10 @@ struct FaceIn {
 //
 // Row R of face r: owner slot -> positions 0 (atomic diagonal) and 1-3,
 // second slot -> 0 and 4-6; padding col = R, val = 0.
-template <int KIND, class Dv>
+template <int KIND, bool ELEM, class Dv>
 __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict__ coords,
                                              const int32_t* __restrict__ tets, const phg_problem& prob,
-                                             const FaceIn& fin, double* __restrict__ a_blocks,
-                                             int32_t* __restrict__ sell_col, double* __restrict__ sell_val,
+                                             const FaceIn& fin, double* __restrict__ a_blocks, const SchurOut& so,
                                              double* __restrict__ rhs_neg, double* __restrict__ bd,
                                              double* __restrict__ rhs, double* __restrict__ slot_coef,
                                              int32_t* __restrict__ slot_mrow, Dv& dv) {
@@ -393,14 +409,16 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
 #pragma unroll
             for (int pp = 0; pp < 4; ++pp) rb = add(rb, mul(cr(r, pp), ainv_b[pp]));
             const int64_t R = sl.row[r];
-            sell_col[sell_idx(R, 0)] = (int32_t)R;
+            if (!ELEM) so.sell_col[sell_idx(R, 0)] = (int32_t)R;
             if (sl.bnd[r]) {
                 rhs_neg[R] = sub(bdv[r], rb);
                 bd[R] = bdv[r];
+                if (!ELEM) {
 #pragma unroll
-                for (int pos = 4; pos < 7; ++pos) {
-                    sell_col[sell_idx(R, pos)] = (int32_t)R;
-                    sell_val[sell_idx(R, pos)] = 0.0;
+                    for (int pos = 4; pos < 7; ++pos) {
+                        so.sell_col[sell_idx(R, pos)] = (int32_t)R;
+                        so.sell_val[sell_idx(R, pos)] = 0.0;
+                    }
                 }
             } else {
                 bd[R] = 0.0;
@@ -421,19 +439,26 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            if (sl.row[r] < 0) continue;
+            if (ELEM && r > q) continue;  // the upper triangle only
+            // element-major: every pair is stored, 0 where a slot has no row
+            if (!ELEM && sl.row[r] < 0) continue;
             double s = 0.0;
-            if (real) {
+            if (real && sl.row[r] >= 0) {
 #pragma unroll
                 for (int pp = 0; pp < 4; ++pp) s = add(s, mul(cr(r, pp), x[pp]));
             }
             if (r == q) {
                 sdiag[r] = s;
+                if (ELEM) so.st_val[st_idx(t, st_pair(r, r))] = s;
+                continue;
+            }
+            if (ELEM) {
+                so.st_val[st_idx(t, st_pair(r, q))] = s;
                 continue;
             }
             const int64_t ix = sell_idx(sl.row[r], (sl.owner[r] ? 1 : 4) + (q < r ? q : q - 1));
-            sell_col[ix] = real ? sl.row[q] : sl.row[r];
-            sell_val[ix] = real ? s : 0.0;
+            so.sell_col[ix] = real ? sl.row[q] : sl.row[r];
+            so.sell_val[ix] = real ? s : 0.0;
         }
     }
     if (!dv.good()) return 1;
@@ -441,7 +466,7 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
     for (int r = 0; r < 4; ++r) {
         if (sl.row[r] < 0) continue;
         const int64_t R = sl.row[r];
-        atomicAdd(sell_val + sell_idx(R, 0), sdiag[r]);
+        atomicAdd(ELEM ? so.diag + R : so.sell_val + sell_idx(R, 0), sdiag[r]);
         if (!sl.bnd[r]) atomicAdd(rhs_neg + R, nrb[r]);
     }
     return 0;
@@ -493,21 +518,21 @@ __global__ void __launch_bounds__(128)
 // in flight and the S rows they scatter into stay in an L2-resident window),
 // FastDiv division.  Elements whose operands left the exact window are
 // appended to redo_list.
-template <int KIND>
+template <int KIND, bool ELEM>
 __global__ void __launch_bounds__(kCondThreads, PHG_COND_MINB)
     assemble_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
-               const double* __restrict__ face_bval, double* __restrict__ rhs, int32_t* __restrict__ sell_col,
-               double* __restrict__ sell_val,
+               const double* __restrict__ face_bval, double* __restrict__ rhs, SchurOut so,
                double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
                double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, int32_t* __restrict__ redo_list,
                int32_t* __restrict__ redo_count, unsigned long long* err) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= ne) return;
     FastDiv fd;
-    const int st = assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area, face_bval},
-                                       a_blocks, sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, fd);
+    const int st = assemble_elem<KIND, ELEM>(t, coords, tets, prob,
+                                             {face_of_slot, slot_mate, face_mrow, face_area, face_bval}, a_blocks, so,
+                                             rhs_neg, bd, rhs, slot_coef, slot_mrow, fd);
     if (st == 1) redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
     // "degenerate element block" (solver.cpp:103-109)
     if (st == 2) report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
@@ -516,40 +541,82 @@ __global__ void __launch_bounds__(kCondThreads, PHG_COND_MINB)
 }
 
 // Exact pass over the listed elements (IEEE division throughout).
-template <int KIND>
+template <int KIND, bool ELEM>
 __global__ void __launch_bounds__(kCondThreads)
     assemble_redo_k(const int32_t* __restrict__ redo_list, const int32_t* __restrict__ redo_count,
                     const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                     const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                     const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
-                    const double* __restrict__ face_bval, double* __restrict__ rhs, int32_t* __restrict__ sell_col,
-                    double* __restrict__ sell_val,
+                    const double* __restrict__ face_bval, double* __restrict__ rhs, SchurOut so,
                     double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
                     double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, unsigned long long* err) {
     const int32_t n = *redo_count;
     for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const int64_t t = redo_list[i];
         ExactDiv ed;
-        if (assemble_elem<KIND>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area, face_bval}, a_blocks,
-                                sell_col, sell_val, rhs_neg, bd, rhs, slot_coef, slot_mrow, ed) == 2)
+        if (assemble_elem<KIND, ELEM>(t, coords, tets, prob, {face_of_slot, slot_mate, face_mrow, face_area, face_bval},
+                                      a_blocks, so, rhs_neg, bd, rhs, slot_coef, slot_mrow, ed) == 2)
             report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
     }
 }
 
 // clear the two-contributor accumulators (S diagonal, rhs_neg) of rows 0..l-1
-__global__ void __launch_bounds__(256) zero_rows_k(int64_t l, double* __restrict__ sell_val,
-                                                   double* __restrict__ rhs_neg) {
+__global__ void __launch_bounds__(256) zero_rows_k(int64_t l, SchurOut so, double* __restrict__ rhs_neg) {
     // two rows per thread and step (16 B stores; rows 2i, 2i+1 share a slice)
     const double2 z = make_double2(0.0, 0.0);
     const int64_t l2 = l / 2;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l2; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t R = 2 * i;
-        reinterpret_cast<double2*>(sell_val + sell_idx(R, 0))[0] = z;
+        reinterpret_cast<double2*>(so.diag ? so.diag + R : so.sell_val + sell_idx(R, 0))[0] = z;
         reinterpret_cast<double2*>(rhs_neg)[i] = z;
     }
     if ((l & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        sell_val[sell_idx(l - 1, 0)] = 0.0;
+        (so.diag ? so.diag[l - 1] : so.sell_val[sell_idx(l - 1, 0)]) = 0.0;
         rhs_neg[l - 1] = 0.0;
+    }
+}
+
+// SELL rows from the element-major S (the positions assemble_elem's SELL
+// mode uses: owner slot -> 0 and 1-3, second slot -> 4-6, boundary rows
+// padded with col = R, val = 0), one thread per element; the diagonal
+// (position 0) by the row's owner slot
+__global__ void __launch_bounds__(256)
+    elem_to_sell_k(int64_t ne, const double* __restrict__ st_val, const int32_t* __restrict__ slot_mrow,
+                   const int32_t* __restrict__ slot_mate, const double* __restrict__ diag,
+                   int32_t* __restrict__ sell_col, double* __restrict__ sell_val) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 rw4 = __ldg(reinterpret_cast<const int4*>(slot_mrow) + t);
+        const int4 m4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        const int32_t rw[4] = {rw4.x, rw4.y, rw4.z, rw4.w}, mt[4] = {m4.x, m4.y, m4.z, m4.w};
+        double sv[10];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) sv[j] = __ldg(st_val + st_idx(t, j));
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (rw[r] < 0) continue;
+            const int64_t R = rw[r];
+            const bool owner = mt[r] < 0 || mt[r] > (int32_t)(4 * t + r);
+            const int base = owner ? 1 : 4;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (q == r) continue;
+                const int64_t ix = sell_idx(R, base + (q < r ? q : q - 1));
+                const bool real = rw[q] >= 0;
+                sell_col[ix] = real ? rw[q] : (int32_t)R;
+                sell_val[ix] = real ? sv[r < q ? st_pair(r, q) : st_pair(q, r)] : 0.0;
+            }
+            if (owner) {
+                sell_col[sell_idx(R, 0)] = (int32_t)R;
+                sell_val[sell_idx(R, 0)] = __ldg(diag + R);
+            }
+            if (mt[r] < 0) {
+#pragma unroll
+                for (int pos = 4; pos < 7; ++pos) {
+                    sell_col[sell_idx(R, pos)] = (int32_t)R;
+                    sell_val[sell_idx(R, pos)] = 0.0;
+                }
+            }
+        }
     }
 }
 
@@ -646,8 +713,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            const int32_t* slot_mate, const int32_t* face_mrow,
                                            const double* face_area, int64_t nd, int64_t nn,
                                            const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
-                                           int32_t* sell_col,
-                                           double* sell_val,
+                                           int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, int32_t* redo,
                                            unsigned long long* err, void* ev_begin, void* ev_end, void* stream) {
@@ -656,28 +722,39 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
     const phg_problem p = *prob;
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
-    zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, sell_val, rhs_neg);
-#define PHG_ASM(K)                                                                                                   \
+    // element-major when sell_col is NULL (st_val, diag, slot_mrow required)
+    const bool elem = sell_col == nullptr;
+    if (elem && (!st_val || !diag || !slot_mrow)) return (int)cudaErrorInvalidValue;
+    const SchurOut so{sell_col, sell_val, elem ? st_val : nullptr, elem ? diag : nullptr};
+    zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, so, rhs_neg);
+#define PHG_ASM(K, E)                                                                                                \
+    assemble_k<K, E><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow,          \
+                                                   face_area, face_bval, rhs, so, rhs_neg, bd, a_blocks, slot_coef,  \
+                                                   slot_mrow, redo + 1, redo, err);                                  \
+    if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);                                                             \
+    assemble_redo_k<K, E><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,    \
+                                                        face_mrow, face_area, face_bval, rhs, so, rhs_neg, bd,       \
+                                                        a_blocks, slot_coef, slot_mrow, err)
+#define PHG_KIND(K)                                                                                                  \
     if (nd + nn > 0)                                                                                                 \
         boundary_terms_k<K><<<(unsigned)((nd + nn + 127) / 128), 128, 0, s>>>(nd, nn, entry_face, face_slots, coords, \
                                                                              tets, p, face_area, face_bval);        \
     if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);                                                         \
-    assemble_k<K><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow, face_area,  \
-                                                face_bval, rhs, sell_col, sell_val, rhs_neg, bd, a_blocks,          \
-                                                slot_coef, slot_mrow, redo + 1, redo, err);                         \
-    if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);                                                             \
-    assemble_redo_k<K><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,       \
-                                                     face_mrow, face_area, face_bval, rhs, sell_col, sell_val,      \
-                                                     rhs_neg, bd, a_blocks, slot_coef, slot_mrow, err)
+    if (elem) {                                                                                                      \
+        PHG_ASM(K, true);                                                                                            \
+    } else {                                                                                                         \
+        PHG_ASM(K, false);                                                                                           \
+    }
     switch (p.kind) {
-        case 0: PHG_ASM(0); break;
-        case 1: PHG_ASM(1); break;
-        case 2: PHG_ASM(2); break;
-        case 3: PHG_ASM(3); break;
-        case 4: PHG_ASM(4); break;
-        case 5: PHG_ASM(5); break;
+        case 0: PHG_KIND(0); break;
+        case 1: PHG_KIND(1); break;
+        case 2: PHG_KIND(2); break;
+        case 3: PHG_KIND(3); break;
+        case 4: PHG_KIND(4); break;
+        case 5: PHG_KIND(5); break;
         default: return (int)cudaErrorInvalidValue;
     }
+#undef PHG_KIND
 #undef PHG_ASM
     phg::count_launches(4);
     return (int)cudaGetLastError();
@@ -691,5 +768,16 @@ extern "C" int phfem_gpu_sumsq2(const double* rhs, int64_t n, const double* bd, 
     sumsq2_k<<<kNormGrid, 256, 0, s>>>(rhs, n, bd, l, partials);
     reduce_pairs<<<1, 1024, 0, s>>>(partials, kNormGrid, norms);
     phg::count_launches(2);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_elem_to_sell(int64_t ne, int64_t l, const double* st_val, const int32_t* slot_mrow,
+                                      const int32_t* slot_mate, const double* diag, int32_t* sell_col,
+                                      double* sell_val, void* stream) {
+    (void)l;
+    if (ne == 0) return 0;
+    elem_to_sell_k<<<grid_for(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, st_val, slot_mrow, slot_mate, diag,
+                                                                        sell_col, sell_val);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }

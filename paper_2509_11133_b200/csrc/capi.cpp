@@ -833,6 +833,8 @@ int phfem_mesh_get_system(const phfem_mesh* mesh, double* a_blocks, double* slot
         const int64_t ne = mesh->data()->ne;
         if ((a_blocks || slot_coef || slot_mrow) && !sys.a_blocks.p)
             throw InvalidArgument("element views were not kept");
+        if ((s_rowptr || s_col || s_val) && sys.elem)
+            throw InvalidArgument("the Schur matrix was not kept in row form (call phfem_mesh_assemble)");
         if (a_blocks) sys.a_blocks.download_to(a_blocks, 16 * ne);
         if (slot_coef) sys.slot_coef.download_to(slot_coef, 4 * ne);
         if (slot_mrow) sys.slot_mrow.download_to(slot_mrow, 4 * ne);
@@ -979,7 +981,8 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
             counts[0] = c->ned;
             counts[1] = c->nf;
             counts[2] = c->l;
-            counts[3] = do_assemble ? s->nchunks * PHG_SELL_C * PHG_SELL_W : 0;
+            // stored S values: element-major 10 per element, or SELL slots
+            counts[3] = !do_assemble ? 0 : (s->elem ? 10 * mesh->data()->ne : s->nchunks * PHG_SELL_C * PHG_SELL_W);
             counts[4] = ne_child;
         }
     });

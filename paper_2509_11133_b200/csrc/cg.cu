@@ -336,3 +336,4 @@ extern "C" int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col
     }
     return (int)cudaGetLastError();
 }
+

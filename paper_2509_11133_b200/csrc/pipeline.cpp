@@ -354,10 +354,23 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     sys.coef_version = k.version;
     sys.n = 4 * m.ne;
     sys.l = c.l;
+    // S in SELL-32 when the views are exported (the reference's rows, both
+    // triangles), else element-major for the solve (half the bytes per CG
+    // iteration and per assembly)
+    sys.elem = !debug_views;
     sys.nchunks = (c.l + PHG_SELL_C - 1) / PHG_SELL_C;
-    const int64_t width = PHG_SELL_C * PHG_SELL_W;
-    sys.sell_col.alloc(sys.nchunks * width);
-    sys.sell_val.alloc(sys.nchunks * width);
+    if (sys.elem) {
+        sys.sell_col.release();
+        sys.sell_val.release();
+        sys.st_val.alloc(10 * ((m.ne + 31) / 32) * 32);
+        sys.diag.alloc(c.l);
+    } else {
+        const int64_t width = PHG_SELL_C * PHG_SELL_W;
+        sys.sell_col.alloc(sys.nchunks * width);
+        sys.sell_val.alloc(sys.nchunks * width);
+        sys.st_val.release();
+        sys.diag.release();
+    }
     // the S diagonal, rhs_neg and b_D are cleared by the assembly kernel
     // itself (row owners), every other SELL slot is written exactly once
     sys.rhs_neg.alloc(c.l);
@@ -366,12 +379,11 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     if (debug_views) {
         sys.a_blocks.alloc(16 * m.ne);
         sys.slot_coef.alloc(4 * m.ne);
-        sys.slot_mrow.alloc(4 * m.ne);
     } else {
         sys.a_blocks.release();
         sys.slot_coef.release();
-        sys.slot_mrow.release();
     }
+    sys.slot_mrow.alloc(4 * m.ne);
     Work& w = sys.w;
     w.redo.alloc(m.ne + 1);
     reset_err(w);
@@ -381,10 +393,11 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
     w.face_bval.alloc(c.nf);
     check(phfem_gpu_assemble_condense(m.ne, c.l, m.coords.p, m.tets.p, &p, c.face_of_slot.p, c.slot_mate.p,
                                       c.face_mrow.p, c.face_area.p, m.nd, m.nn, c.entry_face.p, c.face_slots.p,
-                                      w.face_bval.p, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p,
-                                      sys.bd.p, sys.rhs.p, debug_views ? sys.a_blocks.p : nullptr,
-                                      debug_views ? sys.slot_coef.p : nullptr,
-                                      debug_views ? sys.slot_mrow.p : nullptr, w.redo.p, w.err.p, ka, kb, SV()),
+                                      w.face_bval.p, sys.elem ? nullptr : sys.sell_col.p,
+                                      sys.elem ? nullptr : sys.sell_val.p, sys.elem ? sys.st_val.p : nullptr,
+                                      sys.elem ? sys.diag.p : nullptr, sys.rhs_neg.p, sys.bd.p, sys.rhs.p,
+                                      debug_views ? sys.a_blocks.p : nullptr, debug_views ? sys.slot_coef.p : nullptr,
+                                      sys.slot_mrow.p, w.redo.p, w.err.p, ka, kb, SV()),
           "assemble");
     if (st) {
         st->span(&st->assemble, t0);

@@ -373,8 +373,24 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
     DBuf<double> partials(2 * 148 * 8 + 64);
     Timer tm;
     tm.start();
-    check(phfem_gpu_cg_init(l, sys.sell_col.p, sys.sell_val.p, sys.rhs_neg.p, out.lambda.p, r.p, p.p, d.p, tol,
-                            abs_tol, mi, state.p, partials.p, SV()),
+    // the CG streams S by rows: an element-major system is laid out as SELL
+    // once here (S_T's upper triangle mirrored; an element-major SpMV with
+    // atomics measured slower)
+    DBuf<int32_t> tmp_col;
+    DBuf<double> tmp_val;
+    const int32_t* sell_col = sys.sell_col.p;
+    const double* sell_val = sys.sell_val.p;
+    if (sys.elem) {
+        tmp_col.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
+        tmp_val.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
+        check(phfem_gpu_elem_to_sell(m.ne, l, sys.st_val.p, sys.slot_mrow.p, c.slot_mate.p, sys.diag.p, tmp_col.p,
+                                     tmp_val.p, SV()),
+              "elem to sell");
+        sell_col = tmp_col.p;
+        sell_val = tmp_val.p;
+    }
+    check(phfem_gpu_cg_init(l, sell_col, sell_val, sys.rhs_neg.p, out.lambda.p, r.p, p.p, d.p, tol, abs_tol, mi,
+                            state.p, partials.p, SV()),
           "cg init");
     phg_cg_state hs{};
     phg_cg_state* pinned = nullptr;
@@ -391,8 +407,8 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
         hs = *pinned;
         if (!hs.done) {
             check(cudaStreamBeginCapture(S(), cudaStreamCaptureModeThreadLocal), "capture");
-            phfem_gpu_cg_iterations(batch, l, sys.sell_col.p, sys.sell_val.p, out.lambda.p, r.p, p.p, q.p, d.p,
-                                    state.p, partials.p, SV());
+            phfem_gpu_cg_iterations(batch, l, sell_col, sell_val, out.lambda.p, r.p, p.p, q.p, d.p, state.p,
+                                    partials.p, SV());
             check(cudaStreamEndCapture(S(), &graph), "capture end");
             check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
             for (;;) {

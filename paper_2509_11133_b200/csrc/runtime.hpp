@@ -226,8 +226,12 @@ struct System {
     int problem = -1;
     uint64_t coef_version = 0;
     int64_t n = 0, l = 0, nchunks = 0;
+    // S: SELL-32 (debug / export systems) or element-major (solve path:
+    // st_val + slot_mrow + diag); elem says which
+    bool elem = false;
     DBuf<int32_t> sell_col;
     DBuf<double> sell_val, rhs_neg, bd, rhs;
+    DBuf<double> st_val, diag;
     // sum(B_T^2), sum(b_D^2) for inner_cg_options: reduced on the device
     // when a solve asks (the reference computes them at solve time too)
     void norms(double& sum_rhs2, double& sum_bd2) const;
