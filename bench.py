@@ -407,9 +407,10 @@ def main():
                          "target_frac": 0.60, "target_ms": total_bytes / (0.60 * hbm * 1e9) * 1e3,
                          "note": "refine + connect + assemble/condense step against the north-star 60% of HBM"}}
     kern_ms = stage_ms.get("assemble_kernel", 0.0)
-    prof = ncu_facts().get(f"assemble_k<{cfg.problem}>") if dom_name == "assemble_condense" else None
+    # the pipeline's instance: element-major condensed operator (ELEM = 1)
+    kname = f"assemble_k<{cfg.problem}, 1>"
+    prof = ncu_facts().get(kname) if dom_name == "assemble_condense" else None
     if dom_name == "assemble_condense" and kern_ms > 0:
-        kname = f"assemble_k<{cfg.problem}>"
         a_gbs = B["assemble"] / (kern_ms / 1e3) / 1e9
         roofline.update({"kernel": kname, "kernel_ms": kern_ms, "algorithmic_bytes": B["assemble"],
                          "hbm": {"achieved": a_gbs, "peak": hbm, "unit": "GB/s", "frac": a_gbs / hbm,

@@ -126,39 +126,52 @@ __global__ void __launch_bounds__(kRgBlock)
     // mates of the sub-triangles of parent face k: FM[k][a] at corner a,
     // MM[k] the middle one (kept in registers across the edge-row stage)
     int32_t FM[4][4], MM[4];
+    // 32-bit ids: 6 x 12 nE < 2^31 (refine_mesh checks it)
+    const int32_t n32 = (int32_t)n, t32 = (int32_t)t;
+    auto ch = [n32](int32_t tt, int q) { return q == 0 ? tt : n32 + 11 * tt + q - 1; };
     if (lt < nb) {
         const int4 pt = ldtet(tets, t);
         const int32_t pv[4] = {pt.x, pt.y, pt.z, pt.w};
-        int32_t eos[6], ef[6];
+        int32_t ef[6];
+        int2 a0p[6];  // both A0 entries of each edge
+        {
+            const int2* eo2 = reinterpret_cast<const int2*>(edge_of_slot) + 3 * t;
+            const int2* ef2 = reinterpret_cast<const int2*>(edge_first) + 3 * t;
+            const int2 e01 = __ldg(eo2), e23 = __ldg(eo2 + 1), e45 = __ldg(eo2 + 2);
+            const int2 f01 = __ldg(ef2), f23 = __ldg(ef2 + 1), f45 = __ldg(ef2 + 2);
+            const int32_t eos[6] = {e01.x, e01.y, e23.x, e23.y, e45.x, e45.y};
+            ef[0] = f01.x; ef[1] = f01.y; ef[2] = f23.x; ef[3] = f23.y; ef[4] = f45.x; ef[5] = f45.y;
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-            eos[k] = __ldg(edge_of_slot + 6 * t + k);
-            ef[k] = __ldg(edge_first + 6 * t + k);
+            for (int k = 0; k < 6; ++k) a0p[k] = __ldg(reinterpret_cast<const int2*>(a0) + eos[k]);
         }
         const int4 sm4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
         const int32_t sm[4] = {sm4.x, sm4.y, sm4.z, sm4.w};
-        // the parents across t's faces
-        int4 mt[4];
+        // the parent across each face and the positions there of the face's
+        // three corners (mp[k][j] for corner face_vert(k, j))
+        int mp[4][3];
 #pragma unroll
-        for (int f = 0; f < 4; ++f) mt[f] = sm[f] >= 0 ? ldtet(tets, sm[f] >> 2) : make_int4(-1, -1, -1, -1);
+        for (int k = 0; k < 4; ++k) {
+            const int4 m4 = sm[k] >= 0 ? ldtet(tets, sm[k] >> 2) : make_int4(-1, -1, -1, -1);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) mp[k][j] = idx_of(m4, pv[face_vert(k, j)]);
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int32_t ms = sm[k];
-            const int64_t t2 = ms >> 2;
+            const int32_t t2 = ms >> 2;
             const int k2 = ms & 3;
-            MM[k] = ms < 0 ? -1 : (int32_t)(4 * child(t2, 8 + k2, n));
+            MM[k] = ms < 0 ? -1 : 4 * ch(t2, 8 + k2);
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
-                const int a = face_vert(k, j);
-                const int a2 = idx_of(mt[k], pv[a]);
-                FM[k][a] = ms < 0 ? -1 : (int32_t)(4 * child(t2, a2, n) + excl(rpos(a2, excl(k2))));
+                const int a2 = mp[k][j];
+                FM[k][face_vert(k, j)] = ms < 0 ? -1 : 4 * ch(t2, a2) + excl(rpos(a2, excl(k2)));
             }
         }
         // The distinct child edges once each (the 72 slots repeat them):
         // V[a][b] for the half-edge (a, m_ab), F[k][a] for the edge
         // (m_ab, m_ac) inside parent face k at its corner a; the C edges are
         // closed-form.  All table indices are compile-time constants after
-        // unrolling.
+        // unrolling; where the first parent is t itself the positions are too.
         int32_t V[4][4], F[4][4];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -167,41 +180,48 @@ __global__ void __launch_bounds__(kRgBlock)
                 if (a == b) continue;
                 const int32_t ga = pv[a], gb = pv[b];
                 const int le = ledge(a, b);
-                const int32_t ts = __ldg(a0 + 2 * (int64_t)eos[le] + (ga < gb ? 0 : 1));
-                int64_t first;
-                if (ts != kNoParent) {
-                    const int4 ps = ts == t ? pt : ldtet(tets, ts);
-                    first = 6 * (int64_t)ts + idx_of(ps, gb) - 1;
+                const int32_t ts = ga < gb ? a0p[le].x : a0p[le].y;
+                int32_t first;
+                if (ts == t32) {
+                    first = 6 * t32 + b - 1;  // C0 of t (vertex 0 = a)
+                } else if (ts != kNoParent) {
+                    first = 6 * ts + idx_of(ldtet(tets, ts), gb) - 1;
                 } else {
-                    const int64_t t1 = ef[le] / 6;
-                    const int4 p1 = t1 == t ? pt : ldtet(tets, t1);
-                    const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
-                    first = 6 * child(t1, qa, n) + rpos(qa, qb) - 1;
+                    const int32_t t1 = ef[le] / 6;
+                    if (t1 == t32) {
+                        first = 6 * ch(t32, a) + rpos(a, b) - 1;
+                    } else {
+                        const int4 p1 = ldtet(tets, t1);
+                        const int qa = idx_of(p1, ga), qb = idx_of(p1, gb);
+                        first = 6 * ch(t1, qa) + rpos(qa, qb) - 1;
+                    }
                 }
-                V[a][b] = (int32_t)first;
+                V[a][b] = first;
             }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            // parent face k and the parent across it; lo = the lower of the two
+            // parent face k and the parent across it: the first of the two
+            // whose vertex 0 is the corner, else the lower one's corner child
             const int32_t ms = sm[k];
-            const int64_t t2 = ms >= 0 ? (ms >> 2) : -1;
-            const bool t_first = t2 < 0 || t < t2;
-            const int64_t lo = t_first ? t : t2, hi = t_first ? t2 : t;
-            const int4 plo = t_first ? pt : mt[k], phi = t_first ? mt[k] : pt;
+            const int32_t t2 = ms >> 2;
+            const bool t_first = ms < 0 || t32 < t2;
 #pragma unroll
             for (int j = 0; j < 3; ++j) {
                 const int a = face_vert(k, j), b = face_vert(k, (j + 1) % 3), c = face_vert(k, (j + 2) % 3);
-                const int32_t ga = pv[a], gb = pv[b], gc = pv[c];
-                int64_t first;
-                if (plo.x == ga) {
-                    first = 6 * lo + ledge(idx_of(plo, gb), idx_of(plo, gc));
-                } else if (hi >= 0 && phi.x == ga) {
-                    first = 6 * hi + ledge(idx_of(phi, gb), idx_of(phi, gc));
+                const int ma = mp[k][j], mb = mp[k][(j + 1) % 3], mc = mp[k][(j + 2) % 3];
+                const int32_t own0 = 6 * t32 + ledge(b, c);                          // t, vertex 0 = a
+                const int32_t own = 6 * ch(t32, a) + ledge(rpos(a, b), rpos(a, c));  // t's corner child
+                int32_t first;
+                if (t_first) {
+                    if (a == 0) first = own0;
+                    else if (ms >= 0 && ma == 0) first = 6 * t2 + ledge(mb, mc);
+                    else first = own;
                 } else {
-                    const int qa = idx_of(plo, ga), qb = idx_of(plo, gb), qc = idx_of(plo, gc);
-                    first = 6 * child(lo, qa, n) + ledge(rpos(qa, qb), rpos(qa, qc));
+                    if (ma == 0) first = 6 * t2 + ledge(mb, mc);
+                    else if (a == 0) first = own0;
+                    else first = 6 * ch(t2, ma) + ledge(rpos(ma, mb), rpos(ma, mc));
                 }
-                F[k][a] = (int32_t)first;
+                F[k][a] = first;
             }
         }
 #pragma unroll
@@ -210,7 +230,7 @@ __global__ void __launch_bounds__(kRgBlock)
 #pragma unroll
             for (int kk = 0; kk < 6; ++kk) {
                 const int kind = kREdge[q][kk][0], a = kREdge[q][kk][1], b = kREdge[q][kk][2], c = kREdge[q][kk][3];
-                if (kind == 2) out[kk] = (int32_t)(6 * child(t, a, n) + b);
+                if (kind == 2) out[kk] = 6 * ch(t32, a) + b;
                 else if (kind == 0) out[kk] = V[a][b];
                 else out[kk] = F[excl(6 - a - b - c)][a];
             }
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(kRgBlock)
             o2[1] = make_int2(out[2], out[3]);
             o2[2] = make_int2(out[4], out[5]);
             // first-occurrence slots of the child (offsets_count_k's bits 0-5)
-            const int32_t base = (int32_t)(6 * child(t, q, n));
+            const int32_t base = 6 * ch(t32, q);
             uint32_t m = 0;
 #pragma unroll
             for (int kk = 0; kk < 6; ++kk) m |= (uint32_t)(out[kk] == base + kk) << kk;
@@ -243,11 +263,11 @@ __global__ void __launch_bounds__(kRgBlock)
 #pragma unroll
                 for (int kf = 0; kf < 4; ++kf) {
                     const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
-                    fo[kf] = kind == 0 ? (int32_t)(4 * child(t, a, n) + b) : (kind == 1 ? FM[b][a] : MM[a]);
+                    fo[kf] = kind == 0 ? 4 * ch(t32, a) + b : (kind == 1 ? FM[b][a] : MM[a]);
                 }
                 s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
                 // owned face slots (bits 6-9)
-                const int32_t sl = (int32_t)(4 * child(t, q, n));
+                const int32_t sl = 4 * ch(t32, q);
                 uint32_t m = 0;
 #pragma unroll
                 for (int kf = 0; kf < 4; ++kf) m |= (uint32_t)(fo[kf] < 0 || fo[kf] > sl + kf) << (6 + kf);

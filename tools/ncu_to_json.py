@@ -30,7 +30,7 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 def short(name):
     name = name.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "")
-    name = re.sub(r"\(int\)", "", name)
+    name = re.sub(r"\((?:int|bool|long|unsigned int)\)", "", name)
     return name.split("(")[0]
 
 
