@@ -219,6 +219,23 @@ def test_refined_chain_with_faces(oracle, name):
     check_system(g, m, fo, oracle, kind=0)
 
 
+def test_refined_edges_only_child(oracle):
+    """A classified mesh refined twice in a row: the first child's edge
+    table (needed by the second refinement) comes from the parent's tables
+    without faces (refined_groups with no face output, edge-only masks), its
+    boundary lists through the star; the grandchild has no parent link."""
+    m = oracle.kuhn(2, 2, 1, jitter=0.15, dmask=0x9)
+    g = to_gpu(m)
+    g.faces()  # classify level 0
+    for _ in range(2):
+        m = oracle.refine(m)[0]
+        g.refine()
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(m, k)), k
+    check_connectivity(g, m, oracle)
+
+
 def test_reference_golden_counts_levels_1_to_4(goldens):
     table = goldens["refine_counts_ne_nc_ned_nf"]["value"]
     dims = goldens["system_dims_n_l"]["value"]
