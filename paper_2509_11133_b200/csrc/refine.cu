@@ -150,6 +150,7 @@ __global__ void refine_boundary_owned_k(int64_t nf, const int32_t* __restrict__ 
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
         const int32_t n1 = faces[3 * f], n2 = faces[3 * f + 1], n3 = faces[3 * f + 2];
         const int32_t fid = __ldg(entry_face + list_base + f);
+        PHG_CHECK(fid >= 0);
         const int64_t t = __ldg(face_slots + 2 * (int64_t)fid) >> 2;
         const int4 tet = ldtet(tets, t);
         const int l1 = tet.x == n1 ? 0 : (tet.y == n1 ? 1 : (tet.z == n1 ? 2 : 3));

@@ -96,6 +96,7 @@ __global__ void a0_k(int64_t ne, const int32_t* __restrict__ tets, const int32_t
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const int32_t e = edge_of_slot[6 * t + k];
+            PHG_CHECK(e >= 0);
             atomicMin(a0 + 2 * (int64_t)e + (p.x < o[k] ? 0 : 1), (int32_t)t);
         }
     }
@@ -234,6 +235,8 @@ __global__ void __launch_bounds__(kRgBlock)
                 else if (kind == 0) out[kk] = V[a][b];
                 else out[kk] = F[excl(6 - a - b - c)][a];
             }
+#pragma unroll
+            for (int kk = 0; kk < 6; ++kk) PHG_CHECK(out[kk] >= 0 && out[kk] <= 6 * ch(t32, q) + kk);
             int2* o2 = s_ef + 3 * stage_row(lt, q);
             o2[0] = make_int2(out[0], out[1]);
             o2[1] = make_int2(out[2], out[3]);
@@ -265,6 +268,8 @@ __global__ void __launch_bounds__(kRgBlock)
                     const int kind = kRFace[q][kf][0], a = kRFace[q][kf][1], b = kRFace[q][kf][2];
                     fo[kf] = kind == 0 ? 4 * ch(t32, a) + b : (kind == 1 ? FM[b][a] : MM[a]);
                 }
+#pragma unroll
+                for (int kf = 0; kf < 4; ++kf) PHG_CHECK(fo[kf] >= -1 && fo[kf] < 48 * n32 && fo[kf] != 4 * ch(t32, q) + kf);
                 s_sm[stage_row(lt, q)] = make_int4(fo[0], fo[1], fo[2], fo[3]);
                 // owned face slots (bits 6-9)
                 const int32_t sl = 4 * ch(t32, q);
