@@ -219,6 +219,32 @@ def test_refined_chain_with_faces(oracle, name):
     check_system(g, m, fo, oracle, kind=0)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_random_meshes_refined_with_faces(oracle, seed):
+    """Seeded random Kuhn boxes (sizes, jitter, boundary split, an array-built
+    handle or the device generator), classified and refined twice: the meshes,
+    the whole connectivity and the system (polynomial data: bit-exact) at every
+    level against the oracle."""
+    rng = np.random.default_rng(11133 + seed)
+    nx, ny, nz = (int(v) for v in rng.integers(1, 4, 3))
+    jitter = float(rng.choice([0.0, 0.1, 0.2]))
+    dmask = int(rng.integers(1, 64))
+    m = oracle.kuhn(nx, ny, nz, lx=float(rng.uniform(0.5, 2)), jitter=jitter, seed=int(rng.integers(1, 1 << 30)),
+                    dmask=dmask)
+    g = to_gpu(m)
+    for lv in range(3):
+        fo = check_connectivity(g, m, oracle)
+        if lv == 2:
+            check_system(g, m, fo, oracle, kind=int(rng.integers(0, 3)))
+            break
+        mo = oracle.refine(m)[0]
+        g.refine()
+        mg = from_gpu(g)
+        for k in ("coords", "tets", "db", "nb"):
+            assert np.array_equal(getattr(mg, k), getattr(mo, k)), (lv, k)
+        m = mo
+
+
 def test_refined_edges_only_child(oracle):
     """A classified mesh refined twice in a row: the first child's edge
     table (needed by the second refinement) comes from the parent's tables
