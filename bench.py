@@ -239,7 +239,7 @@ def cpu_baseline(n=64, gpu_iterations=None, l_target=None):
     return out
 
 
-def measure_fp64_peak(ph, torch, stream, iters=4096, reps=3):
+def measure_fp64_peak(ph, torch, stream, iters=16384, reps=5):
     """fp64 FMA throughput of this GPU (TFLOP/s, best of reps) from the
     library's DFMA probe kernel, timed with CUDA events on its stream."""
     import ctypes
