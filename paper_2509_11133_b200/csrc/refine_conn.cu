@@ -1,8 +1,10 @@
 // Connectivity of a red-refined mesh in closed form from its parent's tables
 // (no vertex star, no hashing): the child's first-occurrence edge slots
-// (edge_first) and face mates (slot_mate), one thread per parent element
-// writing the 12 children's 72 edge and 48 face slots.  The rest of the
-// numbering (offsets, ids, classification) is the generic pipeline's.
+// (edge_first), face mates (slot_mate) and per-element first/owner masks
+// with the offsets' tile sums, one thread per parent element writing the 12
+// children's 72 edge and 48 face slots (refined_groups_k); the child's
+// boundary classification from the parent's (refined_classify_k).  The
+// offsets' scan and the ids / tables (`number`) are the generic pipeline's.
 //
 // Children of parent t = (i, j, k, l) with midpoints m_ab and centroid c
 // (refine.cpp:58-61): C0 = (i ij ik il) at index t, C1..C11 at
