@@ -123,11 +123,13 @@ int phfem_gpu_refined_groups(int64_t n, const int32_t* tets, const int32_t* edge
 /* classification (connectivity.cpp:120-160) of a refined mesh's lists: the
  * child entries' faces from the parent's classification (nd, nn, db, nb,
  * entry_face, face_slots, tets of the PARENT, n = parent nE), the child's
- * face_of_slot / face_slots; claims and errors as phfem_gpu_classify */
+ * face_of_slot / face_slots; claims and errors as phfem_gpu_classify;
+ * face_class (may be NULL, else zeroed) gets 1 / 2 on the listed faces */
 int phfem_gpu_refined_classify(int64_t nd, int64_t nn, const int32_t* db, const int32_t* nb,
                                const int32_t* p_entry_face, const int32_t* p_face_slots, const int32_t* p_tets,
                                int64_t n, const int32_t* face_of_slot, const int32_t* face_slots,
-                               uint32_t* claim, int32_t* entry_face, unsigned long long* err, void* stream);
+                               uint32_t* claim, int32_t* entry_face, uint8_t* face_class,
+                               unsigned long long* err, void* stream);
 /* a star listed by star_groups as too large for shared memory (defer_list
  * + 2 nC, count defer_count[2], PHG_ERR_VALENCE set): tables of capacity
  * cap (power of two > 3 m) in global scratch [20 cap bytes] */
@@ -184,6 +186,9 @@ int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const in
  * phfem_gpu_face_class */
 int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const void* scratch, int32_t* face_mrow,
                         int32_t* row_face, void* stream);
+/* rows when every face is a row (no Neumann faces): face_mrow = row_face =
+ * 0..nf-1 */
+int phfem_gpu_face_rows_identity(int64_t nf, int32_t* face_mrow, int32_t* row_face, void* stream);
 
 /* ----------------------------------------------------------- refinement */
 /* red_refine (refine.cpp:16-74): one thread per parent; child 0 at row t,

@@ -661,6 +661,14 @@ __global__ void __launch_bounds__(kScanThreads)
     store_tile_i64(stage, face_off, base, ne);
 }
 
+__global__ void __launch_bounds__(256) face_rows_identity_k(int64_t nf, int32_t* __restrict__ mrow,
+                                                             int32_t* __restrict__ row_face) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < nf; f += (int64_t)gridDim.x * blockDim.x) {
+        mrow[f] = (int32_t)f;
+        row_face[f] = (int32_t)f;
+    }
+}
+
 // grand totals edge_off[ne], face_off[ne] from the packed total
 __global__ void offsets_total_k(const int64_t* __restrict__ packed_total, int64_t ne, int64_t* __restrict__ edge_off,
                                 int64_t* __restrict__ face_off) {
@@ -1086,6 +1094,13 @@ extern "C" int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const 
     if (nf <= 0) return 0;
     face_rows_k<<<(unsigned)scan_tiles(nf), kScanThreads, 0, (cudaStream_t)stream>>>(
         nf, face_class, static_cast<const long long*>(scratch), face_mrow, row_face);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_face_rows_identity(int64_t nf, int32_t* face_mrow, int32_t* row_face, void* stream) {
+    if (nf == 0) return 0;
+    face_rows_identity_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_mrow, row_face);
     phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -227,10 +227,20 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     w.claim.alloc(nf);
     w.claim.fill_bytes(0xff);
     c.entry_face.alloc(m.nd + m.nn);
+    // A refined child's boundary faces are exactly the sub-triangles of its
+    // parent's classified boundary faces, each listed once in the child's
+    // lists: without Neumann faces every face is a multiplier row (rows =
+    // face ids) and the class counts follow from the list sizes, so the
+    // per-face class / row passes reduce to writing the boundary classes.
+    const bool closed_rows = refined_cls && m.nn == 0;
+    if (closed_rows) {
+        c.face_class.alloc(nf + 16);
+        c.face_class.zero();
+    }
     if (refined_cls) {
         check(phfem_gpu_refined_classify(pm->nd, pm->nn, pm->db.p, pm->nb.p, pc->entry_face.p, pc->face_slots.p,
                                          pm->tets.p, pm->ne, c.face_of_slot.p, c.face_slots.p, w.claim.p,
-                                         c.entry_face.p, w.err.p, SV()),
+                                         c.entry_face.p, closed_rows ? c.face_class.p : nullptr, w.err.p, SV()),
               "refined classify");
     } else {
         check(phfem_gpu_classify(m.nd, m.db.p, m.nn, m.nb.p, c.star_ptr.p, c.star.p, m.tets.p, c.face_of_slot.p,
@@ -238,6 +248,23 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
               "classify");
     }
     check(phfem_gpu_classify_check(m.nd, m.nn, c.entry_face.p, w.claim.p, w.err.p, SV()), "classify check");
+    if (closed_rows) {
+        static_assert(PHG_ERR_COUNT == 7, "error slots");
+        const auto e = read_many<unsigned long long, 7>(
+            {w.err.p, w.err.p + 1, w.err.p + 2, w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6});
+        replay_connectivity_errors(std::vector<unsigned long long>(e.begin(), e.end()), m, c);
+        c.n_dir = m.nd;
+        c.n_neu = 0;
+        c.n_int = nf - m.nd;
+        c.l = nf;
+        c.face_mrow.alloc(nf);
+        c.row_face.alloc(nf);
+        check(phfem_gpu_face_rows_identity(nf, c.face_mrow.p, c.row_face.p, SV()), "face rows");
+        if (st) st->span(&st->classify, t0);
+        c.has_faces = true;
+        c.t_faces = std::chrono::duration<double>(std::chrono::steady_clock::now() - w1).count();
+        return;
+    }
     c.face_class.alloc(nf + 16);
     w.counts.alloc(4);
     w.counts.zero();

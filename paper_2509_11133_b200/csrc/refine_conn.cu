@@ -330,7 +330,8 @@ __global__ void refined_classify_k(int64_t nd, int64_t nn, const int32_t* __rest
                                    const int32_t* __restrict__ p_face_slots, const int32_t* __restrict__ p_tets,
                                    int64_t n, const int32_t* __restrict__ face_of_slot,
                                    const int32_t* __restrict__ face_slots, uint32_t* __restrict__ claim,
-                                   int32_t* __restrict__ entry_face, unsigned long long* err) {
+                                   int32_t* __restrict__ entry_face, uint8_t* __restrict__ face_class,
+                                   unsigned long long* err) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nd + nn; j += (int64_t)gridDim.x * blockDim.x) {
         const bool dir = j < nd;
         const int64_t jl = dir ? j : j - nd, nl = dir ? nd : nn, base = dir ? 0 : 4 * nd;
@@ -349,6 +350,7 @@ __global__ void refined_classify_k(int64_t nd, int64_t nn, const int32_t* __rest
             PHG_CHECK(f >= 0);
             entry_face[rows[q]] = f;
             atomicMin(claim + f, (uint32_t)rows[q]);
+            if (face_class) face_class[f] = dir ? 1 : 2;
             if (__ldg(face_slots + 2 * (int64_t)f + 1) >= 0)
                 report(err, PHG_ERR_CLASSIFY, (unsigned long long)rows[q] << 2 | 2);
         }
@@ -377,10 +379,11 @@ extern "C" int phfem_gpu_refined_classify(int64_t nd, int64_t nn, const int32_t*
                                           const int32_t* p_entry_face, const int32_t* p_face_slots,
                                           const int32_t* p_tets, int64_t n, const int32_t* face_of_slot,
                                           const int32_t* face_slots, uint32_t* claim, int32_t* entry_face,
-                                          unsigned long long* err, void* stream) {
+                                          uint8_t* face_class, unsigned long long* err, void* stream) {
     if (nd + nn == 0) return 0;
     refined_classify_k<<<grid_for(nd + nn, 128), 128, 0, (cudaStream_t)stream>>>(
-        nd, nn, db, nb, p_entry_face, p_face_slots, p_tets, n, face_of_slot, face_slots, claim, entry_face, err);
+        nd, nn, db, nb, p_entry_face, p_face_slots, p_tets, n, face_of_slot, face_slots, claim, entry_face,
+        face_class, err);
     phg::count_launches(1);
     return (int)cudaGetLastError();
 }
