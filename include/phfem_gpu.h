@@ -186,6 +186,10 @@ int phfem_gpu_face_class(int64_t nf, int64_t nd, const uint32_t* claim, const in
  * phfem_gpu_face_class */
 int phfem_gpu_face_rows(int64_t nf, const uint8_t* face_class, const void* scratch, int32_t* face_mrow,
                         int32_t* row_face, void* stream);
+/* phfem_gpu_face_class's tile row counts (scratch) from classes already in
+ * face_class (a refined child's, refined_classify) */
+int phfem_gpu_face_tile_rows(int64_t nf, const uint8_t* face_class, void* scratch, int64_t* n_rows,
+                             void* stream);
 /* rows when every face is a row (no Neumann faces): face_mrow = row_face =
  * 0..nf-1 */
 int phfem_gpu_face_rows_identity(int64_t nf, int32_t* face_mrow, int32_t* row_face, void* stream);

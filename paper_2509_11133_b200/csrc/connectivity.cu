@@ -888,6 +888,25 @@ __global__ void __launch_bounds__(kScanThreads)
     if (threadIdx.x < 3) atomicAdd(counts + threadIdx.x, (unsigned long long)sc[threadIdx.x]);
 }
 
+// the tile row counts alone, from classes already written (refined meshes)
+__global__ void __launch_bounds__(kScanThreads)
+    face_tile_rows_k(int64_t nf, const uint8_t* __restrict__ face_class, long long* __restrict__ sums) {
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    int rows = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems / 4; ++i) {
+        const int64_t f = base + 4 * (i * kScanThreads + (int64_t)threadIdx.x);
+        if (f + 4 <= nf) {
+            const uchar4 k = __ldg(reinterpret_cast<const uchar4*>(face_class + f));
+            rows += (k.x != 2) + (k.y != 2) + (k.z != 2) + (k.w != 2);
+        } else {
+            for (int j = 0; j < 4 && f + j < nf; ++j) rows += face_class[f + j] != 2;
+        }
+    }
+    const long long tot = block_sum_ll<kScanThreads>(rows);
+    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
 // classes staged in shared memory (striped in, blocked for the scan), rows
 // staged again and written out striped, with the row -> face list
 __global__ void __launch_bounds__(kScanThreads)
@@ -1102,5 +1121,20 @@ extern "C" int phfem_gpu_face_rows_identity(int64_t nf, int32_t* face_mrow, int3
     if (nf == 0) return 0;
     face_rows_identity_k<<<grid_cap(nf, 256), 256, 0, (cudaStream_t)stream>>>(nf, face_mrow, row_face);
     phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_face_tile_rows(int64_t nf, const uint8_t* face_class, void* scratch, int64_t* n_rows,
+                                        void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nf <= 0) {
+        cudaMemsetAsync(n_rows, 0, sizeof(int64_t), s);
+        return (int)cudaGetLastError();
+    }
+    const int64_t ntiles = scan_tiles(nf);
+    long long* sums = static_cast<long long*>(scratch);
+    face_tile_rows_k<<<(unsigned)ntiles, kScanThreads, 0, s>>>(nf, face_class, sums);
+    scan_sums(sums, ntiles, n_rows, s);
+    phg::count_launches(2);
     return (int)cudaGetLastError();
 }

@@ -229,10 +229,10 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     c.entry_face.alloc(m.nd + m.nn);
     // A refined child's boundary faces are exactly the sub-triangles of its
     // parent's classified boundary faces, each listed once in the child's
-    // lists: without Neumann faces every face is a multiplier row (rows =
-    // face ids) and the class counts follow from the list sizes, so the
-    // per-face class / row passes reduce to writing the boundary classes.
-    const bool closed_rows = refined_cls && m.nn == 0;
+    // lists: the classes are written by the refined classification, the
+    // class counts follow from the list sizes, and without Neumann faces
+    // every face is a multiplier row (rows = face ids).
+    const bool closed_rows = refined_cls;
     if (closed_rows) {
         c.face_class.alloc(nf + 16);
         c.face_class.zero();
@@ -254,12 +254,22 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
             {w.err.p, w.err.p + 1, w.err.p + 2, w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6});
         replay_connectivity_errors(std::vector<unsigned long long>(e.begin(), e.end()), m, c);
         c.n_dir = m.nd;
-        c.n_neu = 0;
-        c.n_int = nf - m.nd;
-        c.l = nf;
+        c.n_neu = m.nn;
+        c.n_int = nf - m.nd - m.nn;
+        c.l = nf - m.nn;
         c.face_mrow.alloc(nf);
-        c.row_face.alloc(nf);
-        check(phfem_gpu_face_rows_identity(nf, c.face_mrow.p, c.row_face.p, SV()), "face rows");
+        c.row_face.alloc(c.l);
+        if (m.nn == 0) {
+            check(phfem_gpu_face_rows_identity(nf, c.face_mrow.p, c.row_face.p, SV()), "face rows");
+        } else {
+            w.counts.alloc(4);
+            w.scratch.alloc((int64_t)phfem_gpu_face_rows_scratch(nf));
+            check(phfem_gpu_face_tile_rows(nf, c.face_class.p, w.scratch.p, reinterpret_cast<int64_t*>(w.counts.p + 3),
+                                           SV()),
+                  "face rows");
+            check(phfem_gpu_face_rows(nf, c.face_class.p, w.scratch.p, c.face_mrow.p, c.row_face.p, SV()),
+                  "face rows");
+        }
         if (st) st->span(&st->classify, t0);
         c.has_faces = true;
         c.t_faces = std::chrono::duration<double>(std::chrono::steady_clock::now() - w1).count();
