@@ -87,7 +87,10 @@ int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, do
                        double* partials, void* stream);
 
 /* -------------------------------------------------------- connectivity */
-/* vertex -> (element, local vertex) incidence ("star"), CSR by vertex:
+/* vertex -> (element, local vertex) incidence ("star"), CSR by vertex,
+ * without the incidence of each element's largest vertex (3 nE entries:
+ * every edge and face is grouped at its smallest vertex, and an element's
+ * largest vertex has no candidate above it):
  * count[v] (zeroed) += incidences; star_ptr = exclusive scan of count;
  * star_fill places each incidence at star_ptr[v] + --count[v] (the order
  * inside a vertex's segment is unspecified; every consumer is order free)

@@ -26,13 +26,28 @@ namespace {
 
 using namespace phg;
 
+// The star of v holds the incidences (t, lv) whose vertex v is not t's
+// largest: every edge and face is grouped at its smallest vertex, and no
+// candidate of an element's largest vertex lies above it, so that incidence
+// would contribute nothing (3 incidences per element instead of 4).
+// top = the local vertex with the largest id (the first of equal ones).
+__device__ __forceinline__ int top_vertex(const int4& e) {
+    int k = 0;
+    int32_t m = e.x;
+    if (e.y > m) { k = 1; m = e.y; }
+    if (e.z > m) { k = 2; m = e.z; }
+    if (e.w > m) k = 3;
+    return k;
+}
+
 __global__ void star_count(const int32_t* __restrict__ tets, int64_t ne, int32_t* __restrict__ count) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
         const int4 e = ldtet(tets, t);
-        atomicAdd(count + e.x, 1);
-        atomicAdd(count + e.y, 1);
-        atomicAdd(count + e.z, 1);
-        atomicAdd(count + e.w, 1);
+        const int top = top_vertex(e);
+        if (top != 0) atomicAdd(count + e.x, 1);
+        if (top != 1) atomicAdd(count + e.y, 1);
+        if (top != 2) atomicAdd(count + e.z, 1);
+        if (top != 3) atomicAdd(count + e.w, 1);
     }
 }
 
@@ -41,14 +56,16 @@ __global__ void star_fill(const int32_t* __restrict__ tets, int64_t ne, const in
                           int32_t* __restrict__ count, int32_t* __restrict__ star) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
         const int4 e = ldtet(tets, t);
+        const int top = top_vertex(e);
         const int32_t base = (int32_t)(4 * t);
-        const int32_t c0 = atomicSub(count + e.x, 1), c1 = atomicSub(count + e.y, 1), c2 = atomicSub(count + e.z, 1),
-                      c3 = atomicSub(count + e.w, 1);
-        PHG_CHECK(c0 >= 1 && c0 <= star_ptr[e.x + 1] - star_ptr[e.x] && c1 >= 1 && c2 >= 1 && c3 >= 1);
-        star[__ldg(star_ptr + e.x) + c0 - 1] = base + 0;
-        star[__ldg(star_ptr + e.y) + c1 - 1] = base + 1;
-        star[__ldg(star_ptr + e.z) + c2 - 1] = base + 2;
-        star[__ldg(star_ptr + e.w) + c3 - 1] = base + 3;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k == top) continue;
+            const int32_t v = tv(e, k);
+            const int32_t c = atomicSub(count + v, 1);
+            PHG_CHECK(c >= 1 && c <= star_ptr[v + 1] - star_ptr[v]);
+            star[__ldg(star_ptr + v) + c - 1] = base + k;
+        }
     }
 }
 

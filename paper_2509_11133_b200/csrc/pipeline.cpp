@@ -125,7 +125,7 @@ void build_star(const MeshData& m, Connectivity& c, Stages* st) {
     check(phfem_gpu_star_count(m.tets.p, m.ne, w.cnt.p, SV()), "star count");
     c.star_ptr.alloc(m.nc + 1);
     check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, m.nc, w.scratch.p, SV()), "star scan");
-    c.star.alloc(4 * m.ne);
+    c.star.alloc(3 * m.ne);  // no incidence of an element's largest vertex
     check(phfem_gpu_star_fill(m.tets.p, m.ne, c.star_ptr.p, w.cnt.p, c.star.p, SV()), "star fill");
     if (st) st->span(&st->star, t0);
     c.has_star = true;
