@@ -285,6 +285,18 @@ int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col, const dou
 int phfem_gpu_elem_to_sell(int64_t ne, int64_t l, const double* st_val, const int32_t* slot_mrow,
                            const int32_t* slot_mate, const double* diag, int32_t* sell_col, double* sell_val,
                            void* stream);
+/* The same CG on the element-major S itself (no SELL copy): row_slots
+ * [2 L] = (owner slot, second slot or -1) of each row, built once per solve
+ * by cg_em_rows; cg_em_iterations sums each row in the SELL order of
+ * elem_to_sell, so the iterates equal cg_iterations' on that SELL copy. */
+int phfem_gpu_cg_em_rows(int64_t ne, const int32_t* slot_mrow, const int32_t* slot_mate, int32_t* row_slots,
+                         void* stream);
+int phfem_gpu_cg_em_init(int64_t l, const double* diag, const double* b, double* x, double* r, double* p,
+                         double* d, double tol, double abs_tol, long long max_iter, phg_cg_state* st,
+                         double* partials, void* stream);
+int phfem_gpu_cg_em_iterations(int n, int64_t l, const int32_t* row_slots, const double* st_val,
+                               const int32_t* slot_mrow, const double* diag, double* x, double* r, double* p,
+                               double* q, const double* d, phg_cg_state* st, double* partials, void* stream);
 
 /* Element-local recovery U_T = A_T^-1 (B_T + C_T' Lambda_T) (solver.cpp:168-181)
  * fused with the primal block residual of verify_solution (solver.cpp:44-53):

@@ -61,9 +61,6 @@ struct SchurOut {
     double* st_val;  // [10 x ne], element-major
     double* diag;    // [l], element-major
 };
-__device__ __forceinline__ int64_t st_idx(int64_t t, int j) { return (t >> 5) * 320 + j * 32 + (t & 31); }
-// (r, q), r <= q -> 0..9: (0,0..3) 0-3, (1,1..3) 4-6, (2,2..3) 7-8, (3,3) 9
-__host__ __device__ constexpr int st_pair(int r, int q) { return r == 0 ? q : (r == 1 ? q + 3 : (r == 2 ? q + 5 : 9)); }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));

@@ -89,6 +89,10 @@ struct SellDiag {
     const double* sell_val;
     __device__ __forceinline__ double operator()(int64_t i) const { return sell_val[sell_idx(i, 0)]; }
 };
+struct ArrDiag {
+    const double* diag;
+    __device__ __forceinline__ double operator()(int64_t i) const { return diag[i]; }
+};
 struct CsrDiag {
     const int64_t* ptr;
     const int32_t* col;
@@ -176,6 +180,97 @@ __global__ void __launch_bounds__(kThreads)
             st->done = 1;
         } else {
             st->alpha = st->rz / tot[0];
+        }
+    }
+}
+
+// q = S p straight from the element-major blocks (the pipeline's system):
+// row R is the face of slots (s1 = owner, s2 = second or -1), and its
+// entries are S_T[r][q] of those slots' elements, q over the element's other
+// faces in increasing order, owner first -- the SELL row of elem_to_sell_k,
+// summed in the same order with the same padding (0 * p[R] for a slot
+// without a row, three of them for a face with one element), so the
+// iterates are those of the SELL path bit for bit.  Per row 8 bytes of slots
+// + 8 of diagonal instead of 84 bytes of SELL columns and values; the
+// element's 6 off-diagonal values and its 4 row ids (64 bytes) are gathered
+// by its faces' rows, which run close together (owner rows are consecutive,
+// L2 holds the second elements' blocks in between).
+// pair index (st_pair) of the k-th other face of local face r, 4 bits per
+// (r, k): r = 0: (0,1) (0,2) (0,3); 1: (0,1) (1,2) (1,3); 2: (0,2) (1,2)
+// (2,3); 3: (0,3) (1,3) (2,3)
+constexpr unsigned long long kEmPairs = 0x321ull | 0x651ull << 12 | 0x852ull << 24 | 0x863ull << 36;
+__device__ __forceinline__ double em_slot(int32_t slot, double s, double pi, const double* __restrict__ st_val,
+                                          const int32_t* __restrict__ slot_mrow, const double* __restrict__ p,
+                                          int64_t l) {
+    const int64_t t = slot >> 2;
+    const int r = slot & 3;
+    const int4 m4 = __ldg(reinterpret_cast<const int4*>(slot_mrow) + t);
+    // the other three rows in local order
+    const int32_t c[3] = {r == 0 ? m4.y : m4.x, r <= 1 ? m4.z : m4.y, r <= 2 ? m4.w : m4.z};
+    const double* base = st_val + ((t >> 5) * 320 + (t & 31));
+    const unsigned pairs = (unsigned)(kEmPairs >> (12 * r));
+    double v[3], pc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        PHG_CHECK(c[k] < l);
+        v[k] = c[k] >= 0 ? __ldg(base + 32 * ((pairs >> (4 * k)) & 15u)) : 0.0;
+        pc[k] = c[k] >= 0 ? __ldg(p + c[k]) : pi;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s += v[k] * pc[k];
+    return s;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    cg_spmv_em(int64_t l, const int2* __restrict__ row_slots, const double* __restrict__ st_val,
+               const int32_t* __restrict__ slot_mrow, const double* __restrict__ diag, const double* __restrict__ p,
+               double* __restrict__ q, phg_cg_state* st, double* partials) {
+    if (st->done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->x_pending = 0;
+        return;
+    }
+    double acc[1] = {0.0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        const int2 rs = __ldg(row_slots + i);
+        const double pi = __ldg(p + i);
+        double s = __ldg(diag + i) * pi;
+        s = em_slot(rs.x, s, pi, st_val, slot_mrow, p, l);
+        if (rs.y >= 0) {
+            s = em_slot(rs.y, s, pi, st_val, slot_mrow, p, l);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s += 0.0 * pi;  // SELL padding
+        }
+        q[i] = s;
+        acc[0] += pi * s;
+    }
+    double tot[1];
+    if (!finish<1>(acc, partials, &st->counter[1], tot)) return;
+    if (threadIdx.x == 0) {
+        st->pq = tot[0];
+        if (tot[0] <= 0.0) {  // sparse.cpp:185
+            st->not_spd = 1;
+            st->done = 1;
+        } else {
+            st->alpha = st->rz / tot[0];
+        }
+    }
+}
+
+// row R -> (owner slot, second slot or -1), from the element-major rows
+__global__ void __launch_bounds__(256)
+    em_row_slots_k(int64_t ne, const int32_t* __restrict__ slot_mrow, const int32_t* __restrict__ slot_mate,
+                   int2* __restrict__ row_slots) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
+        const int4 rw4 = __ldg(reinterpret_cast<const int4*>(slot_mrow) + t);
+        const int4 m4 = __ldg(reinterpret_cast<const int4*>(slot_mate) + t);
+        const int32_t rw[4] = {rw4.x, rw4.y, rw4.z, rw4.w}, mt[4] = {m4.x, m4.y, m4.z, m4.w};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (rw[r] < 0) continue;
+            const int32_t slot = (int32_t)(4 * t + r);
+            const bool owner = mt[r] < 0 || mt[r] > slot;
+            if (owner) row_slots[rw[r]] = make_int2(slot, mt[r] < 0 ? -1 : mt[r]);
         }
     }
 }
@@ -337,3 +432,38 @@ extern "C" int phfem_gpu_cg_iterations(int n, int64_t l, const int32_t* sell_col
     return (int)cudaGetLastError();
 }
 
+
+extern "C" int phfem_gpu_cg_em_rows(int64_t ne, const int32_t* slot_mrow, const int32_t* slot_mate, int32_t* row_slots,
+                                    void* stream) {
+    if (ne == 0) return 0;
+    em_row_slots_k<<<grid_for(ne, 256), 256, 0, (cudaStream_t)stream>>>(ne, slot_mrow, slot_mate,
+                                                                        reinterpret_cast<int2*>(row_slots));
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_cg_em_init(int64_t l, const double* diag, const double* b, double* x, double* r, double* p,
+                                    double* d, double tol, double abs_tol, long long max_iter, phg_cg_state* st,
+                                    double* partials, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(st, 0, sizeof(phg_cg_state), s);
+    cg_init<<<cg_grid(l), kThreads, 0, s>>>(l, ArrDiag{diag}, b, x, r, p, d, tol, abs_tol, max_iter, st, partials);
+    phg::count_launches(1);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int phfem_gpu_cg_em_iterations(int n, int64_t l, const int32_t* row_slots, const double* st_val,
+                                          const int32_t* slot_mrow, const double* diag, double* x, double* r,
+                                          double* p, double* q, const double* d, phg_cg_state* st, double* partials,
+                                          void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const int g = cg_grid(l);
+    for (int i = 0; i < n; ++i) {
+        cg_spmv_em<<<g, kThreads, 0, s>>>(l, reinterpret_cast<const int2*>(row_slots), st_val, slot_mrow, diag, p, q,
+                                          st, partials);
+        cg_update<<<g, kThreads, 0, s>>>(l, r, q, d, st, partials);
+        cg_pdir<<<g, kThreads, 0, s>>>(l, x, r, p, d, st);
+    }
+    phg::count_launches(3 * n);
+    return (int)cudaGetLastError();
+}

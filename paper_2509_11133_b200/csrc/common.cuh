@@ -140,6 +140,12 @@ __device__ __forceinline__ int tv(const int4& t, int i) {
     return i == 0 ? t.x : (i == 1 ? t.y : (i == 2 ? t.z : t.w));
 }
 
+// Element-major Schur blocks (assemble.cu's SchurOut::st_val, read by the
+// CG): S_T[r][q], r <= q, 10 values per element in 32-element AoSoA chunks.
+__device__ __forceinline__ int64_t st_idx(int64_t t, int j) { return (t >> 5) * 320 + j * 32 + (t & 31); }
+// (r, q), r <= q -> 0..9: (0,0..3) 0-3, (1,1..3) 4-6, (2,2..3) 7-8, (3,3) 9
+__host__ __device__ constexpr int st_pair(int r, int q) { return r == 0 ? q : (r == 1 ? q + 3 : (r == 2 ? q + 5 : 9)); }
+
 // ----------------------------------------------------------- error reporting
 // Device error slots, each holding the minimum offending key (ULLONG_MAX =
 // none); the host replays them in the reference's check order.

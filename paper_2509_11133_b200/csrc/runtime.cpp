@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -373,25 +374,40 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
     DBuf<double> partials(2 * 148 * 8 + 64);
     Timer tm;
     tm.start();
-    // the CG streams S by rows: an element-major system is laid out as SELL
-    // once here (S_T's upper triangle mirrored; an element-major SpMV with
-    // atomics measured slower)
-    DBuf<int32_t> tmp_col;
+    // An element-major system is streamed by rows straight from its blocks
+    // (cg_spmv_em: per row its two slots, the elements' off-diagonal values
+    // and row ids gathered); PHFEM_CG_SELL=1 lays it out as SELL-32 once
+    // instead (S_T's upper triangle mirrored; the same iterates bit for bit).
+    // A SELL system (exports) is streamed as it is.
+    static const bool force_sell = [] {
+        const char* e = std::getenv("PHFEM_CG_SELL");
+        return e && std::atoi(e) != 0;
+    }();
+    const bool em = sys.elem && !force_sell;
+    DBuf<int32_t> tmp_col, row_slots;
     DBuf<double> tmp_val;
     const int32_t* sell_col = sys.sell_col.p;
     const double* sell_val = sys.sell_val.p;
-    if (sys.elem) {
-        tmp_col.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
-        tmp_val.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
-        check(phfem_gpu_elem_to_sell(m.ne, l, sys.st_val.p, sys.slot_mrow.p, c.slot_mate.p, sys.diag.p, tmp_col.p,
-                                     tmp_val.p, SV()),
-              "elem to sell");
-        sell_col = tmp_col.p;
-        sell_val = tmp_val.p;
+    if (em) {
+        row_slots.alloc(2 * l);
+        check(phfem_gpu_cg_em_rows(m.ne, sys.slot_mrow.p, c.slot_mate.p, row_slots.p, SV()), "cg rows");
+        check(phfem_gpu_cg_em_init(l, sys.diag.p, sys.rhs_neg.p, out.lambda.p, r.p, p.p, d.p, tol, abs_tol, mi,
+                                   state.p, partials.p, SV()),
+              "cg init");
+    } else {
+        if (sys.elem) {
+            tmp_col.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
+            tmp_val.alloc(sys.nchunks * PHG_SELL_C * PHG_SELL_W);
+            check(phfem_gpu_elem_to_sell(m.ne, l, sys.st_val.p, sys.slot_mrow.p, c.slot_mate.p, sys.diag.p,
+                                         tmp_col.p, tmp_val.p, SV()),
+                  "elem to sell");
+            sell_col = tmp_col.p;
+            sell_val = tmp_val.p;
+        }
+        check(phfem_gpu_cg_init(l, sell_col, sell_val, sys.rhs_neg.p, out.lambda.p, r.p, p.p, d.p, tol, abs_tol,
+                                mi, state.p, partials.p, SV()),
+              "cg init");
     }
-    check(phfem_gpu_cg_init(l, sell_col, sell_val, sys.rhs_neg.p, out.lambda.p, r.p, p.p, d.p, tol, abs_tol, mi,
-                            state.p, partials.p, SV()),
-          "cg init");
     phg_cg_state hs{};
     phg_cg_state* pinned = nullptr;
     check(cudaMallocHost(reinterpret_cast<void**>(&pinned), sizeof(phg_cg_state)), "pinned alloc");
@@ -407,8 +423,12 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
         hs = *pinned;
         if (!hs.done) {
             check(cudaStreamBeginCapture(S(), cudaStreamCaptureModeThreadLocal), "capture");
-            phfem_gpu_cg_iterations(batch, l, sell_col, sell_val, out.lambda.p, r.p, p.p, q.p, d.p, state.p,
-                                    partials.p, SV());
+            if (em)
+                phfem_gpu_cg_em_iterations(batch, l, row_slots.p, sys.st_val.p, sys.slot_mrow.p, sys.diag.p,
+                                           out.lambda.p, r.p, p.p, q.p, d.p, state.p, partials.p, SV());
+            else
+                phfem_gpu_cg_iterations(batch, l, sell_col, sell_val, out.lambda.p, r.p, p.p, q.p, d.p, state.p,
+                                        partials.p, SV());
             check(cudaStreamEndCapture(S(), &graph), "capture end");
             check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
             for (;;) {
