@@ -17,6 +17,7 @@
 // The directed edge-pair map (E2T) is never materialised; its only check
 // (two elements claiming the same oriented face) is the orientation test in 2.
 #include <climits>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -484,6 +485,158 @@ __global__ void __launch_bounds__(32 * kFastWarps)
             I2[u] = I3[u];
             T1[u] = T2[u];
         }
+    }
+}
+
+// The first pass without hash tables: stars of <= 32 incidences, one per
+// lane.  A vertex's edge candidates go to two lists by one hash bit of the
+// other vertex b (so equal keys share a list) and its face candidates to a
+// third; with every list <= 32 entries, one warp-wide match per list groups
+// equal keys (__match_any_sync), the group minimum is a warp reduction
+// (__reduce_min_sync) and a face's mate the other lane of its pair
+// (__shfl_sync) -- no shared-memory table to probe, fill or reset.  A vertex
+// with a longer list is deferred to the hashing pass (star_groups_warp<2>).
+constexpr int kMatchWarps = 8;
+#ifndef PHG_MATCH_MINB
+#define PHG_MATCH_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
+    star_groups_match(int64_t nv, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
+                      const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
+                      int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
+                      int32_t* __restrict__ defer_count, unsigned long long* err) {
+    __shared__ int2 s_e[kMatchWarps][2][32];  // (b, edge slot) by hash bit of b
+    __shared__ int4 s_f[kMatchWarps][32];     // (lo, hi, face slot, orientation)
+    __shared__ int32_t s_min[kMatchWarps][32];  // edge group minimum at the group's first lane
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* gmin = s_min[warp];
+    const unsigned lt = (1u << lane) - 1u;
+    int2* e0 = s_e[warp][0];
+    int2* e1 = s_e[warp][1];
+    int4* fl = s_f[warp];
+    const bool do_faces = slot_mate != nullptr;
+    const int64_t nwarps = (int64_t)gridDim.x * kMatchWarps;
+    // software pipeline of the dependent loads star_ptr -> star -> tets, as
+    // in star_groups_warp
+    struct Ptr {
+        int32_t v;
+        int64_t beg, end;
+    };
+    auto load_ptr = [&](int64_t i) -> Ptr {
+        Ptr P{-1, 0, 0};
+        if (i < nv) {
+            P.v = (int32_t)i;
+            P.beg = star_ptr[i];
+            P.end = star_ptr[i + 1];
+        }
+        return P;
+    };
+    auto load_inc = [&](const Ptr& P) -> int32_t {
+        const int64_t m = P.end - P.beg;
+        return lane < m && m <= 32 ? __ldg(star + P.beg + lane) : -1;
+    };
+    auto load_tet = [&](int32_t inc) -> int4 { return inc >= 0 ? ldtet(tets, inc >> 2) : make_int4(0, 0, 0, 0); };
+    const int64_t it0 = (int64_t)blockIdx.x * kMatchWarps + warp;
+    Ptr P1 = load_ptr(it0), P2 = load_ptr(it0 + nwarps);
+    int32_t I1 = load_inc(P1);
+    int4 T1 = load_tet(I1);
+    int32_t I2 = load_inc(P2);
+    Ptr P3 = load_ptr(it0 + 2 * nwarps);
+    for (int64_t it = it0; it < nv; it += nwarps) {
+        const Ptr P4 = load_ptr(it + 3 * nwarps);
+        const int32_t I3 = load_inc(P3);
+        const int4 T2 = load_tet(I2);
+        const int32_t v = P1.v;
+        const int m = (int)(P1.end - P1.beg);
+        bool defer = m > 32;
+        if (!defer) {
+            const bool valid = lane < m;
+            const int32_t t = valid ? I1 >> 2 : 0;
+            const int lv = valid ? I1 & 3 : 0;
+            const int4 tet = T1;
+            const int32_t o[3] = {lv == 0 ? tet.y : tet.x, lv <= 1 ? tet.z : tet.y, lv <= 2 ? tet.w : tet.z};
+            const unsigned etab = (unsigned)(0xb15663088ull >> (9 * lv));
+            const unsigned ktab = (unsigned)(0x9c72c9u >> (6 * lv)) & 63u;
+            int n0 = 0, n1 = 0, nf = 0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const int32_t b = o[i];
+                const bool q = valid && b > v;
+                const bool hb = (hash32((uint32_t)b) >> 31) != 0;
+                const unsigned bal0 = __ballot_sync(0xffffffffu, q && !hb), bal1 = __ballot_sync(0xffffffffu, q && hb);
+                const int pe = (hb ? n1 + __popc(bal1 & lt) : n0 + __popc(bal0 & lt));
+                if (q && pe < 32) (hb ? e1 : e0)[pe] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
+                n0 += __popc(bal0);
+                n1 += __popc(bal1);
+                if (do_faces) {
+                    const int32_t a = o[(i + 1) % 3], c = o[(i + 2) % 3];
+                    const int32_t lo = min(a, c), hi = max(a, c);
+                    const bool qf = valid && lo > v;
+                    const unsigned balf = __ballot_sync(0xffffffffu, qf);
+                    const bool xy = (lv & 1) ? c < a : a < c;
+                    const int pf = nf + __popc(balf & lt);
+                    if (qf && pf < 32) fl[pf] = make_int4(lo, hi, 4 * t + (int)((ktab >> (2 * i)) & 3u), xy ? 1 : 0);
+                    nf += __popc(balf);
+                }
+            }
+            __syncwarp();
+            defer = n0 > 32 || n1 > 32 || nf > 32;
+            if (!defer) {
+                // one match per list over its own lanes (match_any costs
+                // grow with the distinct keys among the participating lanes:
+                // padding lanes with unique keys made it 1.7x slower)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int n = h ? n1 : n0;
+                    if (lane < n) {
+                        const int2 c = (h ? e1 : e0)[lane];
+                        const unsigned mk = n == 32 ? 0xffffffffu : (1u << n) - 1u;
+                        const unsigned g = __match_any_sync(mk, c.x);
+                        // the group minimum through a shared-memory min at the
+                        // group's first lane (__reduce_min_sync over the
+                        // warp's distinct group masks ran as a loop, a
+                        // quarter of the kernel)
+                        const int lead = __ffs(g) - 1;
+                        gmin[lane] = INT_MAX;
+                        __syncwarp(mk);
+                        atomicMin(gmin + lead, c.y);
+                        __syncwarp(mk);
+                        const int32_t first = gmin[lead];
+                        PHG_CHECK(first <= c.y && first >= 0);
+                        edge_first[c.y] = first;
+                    }
+                    __syncwarp();
+                }
+                if (lane < nf) {
+                    const int4 c = fl[lane];
+                    const unsigned mk = nf == 32 ? 0xffffffffu : (1u << nf) - 1u;
+                    const unsigned long long key = (unsigned long long)c.x << 32 | (uint32_t)c.y;
+                    const unsigned g = __match_any_sync(mk, key);
+                    const unsigned others = g & ~(1u << lane);
+                    const int src = others ? __ffs(others) - 1 : lane;
+                    const int32_t oslot = __shfl_sync(mk, c.z, src);
+                    const int32_t ow = __shfl_sync(mk, c.w, src);
+                    const int cnt = __popc(g);
+                    if (cnt > 2 || (cnt == 2 && ow == c.w)) {
+                        // same orientation twice: "elements A and B claim the
+                        // same oriented face" (connectivity.cpp:62-68; the
+                        // host names the reference's pair from the E2T)
+                        const unsigned long long a = (unsigned long long)(min(c.z, oslot) >> 2),
+                                                 b = (unsigned long long)(max(c.z, oslot) >> 2);
+                        report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
+                    }
+                    slot_mate[c.z] = cnt >= 2 ? oslot : -1;
+                }
+            }
+            __syncwarp();
+        }
+        if (defer && lane == 0) defer_list[atomicAdd(defer_count, 1)] = v;
+        P1 = P2;
+        P2 = P3;
+        P3 = P4;
+        I1 = I2;
+        I2 = I3;
+        T1 = T2;
     }
 }
 
@@ -1003,16 +1156,29 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
     cudaStream_t s = (cudaStream_t)stream;
     cudaMemsetAsync(defer_count, 0, 3 * sizeof(int32_t), s);
     // one full wave of resident blocks (grid-stride over the vertices)
-    static int resident = 0;
+    static int resident = 0, resident_m = 0, use_match = -1;
+    if (use_match < 0) {
+        const char* e = getenv("PHFEM_GROUPS_HASH");
+        use_match = e && atoi(e) != 0 ? 0 : 1;
+    }
     if (resident == 0) {
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, star_groups_warp<1>, 32 * kFastWarps, 0);
         resident = (per_sm > 0 ? per_sm : 8) * kSMs;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, star_groups_match, 32 * kMatchWarps, 0);
+        resident_m = (per_sm > 0 ? per_sm : 4) * kSMs;
     }
-    const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
-    const int grid = (int)(blocks < resident ? blocks : resident);
-    star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
-                                                         slot_mate, defer_list, defer_count, err);
+    if (use_match) {
+        const int64_t blocks = (nc + kMatchWarps - 1) / kMatchWarps;
+        const int grid = (int)(blocks < resident_m ? blocks : resident_m);
+        star_groups_match<<<grid, 32 * kMatchWarps, 0, s>>>(nc, star_ptr, star, tets, edge_first, slot_mate,
+                                                            defer_list, defer_count, err);
+    } else {
+        const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
+        const int grid = (int)(blocks < resident ? blocks : resident);
+        star_groups_warp<1><<<grid, 32 * kFastWarps, 0, s>>>(nc, nullptr, nullptr, star_ptr, star, tets, edge_first,
+                                                             slot_mate, defer_list, defer_count, err);
+    }
     star_groups_warp<2><<<kSMs * 4, 32 * kFastWarps, 0, s>>>(0, defer_list, defer_count, star_ptr, star, tets,
                                                              edge_first, slot_mate, defer_list + nc,
                                                              defer_count + 1, err);
