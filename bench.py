@@ -136,14 +136,18 @@ def algorithmic_bytes(nc, ne, ned, nf, nb, nnz_s, l, k_coef=0, elem=True):
     """compulsory bytes per stage (int32 ids, fp64 reals,
     int8 sigma, u8 class, int64 row pointers, int32 columns).  The step's
     condensed S is element-major (elem: 10 fp64 S_T values + 4 int32 rows
-    per element and the assembled diagonal) or SELL rows (12 nnz_s); the CG
-    streams SELL rows either way."""
+    per element and the assembled diagonal) or SELL rows (12 nnz_s).  The CG
+    on the element-major S (the pipeline's system) reads per row its two
+    slots and the diagonal (16 l) and per element the six off-diagonal
+    S_T values and four row ids (64 ne); the vectors: p and q in the SpMV
+    (16 l), r, q, d read and r written in the update (32 l), x, p, r, d
+    read and x, p written in the direction update (48 l)."""
     b_edges = 44 * ne + 8 * ned
     b_faces = 60 * ne + 24 * nc + 12 * nb + 33 * nf
     s_out = 96 * ne + 8 * l if elem else 12 * nnz_s
     b_asm = 36 * ne + 24 * nc + 13 * nf + k_coef * ne + s_out + 16 * l + 8
     b_refine = 260 * ne + 48 * nc + 24 * ned + 72 * nb
-    b_cg = 12 * nnz_s + 8 * (l + 1) + 80 * l
+    b_cg = (64 * ne + 16 * l if elem else 12 * nnz_s) + 96 * l
     return dict(connect=b_edges + b_faces, assemble=b_asm, refine=b_refine, cg_iteration=b_cg)
 
 
