@@ -152,7 +152,10 @@ def bipyramid(n: int) -> MeshArrays:
     return MeshArrays(coords, tets, db, np.zeros((0, 3), np.int32))
 
 
-@pytest.mark.parametrize("n", [20, 40, 200])
+# n = 16: a star of 32 incidences whose candidate lists overflow the warp
+# matches (96 edge candidates at the centre) and are deferred to the hashing
+# pass; 20: 40 incidences (hashing warps, two per lane); 40, 200: blocks
+@pytest.mark.parametrize("n", [16, 20, 40, 200])
 def test_high_valence_stars(oracle, n):
     m = bipyramid(n)
     g = to_gpu(m)
