@@ -37,7 +37,9 @@ enum phg_err_slot {
     PHG_ERR_SINGULAR = 4,    /* key = element (solver.cpp:103-109, 128-129) */
     PHG_ERR_BOUNDARY_EDGE = 5, /* key = (list index)<<2 | pair (refine.cpp:80-85) */
     PHG_ERR_VALENCE = 6,     /* key = vertex: star larger than the supported maximum */
-    PHG_ERR_COUNT = 7
+    PHG_ERR_DEGEN_FACE = 7,  /* key = slot 4t+k: a face with a repeated node id, which faces_up never lists
+                                (connectivity.cpp:81-84) and full_face_table cannot match (:140-143) */
+    PHG_ERR_COUNT = 8
 };
 
 #define PHG_SELL_C 32
@@ -353,11 +355,14 @@ int phfem_gpu_sort_within(int64_t n, int64_t nseg, const int64_t* seg_ptr, const
                           int64_t* perm, int64_t* tmp, void* stream);
 
 /* edge_pairs_to_elems (connectivity.cpp:46-70): entry 12 m + 3 k + j of
- * element m (from, to) edge pairs; after seg_sort by `from` with minor `to`,
- * e2t_finish writes the sorted keys (from * ned + to) / elements and
- * atomicMin's the first position j whose key equals key j-1. */
-int phfem_gpu_e2t_entries(int64_t ne, const int32_t* edge_of_slot, int64_t* from, int64_t* to,
-                          void* stream);
+ * element m, the reference's key from * ned + to (uint64, pair_to_edge = -1
+ * for an edge of two equal node ids: edge_nodes, may be NULL for meshes
+ * without) stored as (segment, minor) in [0, ned] x [0, ned]; after seg_sort
+ * by segment (ned + 1 of them) with that minor, e2t_finish writes the sorted
+ * keys / elements and atomicMin's the first position j whose key equals key
+ * j-1. */
+int phfem_gpu_e2t_entries(int64_t ne, int64_t ned, const int32_t* edge_of_slot, const int32_t* edge_nodes,
+                          int64_t* from, int64_t* to, void* stream);
 int phfem_gpu_e2t_finish(int64_t n, int64_t ned, const int64_t* perm, const int64_t* from,
                          const int64_t* to, unsigned long long* key, int32_t* elem,
                          unsigned long long* first_dup, void* stream);

@@ -101,23 +101,45 @@ __global__ void iota_k(int64_t n, int64_t* __restrict__ a) {
 // entries of element m in the reference's order: for each oriented face
 // [x y z] (local faces kFaceVerts) the keys (e_yz, e_xy), (e_zx, e_yz),
 // (e_xy, e_zx) (connectivity.cpp:51-61)
-__global__ void e2t_entries_k(int64_t ne, const int32_t* __restrict__ edge_of_slot, int64_t* __restrict__ from,
+// The reference's key of entry (from, to) is from * ned + to in uint64
+// arithmetic, where pair_to_edge gives -1 for a pair of equal node ids
+// (connectivity.hpp:25-30): such keys wrap.  Each entry is stored as the
+// (segment, minor) pair the sort orders by: (K / ned, K % ned) for K < ned^2,
+// else the extra segment ned with minor K + ned + 1 (K >= 2^64 - ned - 1
+// there), so sorting by (segment, minor, entry) orders the reference's keys
+// as its std::sort of (key, element) pairs does.
+__device__ __forceinline__ void e2t_put(int64_t ned, int32_t f, int32_t t, int64_t* from, int64_t* to) {
+    const unsigned long long K = (unsigned long long)(long long)f * (unsigned long long)ned +
+                                 (unsigned long long)(long long)t;
+    const unsigned long long lim = (unsigned long long)ned * (unsigned long long)ned;
+    if (K < lim) {
+        *from = (int64_t)(K / (unsigned long long)ned);
+        *to = (int64_t)(K % (unsigned long long)ned);
+    } else {
+        *from = ned;
+        *to = (int64_t)(K + (unsigned long long)ned + 1ull);
+    }
+}
+
+__global__ void e2t_entries_k(int64_t ne, int64_t ned, const int32_t* __restrict__ edge_of_slot,
+                              const int32_t* __restrict__ edge_nodes, int64_t* __restrict__ from,
                               int64_t* __restrict__ to) {
     for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < ne; m += (int64_t)gridDim.x * blockDim.x) {
         int32_t e[6];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) e[k] = edge_of_slot[6 * m + k];
+        for (int k = 0; k < 6; ++k) {
+            e[k] = edge_of_slot[6 * m + k];
+            // pair_to_edge(a, a) == -1 (an element with a repeated node id)
+            if (edge_nodes && e[k] >= 0 && edge_nodes[2 * (int64_t)e[k]] == edge_nodes[2 * (int64_t)e[k] + 1]) e[k] = -1;
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int x = face_vert(k, 0), y = face_vert(k, 1), z = face_vert(k, 2);
             const int32_t exy = e[edge_index(x, y)], eyz = e[edge_index(y, z)], ezx = e[edge_index(z, x)];
             const int64_t o = 12 * m + 3 * k;
-            from[o] = eyz;
-            to[o] = exy;
-            from[o + 1] = ezx;
-            to[o + 1] = eyz;
-            from[o + 2] = exy;
-            to[o + 2] = ezx;
+            e2t_put(ned, eyz, exy, from + o, to + o);
+            e2t_put(ned, ezx, eyz, from + o + 1, to + o + 1);
+            e2t_put(ned, exy, ezx, from + o + 2, to + o + 2);
         }
     }
 }
@@ -130,7 +152,9 @@ __global__ void e2t_finish_k(int64_t n, int64_t ned, const int64_t* __restrict__
                              unsigned long long* __restrict__ first_dup) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = perm[j];
-        const unsigned long long k = (unsigned long long)from[i] * (unsigned long long)ned + (unsigned long long)to[i];
+        const unsigned long long k =
+            from[i] < ned ? (unsigned long long)from[i] * (unsigned long long)ned + (unsigned long long)to[i]
+                          : (unsigned long long)to[i] - (unsigned long long)ned - 1ull;
         key[j] = k;
         elem[j] = (int32_t)(i / 12);
         if (j > 0) {
@@ -883,9 +907,10 @@ extern "C" int phfem_gpu_sort_within(int64_t n, int64_t nseg, const int64_t* seg
     return (int)cudaGetLastError();
 }
 
-extern "C" int phfem_gpu_e2t_entries(int64_t ne, const int32_t* edge_of_slot, int64_t* from, int64_t* to,
-                                     void* stream) {
-    if (ne > 0) e2t_entries_k<<<blocks_for(ne), kT, 0, (cudaStream_t)stream>>>(ne, edge_of_slot, from, to);
+extern "C" int phfem_gpu_e2t_entries(int64_t ne, int64_t ned, const int32_t* edge_of_slot, const int32_t* edge_nodes,
+                                     int64_t* from, int64_t* to, void* stream) {
+    if (ne > 0)
+        e2t_entries_k<<<blocks_for(ne), kT, 0, (cudaStream_t)stream>>>(ne, ned, edge_of_slot, edge_nodes, from, to);
     phg::count_launches(1);
     return (int)cudaGetLastError();
 }

@@ -130,6 +130,24 @@ __device__ __forceinline__ void face_other(const int4& tet, int k, int lv, int32
 // the local face opposite local vertex lv
 __device__ __forceinline__ int opposite_face(int lv) { return lv == 0 ? 3 : (lv == 3 ? 0 : lv); }
 
+// Elements with a repeated node id (the reference accepts them up to the
+// face table).  Their edge (v, v) is an edge like any other
+// (connectivity.cpp:22-37 keys it (v, v)): it is grouped at v and listed
+// from the incidence with the larger local index of the pair, which is in
+// the star whenever the pair holds the element's largest id.  A face with a
+// repeated id matches only itself in the E2T map, so faces_up never lists it
+// (connectivity.cpp:78-84) and full_face_table fails on it (:140-143); so
+// does a face whose two sides are faces of one element.  Such a slot gets
+// the mate kDegenerate (not an owner, no face id) and is reported.
+constexpr int32_t kDegenerate = -2;
+__device__ __forceinline__ bool edge_here(int32_t b, int32_t v, int w, int lv) {
+    return b > v || (b == v && w < lv);
+}
+__device__ __forceinline__ void mark_degenerate(int32_t* slot_mate, int32_t slot, unsigned long long* err) {
+    slot_mate[slot] = kDegenerate;
+    report(err, PHG_ERR_DEGEN_FACE, (unsigned long long)slot);
+}
+
 // One group (a warp, or a whole block for big stars) processes vertex v.
 template <int NT, typename Sync>
 __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int32_t* __restrict__ star,
@@ -149,7 +167,7 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
             const int4 tet = ldtet(tets, t);
             for (int w = 0; w < 4; ++w) {
                 const int32_t b = tv(tet, w);
-                if (w == lv || b <= v) continue;
+                if (w == lv || !edge_here(b, v, w, lv)) continue;
                 const int h = edge_slot_insert(ekey, mask, b);
                 atomicMin(eval + h, (int32_t)(6 * t + edge_index(lv, w)));
             }
@@ -162,7 +180,7 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
             const int4 tet = ldtet(tets, t);
             for (int w = 0; w < 4; ++w) {
                 const int32_t b = tv(tet, w);
-                if (w == lv || b <= v) continue;
+                if (w == lv || !edge_here(b, v, w, lv)) continue;
                 edge_first[6 * t + edge_index(lv, w)] = eval[edge_slot_find(ekey, mask, b)];
             }
         }
@@ -186,7 +204,11 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
                 if (k == opp) continue;
                 int32_t x, y;
                 face_other(tet, k, lv, x, y);
-                if (x <= v || y <= v) continue;
+                if (x == v || y == v || x == y) {
+                    mark_degenerate(slot_mate, (int32_t)(4 * t + k), err);
+                    continue;
+                }
+                if (x < v || y < v) continue;
                 const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
                                                      : ((unsigned long long)y << 32 | (uint32_t)x);
                 const int h = face_slot_insert(ft.key, mask, key);
@@ -208,7 +230,7 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
                 if (k == opp) continue;
                 int32_t x, y;
                 face_other(tet, k, lv, x, y);
-                if (x <= v || y <= v) continue;
+                if (x <= v || y <= v || x == y) continue;
                 const unsigned long long key = x < y ? ((unsigned long long)x << 32 | (uint32_t)y)
                                                      : ((unsigned long long)y << 32 | (uint32_t)x);
                 const int h = face_slot_find(ft.key, mask, key);
@@ -222,7 +244,10 @@ __device__ void group_vertex(int32_t v, int64_t beg, int m, int rank, const int3
                     const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
                     report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                 }
-                slot_mate[slot] = count >= 2 ? (slot == lo ? hi : lo) : -1;
+                if (count == 2 && lo >> 2 == hi >> 2)
+                    mark_degenerate(slot_mate, slot, err);  // both sides in one element
+                else
+                    slot_mate[slot] = count >= 2 ? (slot == lo ? hi : lo) : -1;
             }
         }
         sync();
@@ -372,7 +397,7 @@ __global__ void __launch_bounds__(32 * kFastWarps)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int32_t b = o[i];
-                const bool q = valid && b > v;
+                const bool q = valid && (b > v || (b == v && i < lv));
                 const unsigned bal = __ballot_sync(0xffffffffu, q);
                 const int pe = ne_l + __popc(bal & lt);
                 if (q && pe < LCAP) el[pe] = make_int2(b, 6 * t + (int)((etab >> (3 * i)) & 7u));
@@ -383,7 +408,8 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     // oriented cycle is a for even lv, b for odd lv
                     const int32_t a = o[(i + 1) % 3], b = o[(i + 2) % 3];
                     const int32_t lo = min(a, b), hi = max(a, b);
-                    const bool qf = valid && lo > v;
+                    if (valid && (lo == v || a == b)) mark_degenerate(slot_mate, 4 * t + (int)((ktab >> (2 * i)) & 3u), err);
+                    const bool qf = valid && lo > v && a != b;
                     const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     // count in bits 2+, orientation (x < y: 1, else 2) below:
                     // exactly one slot of each orientation sums to 11
@@ -456,7 +482,10 @@ __global__ void __launch_bounds__(32 * kFastWarps)
                     const unsigned long long a = (unsigned long long)(lo >> 2), b = (unsigned long long)(hi >> 2);
                     report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                 }
-                slot_mate[slot] = cnt >= 2 ? (slot == pr.x ? pr.y : pr.x) : -1;
+                if (cnt == 2 && pr.x >> 2 == pr.y >> 2)
+                    mark_degenerate(slot_mate, slot, err);  // both sides in one element
+                else
+                    slot_mate[slot] = cnt >= 2 ? (slot == pr.x ? pr.y : pr.x) : -1;
             }
         }
         __syncwarp();
@@ -561,7 +590,7 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int32_t b = o[i];
-                const bool q = valid && b > v;
+                const bool q = valid && (b > v || (b == v && i < lv));
                 const bool hb = (hash32((uint32_t)b) >> 31) != 0;
                 const unsigned bal0 = __ballot_sync(0xffffffffu, q && !hb), bal1 = __ballot_sync(0xffffffffu, q && hb);
                 const int pe = (hb ? n1 + __popc(bal1 & lt) : n0 + __popc(bal0 & lt));
@@ -571,7 +600,8 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
                 if (do_faces) {
                     const int32_t a = o[(i + 1) % 3], c = o[(i + 2) % 3];
                     const int32_t lo = min(a, c), hi = max(a, c);
-                    const bool qf = valid && lo > v;
+                    if (valid && (lo == v || a == c)) mark_degenerate(slot_mate, 4 * t + (int)((ktab >> (2 * i)) & 3u), err);
+                    const bool qf = valid && lo > v && a != c;
                     const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     const bool xy = (lv & 1) ? c < a : a < c;
                     const int pf = nf + __popc(balf & lt);
@@ -625,7 +655,10 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
                                                  b = (unsigned long long)(max(c.z, oslot) >> 2);
                         report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                     }
-                    slot_mate[c.z] = cnt >= 2 ? oslot : -1;
+                    if (cnt == 2 && oslot >> 2 == c.z >> 2)
+                        mark_degenerate(slot_mate, c.z, err);  // both sides in one element
+                    else
+                        slot_mate[c.z] = cnt >= 2 ? oslot : -1;
                 }
             }
             __syncwarp();
@@ -728,7 +761,7 @@ __global__ void __launch_bounds__(256)
 
 // -------------------------------------------------------------- numbering
 
-__device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mate < 0 || mate > s; }
+__device__ __forceinline__ bool face_owner(int32_t s, int32_t mate) { return mate == -1 || mate > s; }
 
 // Per-element masks of first-occurrence edge slots (bits 0-5) and owned face
 // slots (bits 6-9) and the exclusive offsets edge_off / face_off [ne + 1] of
@@ -919,6 +952,10 @@ __global__ void __launch_bounds__(256)
                 if (len == 0.0) report(err, PHG_ERR_FACE, (unsigned long long)id << 2 | 0);
                 face_area[id] = mul(0.5, len);
                 ++id;
+            } else if (mate == kDegenerate) {
+                // a face with a repeated node id: no face (the pass reports it)
+                fid[k] = -1;
+                sg[k] = 0;
             } else {
                 // the owner is slot `mate` of an earlier element g: its rank
                 // among g's owned slots (sigma = -1: opposite orientation,

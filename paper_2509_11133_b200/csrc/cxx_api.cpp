@@ -458,13 +458,15 @@ EdgePairToElem edge_pairs_to_elems(const Mesh& mesh, const EdgeTable& edges) {
     const int64_t ne = mesh.num_elems(), n = 12 * ne, ned = c.ned;
     EdgePairToElem map;
     map.n_edges = ned;
-    DBuf<int64_t> from(n > 0 ? n : 1), to(n > 0 ? n : 1), seg_ptr(ned + 1), perm(n > 0 ? n : 1), tmp(n > 0 ? n : 1);
-    DBuf<int32_t> cnt(ned > 0 ? ned : 1), elem(n > 0 ? n : 1);
+    // ned + 1 segments: the last holds the keys that wrap (phfem_gpu_e2t_entries)
+    DBuf<int64_t> from(n > 0 ? n : 1), to(n > 0 ? n : 1), seg_ptr(ned + 2), perm(n > 0 ? n : 1), tmp(n > 0 ? n : 1);
+    DBuf<int32_t> cnt(ned + 1), elem(n > 0 ? n : 1);
     DBuf<unsigned long long> key(n > 0 ? n : 1), dup(1);
     DBuf<unsigned char> ss;
     dup.fill_bytes(0xff);
-    check(phfem_gpu_e2t_entries(ne, c.edge_of_slot.p, from.p, to.p, phb::SV()), "e2t entries");
-    check(phfem_gpu_seg_sort(n, ned, from.p, to.p, seg_ptr.p, perm.p, cnt.p, tmp.p, scan_scratch(ss, ned), phb::SV()),
+    check(phfem_gpu_e2t_entries(ne, ned, c.edge_of_slot.p, c.edge_nodes.p, from.p, to.p, phb::SV()), "e2t entries");
+    check(phfem_gpu_seg_sort(n, ned + 1, from.p, to.p, seg_ptr.p, perm.p, cnt.p, tmp.p, scan_scratch(ss, ned + 1),
+                             phb::SV()),
           "e2t sort");
     check(phfem_gpu_e2t_finish(n, ned, perm.p, from.p, to.p, key.p, elem.p, dup.p, phb::SV()), "e2t finish");
     const unsigned long long j = get1(dup.p);
@@ -1499,13 +1501,14 @@ namespace phb {
 bool e2t_first_duplicate(const MeshData& m, const Connectivity& c, int32_t& a, int32_t& b) {
     const int64_t ne = m.ne, n = 12 * ne, ned = c.ned;
     if (!c.has_edges || n == 0) return false;
-    DBuf<int64_t> from(n), to(n), seg_ptr(ned + 1), perm(n), tmp(n);
-    DBuf<int32_t> cnt(ned > 0 ? ned : 1), elem(n);
+    // ned + 1 segments: the last holds the keys that wrap (phfem_gpu_e2t_entries)
+    DBuf<int64_t> from(n), to(n), seg_ptr(ned + 2), perm(n), tmp(n);
+    DBuf<int32_t> cnt(ned + 1), elem(n);
     DBuf<unsigned long long> key(n), dup(1);
-    DBuf<unsigned char> ss(phfem_gpu_scan_scratch(ned > 0 ? ned : 1));
+    DBuf<unsigned char> ss(phfem_gpu_scan_scratch(ned + 1));
     dup.fill_bytes(0xff);
-    check(phfem_gpu_e2t_entries(ne, c.edge_of_slot.p, from.p, to.p, SV()), "e2t entries");
-    check(phfem_gpu_seg_sort(n, ned, from.p, to.p, seg_ptr.p, perm.p, cnt.p, tmp.p, ss.p, SV()), "e2t sort");
+    check(phfem_gpu_e2t_entries(ne, ned, c.edge_of_slot.p, c.edge_nodes.p, from.p, to.p, SV()), "e2t entries");
+    check(phfem_gpu_seg_sort(n, ned + 1, from.p, to.p, seg_ptr.p, perm.p, cnt.p, tmp.p, ss.p, SV()), "e2t sort");
     check(phfem_gpu_e2t_finish(n, ned, perm.p, from.p, to.p, key.p, elem.p, dup.p, SV()), "e2t finish");
     unsigned long long j;
     check(cudaMemcpyAsync(&j, dup.p, sizeof j, cudaMemcpyDeviceToHost, S()), "D2H");

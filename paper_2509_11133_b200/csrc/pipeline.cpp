@@ -51,16 +51,34 @@ void replay_connectivity_errors(const std::vector<unsigned long long>& e, const 
                                 int upto = 3) {
     // (PHG_ERR_VALENCE is not an error: those stars took the global path)
     if (upto < 2) return;
-    if (e[PHG_ERR_DUP_ORIENT] != kNone) {
+    const bool degen = e[PHG_ERR_DEGEN_FACE] != kNone;
+    if (e[PHG_ERR_DUP_ORIENT] != kNone || degen) {
         // the reference names the first repeated key of its sorted E2T
         // entries: build that map on this error path to name the same pair
+        // (faces with a repeated node id register their own keys there, so
+        // their elements are checked the same way)
         const unsigned long long k = e[PHG_ERR_DUP_ORIENT];
         int32_t a = (int32_t)(k >> 32), b = (int32_t)(k & 0xffffffffull);
-        e2t_first_duplicate(m, c, a, b);
-        throw MeshError("inconsistent mesh: elements " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
-                        " claim the same oriented face");
+        if (e2t_first_duplicate(m, c, a, b) || !degen)
+            throw MeshError("inconsistent mesh: elements " + std::to_string(a + 1) + " and " + std::to_string(b + 1) +
+                            " claim the same oriented face");
     }
     if (upto < 3) return;
+    if (degen) {
+        // full_face_table's element loop (connectivity.cpp:136-143): the
+        // first slot whose oriented face is not in faces_up's list is the
+        // first face with a repeated node id
+        const int64_t slot = (int64_t)e[PHG_ERR_DEGEN_FACE];
+        const int64_t t = slot >> 2;
+        const int k = (int)(slot & 3);
+        int32_t tet[4];
+        check(cudaMemcpyAsync(tet, m.tets.p + 4 * t, sizeof tet, cudaMemcpyDeviceToHost, S()), "D2H");
+        sync();
+        static const int fv[4][3] = {{0, 1, 2}, {0, 2, 3}, {0, 3, 1}, {3, 2, 1}};  // elem_oriented_faces
+        const int32_t f[3] = {tet[fv[k][0]], tet[fv[k][1]], tet[fv[k][2]]};
+        throw MeshError("inconsistent mesh: face " + tri_str(f) + " of element " + std::to_string(t + 1) +
+                        " matches no unique face");
+    }
     if (e[PHG_ERR_CLASSIFY] != kNone) {
         const int64_t i = (int64_t)(e[PHG_ERR_CLASSIFY] >> 2);
         const int kind = (int)(e[PHG_ERR_CLASSIFY] & 3);
@@ -249,9 +267,9 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
     }
     check(phfem_gpu_classify_check(m.nd, m.nn, c.entry_face.p, w.claim.p, w.err.p, SV()), "classify check");
     if (closed_rows) {
-        static_assert(PHG_ERR_COUNT == 7, "error slots");
-        const auto e = read_many<unsigned long long, 7>(
-            {w.err.p, w.err.p + 1, w.err.p + 2, w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6});
+        static_assert(PHG_ERR_COUNT == 8, "error slots");
+        const auto e = read_many<unsigned long long, 8>(
+            {w.err.p, w.err.p + 1, w.err.p + 2, w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6, w.err.p + 7});
         replay_connectivity_errors(std::vector<unsigned long long>(e.begin(), e.end()), m, c);
         c.n_dir = m.nd;
         c.n_neu = m.nn;
@@ -284,10 +302,10 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
           "face class");
     // the class counts and every connectivity error slot in one read (face
     // rows below report nothing)
-    static_assert(PHG_ERR_COUNT == 7, "error slots");
-    const auto cnt = read_many<unsigned long long, 11>(
+    static_assert(PHG_ERR_COUNT == 8, "error slots");
+    const auto cnt = read_many<unsigned long long, 12>(
         {w.counts.p, w.counts.p + 1, w.counts.p + 2, w.counts.p + 3, w.err.p, w.err.p + 1, w.err.p + 2,
-         w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6});
+         w.err.p + 3, w.err.p + 4, w.err.p + 5, w.err.p + 6, w.err.p + 7});
     replay_connectivity_errors(std::vector<unsigned long long>(cnt.begin() + 4, cnt.end()), m, c);
     c.n_int = (int64_t)cnt[0];
     c.n_dir = (int64_t)cnt[1];

@@ -542,3 +542,39 @@ def test_high_valence_star(oracle, k):
     mg = from_gpu(g)
     for key in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
+
+
+def _degenerate_cases():
+    """Elements with a repeated node id (the reference accepts them up to its
+    face table): a repeated smaller id, a repeated largest id (its face and
+    that face's reverse in one element), a degenerate face shared by two
+    elements, a triple id, a repeated id at local positions 1 and 2."""
+    coords = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]], float)
+    e = np.zeros((0, 3), np.int32)
+    tets = [[[0, 1, 2, 3], [1, 1, 2, 4]], [[0, 1, 2, 3], [1, 2, 4, 4]], [[1, 1, 2, 3], [1, 1, 2, 4]],
+            [[0, 1, 2, 3], [4, 4, 4, 1]], [[0, 1, 2, 3], [2, 1, 1, 4]]]
+    return [MeshArrays(coords, np.array(t, np.int32), e, e, 0) for t in tets]
+
+
+@pytest.mark.parametrize("case", range(5))
+def test_repeated_node_ids_match_oracle(oracle, case):
+    """one red refinement (it needs only the edge numbering, in which an edge
+    (a, a) is numbered like any other: the new nodes follow it) and the face
+    table's error (E2T duplicate or "matches no unique face", with the
+    oracle's element pair / face) on meshes whose elements repeat a node id;
+    the star grouping must not leave slots unwritten there.  (The edge table
+    alone is the C++ API's num_edges; the C ABI's counts need the face table,
+    which fails for these meshes in the reference too.)"""
+    from oracle_bind import CheckerError
+    m = _degenerate_cases()[case]
+    g = to_gpu(m)
+    with pytest.raises(CheckerError) as eo:
+        oracle.faces(m)
+    with pytest.raises(ph.MeshError) as eg:
+        to_gpu(m).faces()
+    assert eg.value.msg == eo.value.msg
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(mo, k)), k

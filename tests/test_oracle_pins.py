@@ -321,3 +321,31 @@ def test_streaming_digests_match_full_tables(oracle):
             assert hashlib.sha256(np.ascontiguousarray(v).tobytes()).hexdigest() == d[k], k
         assert oracle.sha256(en) == hashlib.sha256(en.tobytes()).hexdigest()
         m = oracle.refine(m)[0]
+
+
+@needs_ref
+def test_repeated_node_ids_match_reference(oracle):
+    """Elements with a repeated node id (the cases of
+    test_gpu_parity.test_repeated_node_ids_match_oracle): the oracle's edge
+    table, E2T keys (pair_to_edge(a, a) = -1 wraps the reference's uint64
+    keys) and face-table error equal the reference's."""
+    coords = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 1, 1]], float)
+    e = np.zeros((0, 3), np.int32)
+    for t in ([[0, 1, 2, 3], [1, 1, 2, 4]], [[0, 1, 2, 3], [1, 2, 4, 4]], [[1, 1, 2, 3], [1, 1, 2, 4]],
+              [[0, 1, 2, 3], [4, 4, 4, 1]], [[0, 1, 2, 3], [2, 1, 1, 4]]):
+        m = MeshArrays(coords, np.array(t, np.int32), e, e, 0)
+        r = RefCtx(m)
+        with pytest.raises(CheckerError) as er:
+            r.connectivity()
+        with pytest.raises(CheckerError) as eo:
+            oracle.faces(m)
+        assert er.value.msg == eo.value.msg
+        en_o, _ = oracle.edges(m)
+        r2 = RefCtx(m)
+        r2.num_edges()
+        en_r, _ = r2.edges()
+        assert np.array_equal(en_o, en_r)
+        if "claim the same oriented face" not in er.value.msg:
+            kr, elr = r.e2t()
+            ko, elo = oracle.e2t(m)
+            assert np.array_equal(kr, ko) and np.array_equal(elr, elo)
