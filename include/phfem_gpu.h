@@ -97,7 +97,9 @@ int phfem_gpu_diameter(const double* coords, const int32_t* tets, int64_t ne, do
  * star_fill places each incidence at star_ptr[v] + --count[v] (the order
  * inside a vertex's segment is unspecified; every consumer is order free)
  * and leaves count zeroed. */
-int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream);
+/* repeated (may be NULL, zeroed by the caller) is set to 1 if an element
+ * repeats a node id; star_groups then checks its stars for such elements */
+int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, int32_t* repeated, void* stream);
 int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr, int32_t* count, int32_t* star,
                         void* stream);
 
@@ -114,7 +116,7 @@ int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_t* star_ptr
 int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star,
                           const int32_t* tets, int32_t* edge_first, int32_t* slot_mate,
                           int32_t* defer_list, int32_t* defer_count, unsigned long long* err,
-                          void* stream);
+                          const int32_t* repeated, void* stream);
 /* The child of a red refinement (refine_conn.cu): edge_first [6 x 12 n] and
  * slot_mate [4 x 12 n] (may be NULL) of the child mesh in closed form from
  * the parent's tets [4 n], edge_of_slot, edge_first, slot_mate and nEd;

@@ -41,9 +41,15 @@ __device__ __forceinline__ int top_vertex(const int4& e) {
     return k;
 }
 
-__global__ void star_count(const int32_t* __restrict__ tets, int64_t ne, int32_t* __restrict__ count) {
+__device__ __forceinline__ bool repeats_id(const int4& e) {
+    return e.x == e.y || e.x == e.z || e.x == e.w || e.y == e.z || e.y == e.w || e.z == e.w;
+}
+
+__global__ void star_count(const int32_t* __restrict__ tets, int64_t ne, int32_t* __restrict__ count,
+                           int32_t* __restrict__ repeated) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ne; t += (int64_t)gridDim.x * blockDim.x) {
         const int4 e = ldtet(tets, t);
+        if (repeated && repeats_id(e)) *repeated = 1;
         const int top = top_vertex(e);
         if (top != 0) atomicAdd(count + e.x, 1);
         if (top != 1) atomicAdd(count + e.y, 1);
@@ -533,8 +539,11 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
     star_groups_match(int64_t nv, const int64_t* __restrict__ star_ptr, const int32_t* __restrict__ star,
                       const int32_t* __restrict__ tets, int32_t* __restrict__ edge_first,
                       int32_t* __restrict__ slot_mate, int32_t* __restrict__ defer_list,
-                      int32_t* __restrict__ defer_count, unsigned long long* err) {
+                      int32_t* __restrict__ defer_count, const int32_t* __restrict__ repeated,
+                      unsigned long long* err) {
     __shared__ int2 s_e[kMatchWarps][2][32];  // (b, edge slot) by hash bit of b
+    // an element repeats a node id somewhere (star_count): check every star
+    const bool any_rep = repeated == nullptr || *repeated != 0;
     __shared__ int4 s_f[kMatchWarps][32];     // (lo, hi, face slot, orientation)
     __shared__ int32_t s_min[kMatchWarps][32];  // edge group minimum at the group's first lane
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -577,7 +586,10 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
         const int4 T2 = load_tet(I2);
         const int32_t v = P1.v;
         const int m = (int)(P1.end - P1.beg);
+        // a star with an element that repeats a node id goes to the hashing
+        // pass, which handles edges (a, a) and faces without a mate
         bool defer = m > 32;
+        if (any_rep) defer = defer || __any_sync(0xffffffffu, lane < m && repeats_id(T1));
         if (!defer) {
             const bool valid = lane < m;
             const int32_t t = valid ? I1 >> 2 : 0;
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
                 const int32_t b = o[i];
-                const bool q = valid && (b > v || (b == v && i < lv));
+                const bool q = valid && b > v;
                 const bool hb = (hash32((uint32_t)b) >> 31) != 0;
                 const unsigned bal0 = __ballot_sync(0xffffffffu, q && !hb), bal1 = __ballot_sync(0xffffffffu, q && hb);
                 const int pe = (hb ? n1 + __popc(bal1 & lt) : n0 + __popc(bal0 & lt));
@@ -600,8 +612,7 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
                 if (do_faces) {
                     const int32_t a = o[(i + 1) % 3], c = o[(i + 2) % 3];
                     const int32_t lo = min(a, c), hi = max(a, c);
-                    if (valid && (lo == v || a == c)) mark_degenerate(slot_mate, 4 * t + (int)((ktab >> (2 * i)) & 3u), err);
-                    const bool qf = valid && lo > v && a != c;
+                    const bool qf = valid && lo > v;
                     const unsigned balf = __ballot_sync(0xffffffffu, qf);
                     const bool xy = (lv & 1) ? c < a : a < c;
                     const int pf = nf + __popc(balf & lt);
@@ -655,10 +666,7 @@ __global__ void __launch_bounds__(32 * kMatchWarps, PHG_MATCH_MINB)
                                                  b = (unsigned long long)(max(c.z, oslot) >> 2);
                         report(err, PHG_ERR_DUP_ORIENT, a << 32 | b);
                     }
-                    if (cnt == 2 && oslot >> 2 == c.z >> 2)
-                        mark_degenerate(slot_mate, c.z, err);  // both sides in one element
-                    else
-                        slot_mate[c.z] = cnt >= 2 ? oslot : -1;
+                    slot_mate[c.z] = cnt >= 2 ? oslot : -1;
                 }
             }
             __syncwarp();
@@ -1172,8 +1180,10 @@ inline int grid_cap(int64_t n, int block) {
 
 }  // namespace
 
-extern "C" int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, void* stream) {
-    star_count<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, count); phg::count_launches(1);
+extern "C" int phfem_gpu_star_count(const int32_t* tets, int64_t ne, int32_t* count, int32_t* repeated,
+                                    void* stream) {
+    star_count<<<grid_cap(ne, 256), 256, 0, (cudaStream_t)stream>>>(tets, ne, count, repeated);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 
@@ -1186,7 +1196,8 @@ extern "C" int phfem_gpu_star_fill(const int32_t* tets, int64_t ne, const int64_
 
 extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const int32_t* star, const int32_t* tets,
                                      int32_t* edge_first, int32_t* slot_mate, int32_t* defer_list,
-                                     int32_t* defer_count, unsigned long long* err, void* stream) {
+                                     int32_t* defer_count, unsigned long long* err, const int32_t* repeated,
+                                     void* stream) {
     // pass 1: all vertices, stars <= 32 (warp, one incidence per lane)
     // pass 2: deferred stars <= 64 (warp, two per lane)
     // pass 3: anything larger (block per vertex); counts stay on the device
@@ -1209,7 +1220,7 @@ extern "C" int phfem_gpu_star_groups(int64_t nc, const int64_t* star_ptr, const 
         const int64_t blocks = (nc + kMatchWarps - 1) / kMatchWarps;
         const int grid = (int)(blocks < resident_m ? blocks : resident_m);
         star_groups_match<<<grid, 32 * kMatchWarps, 0, s>>>(nc, star_ptr, star, tets, edge_first, slot_mate,
-                                                            defer_list, defer_count, err);
+                                                            defer_list, defer_count, repeated, err);
     } else {
         const int64_t blocks = (nc + kFastWarps - 1) / kFastWarps;
         const int grid = (int)(blocks < resident ? blocks : resident);

@@ -138,9 +138,11 @@ void build_star(const MeshData& m, Connectivity& c, Stages* st) {
     Work& w = c.w;
     cudaEvent_t t0 = st ? st->mark() : nullptr;
     if (w.scratch.cap < (int64_t)phfem_gpu_scan_scratch(m.nc)) w.scratch.alloc((int64_t)phfem_gpu_scan_scratch(m.nc));
-    w.cnt.alloc(m.nc);
+    // counts, then one word set when an element repeats a node id (read by
+    // the star grouping)
+    w.cnt.alloc(m.nc + 1);
     w.cnt.zero();
-    check(phfem_gpu_star_count(m.tets.p, m.ne, w.cnt.p, SV()), "star count");
+    check(phfem_gpu_star_count(m.tets.p, m.ne, w.cnt.p, w.cnt.p + m.nc, SV()), "star count");
     c.star_ptr.alloc(m.nc + 1);
     check(phfem_gpu_scan_i32(w.cnt.p, c.star_ptr.p, m.nc, w.scratch.p, SV()), "star scan");
     c.star.alloc(3 * m.ne);  // no incidence of an element's largest vertex
@@ -186,7 +188,8 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
               "refined groups");
     } else {
         check(phfem_gpu_star_groups(nc, c.star_ptr.p, c.star.p, m.tets.p, c.edge_first.p,
-                                    faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.err.p, SV()),
+                                    faces ? c.slot_mate.p : nullptr, w.big_list.p, w.big_count.p, w.err.p,
+                                    w.cnt.p + nc, SV()),
               "star groups");
     }
     if (st) st->span(&st->groups, t0);
