@@ -578,3 +578,23 @@ def test_repeated_node_ids_match_oracle(oracle, case):
     mg = from_gpu(g)
     for k in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, k), getattr(mo, k)), k
+
+
+@pytest.mark.parametrize("nc", [0, 1])
+def test_empty_mesh_matches_oracle(oracle, nc):
+    """A mesh without elements (with and without nodes): the reference builds
+    empty tables, refines to an empty child keeping the nodes, and assembles
+    an empty system; so does the device path (no zero-size launch fails)."""
+    e = np.zeros((0, 3), np.int32)
+    m = MeshArrays(np.zeros((nc, 3)), np.zeros((0, 4), np.int32), e, e, 0)
+    fo = oracle.faces(m)
+    g = to_gpu(m)
+    fg = g.faces()
+    for k in ("nf", "n_interior", "n_dirichlet", "n_neumann", "l"):
+        assert fg[k] == fo[k] == 0, k
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for k in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, k), getattr(mo, k)), k
+    assert ph.Mesh.from_arrays(m.coords, m.tets, e, e).sizes() == (nc, 0, 0, 0)
