@@ -598,3 +598,25 @@ def test_empty_mesh_matches_oracle(oracle, nc):
     for k in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, k), getattr(mo, k)), k
     assert ph.Mesh.from_arrays(m.coords, m.tets, e, e).sizes() == (nc, 0, 0, 0)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_relabelled_mesh_matches_oracle(oracle, seed):
+    """A Kuhn box with its nodes renumbered and its elements shuffled (stars
+    of no particular order, first occurrences far from their elements):
+    connectivity, system and one refinement bit-exact against the oracle."""
+    k = oracle.kuhn(6, 5, 4, jitter=0.2, dmask=0x5)
+    rng = np.random.default_rng(seed)
+    pn = rng.permutation(k.nc)  # new id of old node i
+    inv = np.argsort(pn)
+    pe = rng.permutation(k.ne)
+    m = MeshArrays(np.ascontiguousarray(k.coords[inv]), np.ascontiguousarray(pn[k.tets][pe].astype(np.int32)),
+                   np.ascontiguousarray(pn[k.db].astype(np.int32)), np.ascontiguousarray(pn[k.nb].astype(np.int32)), 0)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, kind=0)
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for key in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
