@@ -254,8 +254,14 @@ int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, con
                                 const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
                                 int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
-                                double* slot_coef, int32_t* slot_mrow, int32_t* redo,
+                                double* slot_coef, int32_t* slot_mrow, int32_t* redo, double* halves,
                                 unsigned long long* err, void* ev_begin, void* ev_end, void* stream);
+/* halves (element-major only, may be NULL) [2 l]: the second element's S
+ * diagonal and rhs_neg terms of each row (zero on boundary rows), the
+ * owner's going to diag / rhs_neg, all by plain stores; sum_halves then
+ * gives the assembled diag / rhs_neg (what the atomics on cleared rows that
+ * a NULL halves selects give, bit for bit). */
+int phfem_gpu_sum_halves(int64_t l, double* diag, double* rhs_neg, const double* halves, void* stream);
 int phfem_gpu_assemble_grid(int64_t ne);
 /* norms [2] (device) = ||rhs||^2 [n], ||bd||^2 [l], deterministic; partials
  * [2 phfem_gpu_assemble_grid(n)] */

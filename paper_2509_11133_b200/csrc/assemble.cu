@@ -60,6 +60,13 @@ struct SchurOut {
     double* sell_val;
     double* st_val;  // [10 x ne], element-major
     double* diag;    // [l], element-major
+    // element-major with halves: the second element's diagonal and rhs_neg
+    // terms of each interior row go to diag2 / rhs2 [l] with plain stores
+    // (the owner's to diag / rhs_neg), summed when a solve needs S
+    // (sum_halves_k): no clearing pass, no atomics.  NULL: atomics on
+    // cleared rows.
+    double* diag2;
+    double* rhs2;
 };
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -459,6 +466,31 @@ __device__ __forceinline__ int assemble_elem(int64_t t, const double* __restrict
         }
     }
     if (!dv.good()) return 1;
+    if (ELEM && so.diag2) {
+        // single writers: the owner slot writes the row's first half (and
+        // zero second halves on a boundary row), the second slot the second
+        // half of an interior row (a boundary row's rhs_neg was stored above)
+        double* const d2 = so.diag2;
+        double* const r2 = so.rhs2;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            if (sl.row[r] < 0) continue;
+            const int64_t R = sl.row[r];
+            if (sl.owner[r]) {
+                so.diag[R] = sdiag[r];
+                if (sl.bnd[r]) {
+                    d2[R] = 0.0;
+                    r2[R] = 0.0;
+                } else {
+                    rhs_neg[R] = nrb[r];
+                }
+            } else {
+                d2[R] = sdiag[r];
+                r2[R] = nrb[r];
+            }
+        }
+        return 0;
+    }
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         if (sl.row[r] < 0) continue;
@@ -712,7 +744,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            const int32_t* entry_face, const int32_t* face_slots, double* face_bval,
                                            int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
-                                           double* slot_coef, int32_t* slot_mrow, int32_t* redo,
+                                           double* slot_coef, int32_t* slot_mrow, int32_t* redo, double* halves,
                                            unsigned long long* err, void* ev_begin, void* ev_end, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne == 0) return 0;
@@ -722,8 +754,10 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     // element-major when sell_col is NULL (st_val, diag, slot_mrow required)
     const bool elem = sell_col == nullptr;
     if (elem && (!st_val || !diag || !slot_mrow)) return (int)cudaErrorInvalidValue;
-    const SchurOut so{sell_col, sell_val, elem ? st_val : nullptr, elem ? diag : nullptr};
-    zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, so, rhs_neg);
+    const bool split = elem && halves != nullptr;
+    const SchurOut so{sell_col, sell_val, elem ? st_val : nullptr, elem ? diag : nullptr,
+                      split ? halves : nullptr, split ? halves + l : nullptr};
+    if (!split) zero_rows_k<<<kSMs * 8, 256, 0, s>>>(l, so, rhs_neg);
 #define PHG_ASM(K, E)                                                                                                \
     assemble_k<K, E><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow,          \
                                                    face_area, face_bval, rhs, so, rhs_neg, bd, a_blocks, slot_coef,  \
@@ -753,7 +787,24 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     }
 #undef PHG_KIND
 #undef PHG_ASM
-    phg::count_launches(4);
+    phg::count_launches(split ? 3 : 4);
+    return (int)cudaGetLastError();
+}
+
+// diag = (0 + diag) + diag2, rhs_neg = (0 + rhs_neg) + rhs2: the value the
+// atomics on cleared rows give (a two-term sum is order free)
+__global__ void __launch_bounds__(256) sum_halves_k(int64_t l, double* __restrict__ diag,
+                                                    double* __restrict__ rhs_neg, const double* __restrict__ halves) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < l; i += (int64_t)gridDim.x * blockDim.x) {
+        diag[i] = (0.0 + diag[i]) + halves[i];
+        rhs_neg[i] = (0.0 + rhs_neg[i]) + halves[l + i];
+    }
+}
+
+extern "C" int phfem_gpu_sum_halves(int64_t l, double* diag, double* rhs_neg, const double* halves, void* stream) {
+    if (l == 0) return 0;
+    sum_halves_k<<<grid_for(l, 256), 256, 0, (cudaStream_t)stream>>>(l, diag, rhs_neg, halves);
+    phg::count_launches(1);
     return (int)cudaGetLastError();
 }
 

@@ -840,7 +840,10 @@ int phfem_mesh_get_system(const phfem_mesh* mesh, double* a_blocks, double* slot
         if (slot_mrow) sys.slot_mrow.download_to(slot_mrow, 4 * ne);
         if (rhs) sys.rhs.download_to(rhs, 4 * ne);
         if (bd) sys.bd.download_to(bd, sys.l);
-        if (rhs_neg) sys.rhs_neg.download_to(rhs_neg, sys.l);
+        if (rhs_neg) {
+            sys.finish();  // an element-major system's halves
+            sys.rhs_neg.download_to(rhs_neg, sys.l);
+        }
         if (s_rowptr || s_col || s_val) {
             DBuf<int32_t> nnz(sys.l);
             check(phfem_gpu_sell_row_nnz(sys.l, sys.sell_col.p, nnz.p, SV()), "row nnz");

@@ -1258,8 +1258,9 @@ extern "C" int phfem_gpu_element_offsets(int64_t ne, const int32_t* edge_first, 
                                          void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (ne <= 0) {
+        // (no slots: slot_mate may be NULL even when faces are asked for)
         cudaMemsetAsync(edge_off, 0, sizeof(int64_t), s);
-        if (slot_mate) cudaMemsetAsync(face_off, 0, sizeof(int64_t), s);
+        if (face_off) cudaMemsetAsync(face_off, 0, sizeof(int64_t), s);
         return (int)cudaGetLastError();
     }
     const int64_t ntiles = scan_tiles(ne);

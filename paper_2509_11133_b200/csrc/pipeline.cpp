@@ -403,6 +403,13 @@ phg_problem device_problem(const Coefs& k, int problem) {
     return p;
 }
 
+void System::finish() const {
+    if (!split) return;
+    check(phfem_gpu_sum_halves(l, const_cast<double*>(diag.p), const_cast<double*>(rhs_neg.p), halves.p, SV()),
+          "sum halves");
+    split = false;
+}
+
 void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
                      bool debug_views, Stages* st) {
     if (!c.has_faces) throw MeshError("assemble: face table missing");
@@ -422,12 +429,14 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
         sys.sell_val.release();
         sys.st_val.alloc(10 * ((m.ne + 31) / 32) * 32);
         sys.diag.alloc(c.l);
+        sys.halves.alloc(2 * c.l);
     } else {
         const int64_t width = PHG_SELL_C * PHG_SELL_W;
         sys.sell_col.alloc(sys.nchunks * width);
         sys.sell_val.alloc(sys.nchunks * width);
         sys.st_val.release();
         sys.diag.release();
+        sys.halves.release();
     }
     // the S diagonal, rhs_neg and b_D are cleared by the assembly kernel
     // itself (row owners), every other SELL slot is written exactly once
@@ -455,8 +464,10 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
                                       sys.elem ? nullptr : sys.sell_val.p, sys.elem ? sys.st_val.p : nullptr,
                                       sys.elem ? sys.diag.p : nullptr, sys.rhs_neg.p, sys.bd.p, sys.rhs.p,
                                       debug_views ? sys.a_blocks.p : nullptr, debug_views ? sys.slot_coef.p : nullptr,
-                                      sys.slot_mrow.p, w.redo.p, w.err.p, ka, kb, SV()),
+                                      sys.slot_mrow.p, w.redo.p, sys.elem ? sys.halves.p : nullptr, w.err.p, ka, kb,
+                                      SV()),
           "assemble");
+    sys.split = sys.elem;
     if (st) {
         st->span(&st->assemble, t0);
         st->span(&st->assemble_kernel, ka, kb);

@@ -21,7 +21,7 @@ void check(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
-        throw MeshError("out of memory");
+        throw MeshError(std::string("out of memory (device, ") + what + ")");
     }
     throw MeshError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
@@ -362,6 +362,7 @@ void solve_schur(const MeshData& m, const Coefs& k, const Connectivity& c, const
                  bool refuse_throws) {
     const auto t0 = std::chrono::steady_clock::now();
     const int64_t l = sys.l;
+    sys.finish();  // an element-major system's diag / rhs_neg halves
     double sum_rhs2, sum_bd2;
     sys.norms(sum_rhs2, sum_bd2);
     const double nrm_rhs = std::sqrt(sum_rhs2), nrm_bd = std::sqrt(sum_bd2);

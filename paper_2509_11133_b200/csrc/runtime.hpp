@@ -232,6 +232,12 @@ struct System {
     DBuf<int32_t> sell_col;
     DBuf<double> sell_val, rhs_neg, bd, rhs;
     DBuf<double> st_val, diag;
+    // element-major: the rows' second halves of diag / rhs_neg [2 l] until a
+    // solve sums them in (split)
+    DBuf<double> halves;
+    mutable bool split = false;
+    // diag / rhs_neg assembled (sums the halves once)
+    void finish() const;
     // sum(B_T^2), sum(b_D^2) for inner_cg_options: reduced on the device
     // when a solve asks (the reference computes them at solve time too)
     void norms(double& sum_rhs2, double& sum_bd2) const;
