@@ -244,7 +244,7 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * terms, formed first by a pass over the nd + nn boundary entries
  * (entry_face of the classification, face_slots).  ev_begin / ev_end (cudaEvent_t, may be NULL) bracket the
  * main kernel.  S goes to SELL-32 (sell_col, sell_val: the reference's rows,
- * both triangles) or, when sell_col is NULL, element-major: st_val [10 ne]
+ * both triangles) or, when st_val is not NULL, element-major: st_val [10 ne]
  * (S_T[r][q], r <= q, in 32-element chunks: (t/32)*320 + pair*32 + t%32),
  * the rows slot_mrow [4 ne] (required) and the assembled diagonal diag [l]. */
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,

@@ -751,9 +751,10 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
     const phg_problem p = *prob;
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);
-    // element-major when sell_col is NULL (st_val, diag, slot_mrow required)
-    const bool elem = sell_col == nullptr;
-    if (elem && (!st_val || !diag || !slot_mrow)) return (int)cudaErrorInvalidValue;
+    // element-major when st_val is given (diag and slot_mrow required), else
+    // SELL rows (sell_col / sell_val: NULL when there are no rows, L = 0)
+    const bool elem = st_val != nullptr;
+    if (elem && ((!diag && l > 0) || !slot_mrow)) return (int)cudaErrorInvalidValue;
     const bool split = elem && halves != nullptr;
     const SchurOut so{sell_col, sell_val, elem ? st_val : nullptr, elem ? diag : nullptr,
                       split ? halves : nullptr, split ? halves + l : nullptr};

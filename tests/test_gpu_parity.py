@@ -620,3 +620,35 @@ def test_relabelled_mesh_matches_oracle(oracle, seed):
     mg = from_gpu(g)
     for key in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
+
+
+@pytest.mark.parametrize("dirichlet", [(0, 1, 2, 3), (), (0, 3)])
+def test_single_element_solve_matches_oracle(oracle, dirichlet):
+    """One element with all four faces Dirichlet (L = 4), all Neumann (L = 0:
+    an empty face system) or mixed: connectivity, system and the Schur solve
+    (U, Lambda, iterations) against the oracle, or the same error."""
+    from oracle_bind import CheckerError
+    coords = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    tets = np.array([[0, 1, 2, 3]], np.int32)
+    fv = [[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]
+    db = np.array([tets[0][fv[k]] for k in range(4) if k in dirichlet], np.int32).reshape(-1, 3)
+    nb = np.array([tets[0][fv[k]] for k in range(4) if k not in dirichlet], np.int32).reshape(-1, 3)
+    m = MeshArrays(coords, tets, db, nb, 0)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    so = check_system(g, m, fo, oracle, kind=0)
+    try:
+        uo, lo, sto = oracle.solve(m, so, kind=0)
+    except CheckerError as eo:
+        with pytest.raises(ph.PhfemError) as eg:
+            g.solve_unverified(0)
+        assert eg.value.msg == eo.msg
+        return
+    ug, lg, stg = g.solve_unverified(0)
+    assert len(lg) == len(lo) == fo["l"]
+    # the north-star bar for solutions (dot products are summed in another
+    # order than the reference's serial loops)
+    assert rel_l2(ug, uo) <= 1e-9
+    if len(lo):
+        assert rel_l2(lg, lo) <= 1e-9
+    assert int(stg["iterations"]) == sto["iterations"]
