@@ -298,7 +298,9 @@ def _config_case(oracle, cfg, factor):
     return c, m, k
 
 
-@pytest.mark.parametrize("cid,factor", [(1, 1), (3, 8), (4, 16), (5, 8)])
+# (and each config on one or two grid cells: 6 / 48 elements, most faces on
+# the boundary)
+@pytest.mark.parametrize("cid,factor", [(1, 1), (3, 8), (4, 16), (5, 8), (3, 64), (4, 64), (5, 256), (3, 32)])
 def test_config_parity(oracle, cid, factor):
     cfg, m, k = _config_case(oracle, configs.CONFIGS[cid], factor)
     g = to_gpu(m)
@@ -652,3 +654,51 @@ def test_single_element_solve_matches_oracle(oracle, dirichlet):
     if len(lo):
         assert rel_l2(lg, lo) <= 1e-9
     assert int(stg["iterations"]) == sto["iterations"]
+
+
+@pytest.mark.parametrize("dmask", [0x0, 0x20])
+def test_neumann_heavy_solve_matches_oracle(oracle, dmask):
+    """Kuhn boxes with no Dirichlet face (the multipliers live on interior
+    faces only; c = 1 keeps the system definite) and with Dirichlet on one
+    side: the whole Schur path against the oracle."""
+    m = oracle.kuhn(3, 2, 2, jitter=0.15, dmask=dmask)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    so = check_system(g, m, fo, oracle, kind=0)
+    uo, lo, st_o, rc_o, msg_o = oracle.solve_raw(m, so, 0)
+    ug, lg, st_g = g.solve_unverified(0)
+    assert rel_l2(ug, uo) <= 1e-9 and rel_l2(lg, lo) <= 1e-9
+    assert abs(st_g["iterations"] - st_o["iterations"]) <= max(3, 0.02 * st_o["iterations"])
+    assert st_g["accepted"] == (rc_o == 0)
+
+
+def _small_meshes(oracle):
+    coords = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    tets = np.array([[0, 1, 2, 3]], np.int32)
+    fv = [[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]
+    e = np.zeros((0, 3), np.int32)
+    allneu = np.array([tets[0][f] for f in fv], np.int32)
+    return [MeshArrays(coords, tets, e, allneu, 0), MeshArrays(coords, tets, allneu, e, 0),
+            oracle.kuhn(1, 1, 1, dmask=0x3F), oracle.kuhn(2, 1, 1, jitter=0.1, dmask=0x5)]
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_pipeline_small_meshes(oracle, case):
+    """The benchmark pass (phfem_pipeline: connectivity, element-major
+    assembly with its plain-store row halves, refinement) on meshes of one
+    to a few elements, down to L = 0: its counts against the oracle's, and a
+    face solve on the system it left against the oracle's."""
+    m = _small_meshes(oracle)[case]
+    g = to_gpu(m)
+    _, counts = g.pipeline(0, True)
+    fo = oracle.faces(m)
+    en_o, _ = oracle.edges(m)
+    assert int(counts[0]) == len(en_o) and int(counts[1]) == fo["nf"] and int(counts[2]) == fo["l"]
+    assert int(counts[4]) == 12 * m.ne
+    so = oracle.assemble(m, fo, kind=0)
+    abs_tol = 0.2 * 1e-10 * np.hypot(np.linalg.norm(so["rhs"]), np.linalg.norm(so["bd"]))
+    lo, res = oracle.pcg(so, tol=1e-10, abs_tol=abs_tol, max_iter=10 * max(len(so["bd"]), 1))
+    lg, st = g.solve_faces(0, tol=1e-10)
+    assert len(lg) == len(lo)
+    if len(lo):
+        assert rel_l2(lg, lo) <= 1e-9
