@@ -702,3 +702,26 @@ def test_pipeline_small_meshes(oracle, case):
     assert len(lg) == len(lo)
     if len(lo):
         assert rel_l2(lg, lo) <= 1e-9
+
+
+def test_unused_nodes_match_oracle(oracle):
+    """Nodes no element uses (before, between and after the used ones):
+    empty stars, and the refinement's new node ids start after all of them."""
+    k = oracle.kuhn(2, 2, 1, jitter=0.1, dmask=0x3F)
+    used = np.arange(k.nc)
+    new_id = used + 1 + (used >= k.nc // 2)  # node 0 and one in the middle unused
+    coords = np.zeros((k.nc + 3, 3))
+    coords[new_id] = k.coords
+    coords[0] = (9.0, 9.0, 9.0)
+    coords[k.nc // 2 + 1] = (-1.0, 2.0, 3.0)
+    coords[-1] = (5.0, -5.0, 0.5)
+    m = MeshArrays(coords, new_id[k.tets].astype(np.int32), new_id[k.db].astype(np.int32),
+                   new_id[k.nb].astype(np.int32), 0)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    check_system(g, m, fo, oracle, kind=0)
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for key in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
