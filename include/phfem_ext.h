@@ -141,6 +141,11 @@ typedef struct phfem_stage_ms {
 #define PHFEM_PIPE_NO_ASSEMBLY 2
 int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
                    int64_t counts[5]);
+/* The last phfem_pipeline refinement's child: sizes out [nC, nE, nD, nN];
+ * arrays (each may be NULL) sized from them.  PHFEM_ERR_ARGUMENT when no
+ * pass refined. */
+int phfem_pipeline_child(const phfem_mesh* mesh, int64_t sizes[4], double* coords, int32_t* tets,
+                         int32_t* db, int32_t* nb);
 
 /* Schur solve (assembly cached): Jacobi-PCG timed on the device, then
  * recovery and verify_solution; a verify refusal (SURVEY finding 8) is

@@ -991,6 +991,23 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
     });
 }
 
+int phfem_pipeline_child(const phfem_mesh* mesh, int64_t sizes[4], double* coords, int32_t* tets, int32_t* db,
+                         int32_t* nb) {
+    return guarded([&] {
+        if (!mesh || !sizes) throw InvalidArgument("null argument");
+        const auto& ch = mesh->scratch_child;
+        if (!ch || !ch->tets.p) throw InvalidArgument("no pipeline pass has refined this mesh");
+        sizes[0] = ch->nc;
+        sizes[1] = ch->ne;
+        sizes[2] = ch->nd;
+        sizes[3] = ch->nn;
+        if (coords) ch->coords.download_to(coords, 3 * ch->nc);
+        if (tets) ch->tets.download_to(tets, 4 * ch->ne);
+        if (db) ch->db.download_to(db, 3 * ch->nd);
+        if (nb) ch->nb.download_to(nb, 3 * ch->nn);
+    });
+}
+
 int phfem_solve_timed(const phfem_mesh* mesh, int problem, double tol, int64_t max_iter, double out[8],
                       double* out8) {
     return guarded([&] {

@@ -112,6 +112,7 @@ def lib():
         "phfem_solution_stats": [P, P],
         "phfem_solution_errors_ex": [P, P],
         "phfem_pipeline": [P, C.c_int, C.c_int, P, P],
+        "phfem_pipeline_child": [P, P, P, P, P, P],
         "phfem_solve_timed": [P, C.c_int, C.c_double, I64, P, P],
         "phfem_mesh_solve_faces": [P, C.c_int, C.c_double, I64, P, P],
         "phfem_mesh_solve_unverified": [P, C.c_int, C.c_double, I64, P, P, P],
@@ -141,7 +142,7 @@ EXPORTED = [
     "phfem_mesh_create_from_arrays", "phfem_mesh_create_from_arrays_async", "phfem_mesh_create_kuhn", "phfem_mesh_sizes", "phfem_mesh_get_arrays",
     "phfem_mesh_set_coefficients", "phfem_mesh_connectivity", "phfem_mesh_get_edges", "phfem_mesh_get_faces",
     "phfem_mesh_refinement_map", "phfem_mesh_assemble", "phfem_mesh_get_system", "phfem_solve_ex",
-    "phfem_solution_stats", "phfem_solution_errors_ex", "phfem_stream", "phfem_pipeline", "phfem_solve_timed",
+    "phfem_solution_stats", "phfem_solution_errors_ex", "phfem_stream", "phfem_pipeline", "phfem_pipeline_child", "phfem_solve_timed",
     "phfem_mesh_solve_faces", "phfem_mesh_solve_unverified",
 ]
 
@@ -365,6 +366,18 @@ class Mesh:
         flags = (1 if do_refine else 0) | (0 if assemble else 2)
         _check(lib().phfem_pipeline(self._h, problem, flags, C.byref(ms), _ptr(counts)))
         return {n: getattr(ms, n) for n, _ in StageMs._fields_}, counts
+
+    def pipeline_child(self):
+        """The last pipeline pass's refined child (coords, tets, db, nb)."""
+        sz = np.zeros(4, dtype=np.int64)
+        _check(lib().phfem_pipeline_child(self._h, _ptr(sz), None, None, None, None))
+        nc, ne, nd, nn = (int(v) for v in sz)
+        c = np.zeros((nc, 3))
+        t = np.zeros((ne, 4), dtype=np.int32)
+        d = np.zeros((nd, 3), dtype=np.int32)
+        n = np.zeros((nn, 3), dtype=np.int32)
+        _check(lib().phfem_pipeline_child(self._h, _ptr(sz), _ptr(c), _ptr(t), _ptr(d), _ptr(n)))
+        return c, t, d, n
 
     def solve_timed(self, problem, tol=1e-10, max_iter=-1):
         """Schur solve with timings: CG on the device, then recovery + verify

@@ -725,3 +725,29 @@ def test_unused_nodes_match_oracle(oracle):
     mg = from_gpu(g)
     for key in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
+
+
+@pytest.mark.parametrize("case", ["cube2", "kuhn_mixed", "cfg3", "cfg5"])
+def test_pipeline_refinement_bit_exact(oracle, case):
+    """The benchmark pass's refinement (into a scratch child reused across
+    passes): its child mesh against the oracle's refinement, bit for bit,
+    after the connectivity + assembly of the same pass."""
+    if case == "cube2":
+        m = cube5()
+        for _ in range(2):
+            m = oracle.refine(m)[0]
+        k = None
+    elif case == "kuhn_mixed":
+        m = oracle.kuhn(4, 3, 2, jitter=0.2, dmask=0x9)
+        k = None
+    else:
+        cfg, m, k = _config_case(oracle, configs.CONFIGS[int(case[3])], 16)
+    g = to_gpu(m)
+    if k is not None and (k["a_elem"] is not None or k["a_diag"] is not None):
+        g.set_coefficients(k["a_elem"], k["a_diag"], 1.0)
+    for _ in range(2):  # a second pass reuses the scratch child
+        g.pipeline(0, True)
+    c, t, d, n = g.pipeline_child()
+    mo = oracle.refine(m)[0]
+    assert np.array_equal(c, mo.coords) and np.array_equal(t, mo.tets)
+    assert np.array_equal(d, mo.db) and np.array_equal(n, mo.nb)
