@@ -751,3 +751,53 @@ def test_pipeline_refinement_bit_exact(oracle, case):
     mo = oracle.refine(m)[0]
     assert np.array_equal(c, mo.coords) and np.array_equal(t, mo.tets)
     assert np.array_equal(d, mo.db) and np.array_equal(n, mo.nb)
+
+
+def _delaunay_mesh(seed: int, npts: int) -> MeshArrays:
+    """An unstructured mesh: the Delaunay tetrahedralisation of seeded random
+    points in the unit cube plus its 8 corners (scipy), elements oriented to
+    det > 0, the unshared element faces as the boundary (in their element's
+    orientation), split between Dirichlet and Neumann by a seeded coin."""
+    from collections import Counter
+
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(seed)
+    corners = np.array([[i, j, k] for i in (0, 1) for j in (0, 1) for k in (0, 1)], float)
+    pts = np.vstack([corners, rng.random((npts, 3))])
+    tets = Delaunay(pts).simplices.astype(np.int32)
+    p = pts[tets]
+    det = np.einsum("ij,ij->i", np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), p[:, 3] - p[:, 0])
+    tets = tets[np.abs(det) > 1e-12]
+    det = det[np.abs(det) > 1e-12]
+    tets[det < 0] = tets[det < 0][:, [0, 1, 3, 2]]
+    fv = [[0, 1, 2], [0, 2, 3], [0, 3, 1], [3, 2, 1]]
+    faces = [tuple(t[f]) for t in tets for f in fv]
+    cnt = Counter(tuple(sorted(f)) for f in faces)
+    bnd = [f for f in faces if cnt[tuple(sorted(f))] == 1]
+    coin = rng.random(len(bnd)) < 0.5
+    db = np.array([f for f, c in zip(bnd, coin) if c], np.int32).reshape(-1, 3)
+    nb = np.array([f for f, c in zip(bnd, coin) if not c], np.int32).reshape(-1, 3)
+    return MeshArrays(np.ascontiguousarray(pts), np.ascontiguousarray(tets), db, nb, 0)
+
+
+@pytest.mark.parametrize("seed,npts", [(1, 300), (2, 2000), (3, 6000)])
+def test_unstructured_mesh_matches_oracle(oracle, seed, npts):
+    """Delaunay meshes of random points (irregular stars of 4 to ~100
+    incidences: warp matches, the hashing passes and blocks; irregular
+    elements): connectivity, element and Schur data bit for bit, one
+    refinement, and the face solve to the north-star bar."""
+    m = _delaunay_mesh(seed, npts)
+    g = to_gpu(m)
+    fo = check_connectivity(g, m, oracle)
+    so = check_system(g, m, fo, oracle, kind=0)
+    abs_tol = 0.2 * 1e-10 * np.hypot(np.linalg.norm(so["rhs"]), np.linalg.norm(so["bd"]))
+    lo, res = oracle.pcg(so, tol=1e-10, abs_tol=abs_tol, max_iter=10 * max(len(so["bd"]), 1))
+    lg, st = g.solve_faces(0, tol=1e-10)
+    assert st["converged"] and res[2] == 1.0
+    assert rel_l2(lg, lo) <= 1e-9, rel_l2(lg, lo)
+    assert abs(st["iterations"] - res[0]) <= max(3, 0.02 * res[0])
+    mo = oracle.refine(m)[0]
+    g.refine()
+    mg = from_gpu(g)
+    for key in ("coords", "tets", "db", "nb"):
+        assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
