@@ -747,7 +747,12 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            double* slot_coef, int32_t* slot_mrow, int32_t* redo, double* halves,
                                            unsigned long long* err, void* ev_begin, void* ev_end, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
-    if (ne == 0) return 0;
+    if (ne == 0) {
+        // nothing to assemble; the caller's events still bracket the (empty) kernel
+        if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);
+        if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);
+        return (int)cudaGetLastError();
+    }
     const unsigned grid = (unsigned)((ne + kCondThreads - 1) / kCondThreads);
     const phg_problem p = *prob;
     cudaMemsetAsync(redo, 0, sizeof(int32_t), s);

@@ -801,3 +801,40 @@ def test_unstructured_mesh_matches_oracle(oracle, seed, npts):
     mg = from_gpu(g)
     for key in ("coords", "tets", "db", "nb"):
         assert np.array_equal(getattr(mg, key), getattr(mo, key)), key
+
+
+def test_workspace_recycling_across_meshes(oracle):
+    """Handles of different sizes and boundary mixes one after the other in
+    one process (pooled connectivity / system workspaces and scratch
+    children are recycled between handles): every pass's counts, tables and
+    face solve against the oracle."""
+    coords = np.array([[0.0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]])
+    e = np.zeros((0, 3), np.int32)
+    single = MeshArrays(coords, np.array([[0, 1, 2, 3]], np.int32),
+                        np.array([[0, 1, 2], [0, 2, 3]], np.int32), np.array([[0, 3, 1], [3, 2, 1]], np.int32), 0)
+    cube2 = cube5()
+    for _ in range(2):
+        cube2 = oracle.refine(cube2)[0]
+    seq = [oracle.kuhn(6, 5, 4, jitter=0.1, dmask=0x9), cube2, oracle.kuhn(2, 2, 2, dmask=0x0), single,
+           MeshArrays(np.zeros((1, 3)), np.zeros((0, 4), np.int32), e, e, 0), oracle.kuhn(3, 3, 3, dmask=0x3F),
+           oracle.kuhn(6, 5, 4, jitter=0.1, dmask=0x9)]
+    for m in seq:
+        for _ in range(2):  # a fresh handle each time, the pools warm
+            g = to_gpu(m)
+            _, counts = g.pipeline(0, True)
+            fo = oracle.faces(m)
+            assert int(counts[1]) == fo["nf"] and int(counts[2]) == fo["l"]
+            fg = g.faces()
+            for k in ("faces", "face_of_slot", "face_slots", "mrow"):
+                assert np.array_equal(fg[k], fo[k]), k
+            if m.ne:
+                c, t, d, n = g.pipeline_child()
+                mo = oracle.refine(m)[0]
+                assert np.array_equal(t, mo.tets) and np.array_equal(c, mo.coords)
+            if fo["l"]:
+                so = oracle.assemble(m, fo, kind=0)
+                abs_tol = 0.2 * 1e-10 * np.hypot(np.linalg.norm(so["rhs"]), np.linalg.norm(so["bd"]))
+                lo, _ = oracle.pcg(so, tol=1e-10, abs_tol=abs_tol, max_iter=10 * len(so["bd"]))
+                lg, _ = g.solve_faces(0, tol=1e-10)
+                assert rel_l2(lg, lo) <= 1e-9
+            del g
