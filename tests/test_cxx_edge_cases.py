@@ -14,25 +14,44 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-BIN = os.path.join(ROOT, "build", "cxx_edge_cases")
-GOLDEN = os.path.join(ROOT, "tests", "golden", "cxx_edge_cases.txt")
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def _compare(got, ref):
+    assert len(got) == len(ref), (len(got), len(ref), got[-5:])
+    for g, r in zip(got, ref):
+        if r.startswith("~"):
+            gt, rt = g.split(), r.split()
+            assert len(gt) == len(rt), (g, r)
+            for a, b in zip(gt, rt):
+                try:
+                    x, y = float(a), float(b)
+                except ValueError:
+                    assert a == b, (g, r)
+                    continue
+                assert abs(x - y) <= 1e-9 * max(abs(y), 1e-300), (g, r)
+        else:
+            assert g == r, (g, r)
+
+
+def _run(name, args=()):
+    exe = os.path.join(ROOT, "build", name)
+    if not os.path.exists(exe):
+        pytest.skip(f"build/{name} not built (make -C tests/cxx_diff)")
+    out = subprocess.run([exe, *args], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return out.stdout.splitlines()
 
 
 def test_cxx_edge_cases_match_reference():
-    if not os.path.exists(BIN):
-        pytest.skip("build/cxx_edge_cases not built (make -C tests/cxx_diff)")
-    out = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stderr[-2000:]
-    got = out.stdout.splitlines()
-    ref = open(GOLDEN).read().splitlines()
-    assert len(got) == len(ref), (len(got), len(ref))
-    for g, r in zip(got, ref):
-        if r.startswith("~"):
-            gk, *gv = g.split()
-            rk, *rv = r.split()
-            assert gk == rk and len(gv) == len(rv), (g, r)
-            for a, b in zip(gv, rv):
-                a, b = float(a), float(b)
-                assert abs(a - b) <= 1e-9 * max(abs(b), 1e-300), (g, r)
-        else:
-            assert g == r, (g, r)
+    _compare(_run("cxx_edge_cases"), open(os.path.join(GOLDEN_DIR, "cxx_edge_cases.txt")).read().splitlines())
+
+
+def test_capi_edge_cases_match_reference(tmp_path):
+    """The C ABI on meshes read from the reference's text format (one
+    element all Dirichlet / all Neumann / mixed, no elements, a repeated node
+    id, a bad index, a boundary face missing from the lists): counts, sizes,
+    diameter, both solvers, every output file (byte checksums; solution
+    files by value norm) and the error statuses and messages."""
+    _compare(_run("capi_edge_cases", [str(tmp_path)]),
+             open(os.path.join(GOLDEN_DIR, "capi_edge_cases.txt")).read().splitlines())
