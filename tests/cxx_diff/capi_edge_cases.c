@@ -150,5 +150,31 @@ int main(int argc, char** argv) {
     run_mesh("bad index", "COORD 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\nTETRA 1\n1 2 3 9\nDB 0\nNB 0\n", 1);
     run_mesh("face not on the boundary list",
              "COORD 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\nTETRA 1\n1 2 3 4\nDB 1\n1 2 3\nNB 0\n", 1);
+    /* the reference cube: refined twice, the three problems, a parallel
+     * Schur solve, and the dispatch's argument errors */
+    printf("== cube\n");
+    phfem_mesh* m = NULL;
+    phfem_mesh_create_cube(&m);
+    phfem_mesh_refine(m, NULL);
+    phfem_mesh_refine(m, NULL);
+    for (int problem = 0; problem < 3; ++problem) {
+        phfem_solution* s = NULL;
+        if (report_rc("solve", phfem_solve(m, problem, problem == 1 ? "schur-parallel" : "schur", 4, 0.0, &s)))
+            continue;
+        const double *u, *lam;
+        int64_t nu, nl;
+        phfem_solution_values(s, &u, &nu, &lam, &nl);
+        double eu = 0, ek = 0;
+        phfem_solution_errors(s, &eu, &ek);
+        printf("~problem %d %.17g %.17g %.17g %.17g\n", problem, vnorm(u, nu) + 1.0, vnorm(lam, nl) + 1.0, eu + 1.0,
+               ek + 1.0);
+        phfem_solution_destroy(s);
+    }
+    phfem_solution* s = NULL;
+    report_rc("unknown solver", phfem_solve(m, 0, "cholesky", 1, 0.0, &s));
+    report_rc("unknown problem", phfem_solve(m, 7, "schur", 1, 0.0, &s));
+    report_rc("null out", phfem_solve(m, 0, "schur", 1, 0.0, NULL));
+    report_rc("null mesh", phfem_mesh_refine(NULL, NULL));
+    phfem_mesh_destroy(m);
     return 0;
 }
