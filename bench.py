@@ -148,7 +148,8 @@ def algorithmic_bytes(nc, ne, ned, nf, nb, nnz_s, l, k_coef=0, elem=True):
     b_asm = 36 * ne + 24 * nc + 13 * nf + k_coef * ne + s_out + 16 * l + 8
     b_refine = 260 * ne + 48 * nc + 24 * ned + 72 * nb
     b_cg = (64 * ne + 16 * l if elem else 12 * nnz_s) + 96 * l
-    return dict(connect=b_edges + b_faces, assemble=b_asm, refine=b_refine, cg_iteration=b_cg)
+    return dict(connect=b_edges + b_faces, assemble=b_asm, refine=b_refine, refine_boundary=72 * nb,
+                cg_iteration=b_cg)
 
 
 # ---------------------------------------------------------- reference arm
@@ -375,6 +376,9 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     nlaunch = launches() - l0
     stage_ms = {k: v / args.steps for k, v in acc.items()}
+    # the library's rule (capi.cpp: fused_refine_enabled): a pass that both
+    # assembles and refines writes the children from the assembly kernel
+    fused_refine = os.environ.get("PHFEM_FUSED_REFINE", "1")[:1] != "0"
     ms_max = max_over_ranks(dist, ms, "cuda")
     value = job_throughput(world, ne, ms_max)
 
@@ -391,6 +395,14 @@ def main():
         "assemble_condense": {"ms": stage_ms["assemble"], "bytes": B["assemble"]},
         "refine": {"ms": stage_ms["refine"], "bytes": B["refine"]},
     }
+    if fused_refine:
+        # the assembly kernel writes the children and new nodes itself
+        # (assemble.cu: refine_elem): its bytes are both stages' less the
+        # element rows and vertex coordinates read once instead of twice;
+        # the refinement stage is the boundary lists alone
+        b_fused = B["assemble"] + B["refine"] - B["refine_boundary"] - 16 * ne - 24 * nc
+        per_stage["assemble_condense"]["bytes"] = b_fused
+        per_stage["refine"]["bytes"] = B["refine_boundary"]
     for k, v in per_stage.items():
         v["gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
         v["hbm_frac"] = v["gbs"] / hbm
@@ -419,8 +431,10 @@ def main():
     kname = f"assemble_k<{cfg.problem}, 1>"
     prof = ncu_facts().get(kname) if dom_name == "assemble_condense" else None
     if dom_name == "assemble_condense" and kern_ms > 0:
-        a_gbs = B["assemble"] / (kern_ms / 1e3) / 1e9
-        roofline.update({"kernel": kname, "kernel_ms": kern_ms, "algorithmic_bytes": B["assemble"],
+        b_kern = per_stage["assemble_condense"]["bytes"]
+        a_gbs = b_kern / (kern_ms / 1e3) / 1e9
+        roofline.update({"kernel": kname, "kernel_ms": kern_ms, "algorithmic_bytes": b_kern,
+                         "fused_refinement": fused_refine,
                          "hbm": {"achieved": a_gbs, "peak": hbm, "unit": "GB/s", "frac": a_gbs / hbm,
                                  "peak_kind": hbm_kind}})
         if prof:

@@ -246,7 +246,18 @@ int phfem_gpu_set_rules(const double* lam5, const double* w5, int n5, const doub
  * main kernel.  S goes to SELL-32 (sell_col, sell_val: the reference's rows,
  * both triangles) or, when st_val is not NULL, element-major: st_val [10 ne]
  * (S_T[r][q], r <= q, in 32-element chunks: (t/32)*320 + pair*32 + t%32),
- * the rows slot_mrow [4 ne] (required) and the assembled diagonal diag [l]. */
+ * the rows slot_mrow [4 ne] (required) and the assembled diagonal diag [l].
+ * refine (may be NULL): the same kernel also writes one red refinement of the
+ * mesh (phfem_gpu_refine's coords_out / tets_out, without the node maps) from
+ * the connectivity's edge tables. */
+typedef struct phg_refine_out {
+    int64_t nc;
+    const int32_t* edge_first;
+    const int32_t* edge_of_slot;
+    const int64_t* edge_off;
+    double* coords_out;
+    int32_t* tets_out;
+} phg_refine_out;
 int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, const int32_t* tets,
                                 const phg_problem* prob, const int32_t* face_of_slot,
                                 const int32_t* slot_mate, const int32_t* face_mrow,
@@ -255,7 +266,8 @@ int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* coords, con
                                 int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                 double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                 double* slot_coef, int32_t* slot_mrow, int32_t* redo, double* halves,
-                                unsigned long long* err, void* ev_begin, void* ev_end, void* stream);
+                                unsigned long long* err, const phg_refine_out* refine, void* ev_begin,
+                                void* ev_end, void* stream);
 /* halves (element-major only, may be NULL) [2 l]: the second element's S
  * diagonal and rhs_neg terms of each row (zero on boundary rows), the
  * owner's going to diag / rhs_neg, all by plain stores; sum_halves then

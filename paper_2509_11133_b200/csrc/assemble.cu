@@ -547,21 +547,104 @@ __global__ void __launch_bounds__(128)
 // in flight and the S rows they scatter into stay in an L2-resident window),
 // FastDiv division.  Elements whose operands left the exact window are
 // appended to redo_list.
+// One red refinement of element t written by the assembly kernel itself
+// (refine.cu's refine_staged per-parent body, refine.cpp:16-74): the
+// element's nodes and coordinates are what the assembly loads anyway, and
+// its 12 children (192 B) and new nodes are plain stores that the
+// fp64-bound kernel issues beside its arithmetic, instead of a separate
+// HBM-bound pass re-reading the mesh and the edge tables.  Children 1..11
+// go to ne + 11 t + k as in refine_staged, one 176-byte run per thread (L2
+// merges the lanes' partial sectors).
+struct RefineOut {
+    int64_t nc;                        // parent nodes (child ids start there)
+    const int32_t* edge_first;         // 6 per element: first-occurrence slot
+    const int32_t* edge_of_slot;       // 6 per element: edge id
+    const int64_t* edge_off;           // low word: edges first seen before t
+    double* coords_out;                // child coordinates (parents copied)
+    int32_t* tets_out;                 // 12 ne child rows
+};
+__device__ __forceinline__ void refine_elem(int64_t t, int64_t ne, const double* __restrict__ coords,
+                                            const int32_t* __restrict__ tets, const RefineOut& ro) {
+    const int2* ef2 = reinterpret_cast<const int2*>(ro.edge_first) + 3 * t;
+    const int2* eo2 = reinterpret_cast<const int2*>(ro.edge_of_slot) + 3 * t;
+    const int2 f01 = __ldg(ef2), f23 = __ldg(ef2 + 1), f45 = __ldg(ef2 + 2);
+    const int2 o01 = __ldg(eo2), o23 = __ldg(eo2 + 1), o45 = __ldg(eo2 + 2);
+    const int64_t c = ro.nc + t + (uint32_t)__ldg(ro.edge_off + t);
+    const int4 e = ldtet(tets, t);
+    const V3 p[4] = {ldnode(coords, e.x), ldnode(coords, e.y), ldnode(coords, e.z), ldnode(coords, e.w)};
+    const V3 ct = vdiv(vadd(vadd(vadd(p[0], p[1]), p[2]), p[3]), 4.0);  // refine.cpp:33-34
+    double* const co = ro.coords_out;
+    co[3 * c] = ct.x;
+    co[3 * c + 1] = ct.y;
+    co[3 * c + 2] = ct.z;
+    const int32_t fs[6] = {f01.x, f01.y, f23.x, f23.y, f45.x, f45.y};
+    const int32_t os[6] = {o01.x, o01.y, o23.x, o23.y, o45.x, o45.y};
+    int32_t mid[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        const int64_t sl = 6 * t + k;
+        const int64_t node = ro.nc + fs[k] / 6 + 1 + os[k];
+        PHG_CHECK(fs[k] >= 0 && fs[k] <= (int32_t)sl && os[k] >= 0 && node < c + 7);
+        mid[k] = (int32_t)node;
+        if (fs[k] == (int32_t)sl) {
+            const int a = k < 3 ? 0 : (k < 5 ? 1 : 2);
+            const int b = k < 3 ? k + 1 : (k < 5 ? k - 1 : 3);
+            const V3 pm = vdiv(vadd(p[a], p[b]), 2.0);  // refine.cpp:43
+            co[3 * node] = pm.x;
+            co[3 * node + 1] = pm.y;
+            co[3 * node + 2] = pm.z;
+        }
+    }
+    const int32_t i = e.x, j = e.y, k = e.z, l = e.w;
+    const int32_t ij = mid[0], ik = mid[1], il = mid[2], jk = mid[3], jl = mid[4], kl = mid[5];
+    const int32_t cc = (int32_t)c;
+    int4* const out = reinterpret_cast<int4*>(ro.tets_out);
+#ifdef PHG_REFINE_CS
+#define PHG_ST4(p, v) __stcs(p, v)
+#else
+#define PHG_ST4(p, v) (*(p) = (v))
+#endif
+    PHG_ST4(out + t, make_int4(i, ij, ik, il));  // child 0 keeps slot t
+    int4* const rest = out + ne + 11 * t;  // refine.cpp:58-61
+    PHG_ST4(rest + 0, make_int4(j, jk, ij, jl));
+    PHG_ST4(rest + 1, make_int4(k, ik, jk, kl));
+    PHG_ST4(rest + 2, make_int4(l, kl, jl, il));
+    PHG_ST4(rest + 3, make_int4(ij, ik, il, cc));
+    PHG_ST4(rest + 4, make_int4(jk, ij, jl, cc));
+    PHG_ST4(rest + 5, make_int4(ik, jk, kl, cc));
+    PHG_ST4(rest + 6, make_int4(kl, jl, il, cc));
+    PHG_ST4(rest + 7, make_int4(ij, jk, ik, cc));
+    PHG_ST4(rest + 8, make_int4(ik, kl, il, cc));
+    PHG_ST4(rest + 9, make_int4(ij, il, jl, cc));
+    PHG_ST4(rest + 10, make_int4(kl, jk, jl, cc));
+#undef PHG_ST4
+}
+
 template <int KIND, bool ELEM>
+#ifdef PHG_COND_MAXREG
+__global__ void __maxnreg__(PHG_COND_MAXREG)
+#else
 __global__ void __launch_bounds__(kCondThreads, PHG_COND_MINB)
+#endif
     assemble_k(int64_t ne, const double* __restrict__ coords, const int32_t* __restrict__ tets, phg_problem prob,
                const int32_t* __restrict__ face_of_slot, const int32_t* __restrict__ slot_mate,
                const int32_t* __restrict__ face_mrow, const double* __restrict__ face_area,
                const double* __restrict__ face_bval, double* __restrict__ rhs, SchurOut so,
                double* __restrict__ rhs_neg, double* __restrict__ bd, double* __restrict__ a_blocks,
                double* __restrict__ slot_coef, int32_t* __restrict__ slot_mrow, int32_t* __restrict__ redo_list,
-               int32_t* __restrict__ redo_count, unsigned long long* err) {
+               int32_t* __restrict__ redo_count, unsigned long long* err, RefineOut ro) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= ne) return;
+#ifndef PHG_REFINE_AT_END
+    if (ro.tets_out) refine_elem(t, ne, coords, tets, ro);
+#endif
     FastDiv fd;
     const int st = assemble_elem<KIND, ELEM>(t, coords, tets, prob,
                                              {face_of_slot, slot_mate, face_mrow, face_area, face_bval}, a_blocks, so,
                                              rhs_neg, bd, rhs, slot_coef, slot_mrow, fd);
+#ifdef PHG_REFINE_AT_END
+    if (ro.tets_out) refine_elem(t, ne, coords, tets, ro);
+#endif
     if (st == 1) redo_list[atomicAdd(redo_count, 1)] = (int32_t)t;
     // "degenerate element block" (solver.cpp:103-109)
     if (st == 2) report(err, PHG_ERR_SINGULAR, (unsigned long long)t);
@@ -745,8 +828,16 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
                                            int32_t* sell_col, double* sell_val, double* st_val, double* diag,
                                            double* rhs_neg, double* bd, double* rhs, double* a_blocks,
                                            double* slot_coef, int32_t* slot_mrow, int32_t* redo, double* halves,
-                                           unsigned long long* err, void* ev_begin, void* ev_end, void* stream) {
+                                           unsigned long long* err, const phg_refine_out* refine, void* ev_begin,
+                                           void* ev_end, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
+    RefineOut ro{0, nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (refine) {
+        ro = {refine->nc, refine->edge_first, refine->edge_of_slot, refine->edge_off, refine->coords_out,
+              refine->tets_out};
+        cudaMemcpyAsync(refine->coords_out, coords, (size_t)(3 * refine->nc) * sizeof(double),
+                        cudaMemcpyDeviceToDevice, s);
+    }
     if (ne == 0) {
         // nothing to assemble; the caller's events still bracket the (empty) kernel
         if (ev_begin) cudaEventRecord((cudaEvent_t)ev_begin, s);
@@ -767,7 +858,7 @@ extern "C" int phfem_gpu_assemble_condense(int64_t ne, int64_t l, const double* 
 #define PHG_ASM(K, E)                                                                                                \
     assemble_k<K, E><<<grid, kCondThreads, 0, s>>>(ne, coords, tets, p, face_of_slot, slot_mate, face_mrow,          \
                                                    face_area, face_bval, rhs, so, rhs_neg, bd, a_blocks, slot_coef,  \
-                                                   slot_mrow, redo + 1, redo, err);                                  \
+                                                   slot_mrow, redo + 1, redo, err, ro);                              \
     if (ev_end) cudaEventRecord((cudaEvent_t)ev_end, s);                                                             \
     assemble_redo_k<K, E><<<kSMs, kCondThreads, 0, s>>>(redo + 1, redo, coords, tets, p, face_of_slot, slot_mate,    \
                                                         face_mrow, face_area, face_bval, rhs, so, rhs_neg, bd,       \

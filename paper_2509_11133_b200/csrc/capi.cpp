@@ -936,6 +936,16 @@ void* phfem_stream(void) {
     }
 }
 
+// PHFEM_FUSED_REFINE=0 keeps the separate refinement kernel in the pipeline
+// pass (A/B measurements)
+static bool fused_refine_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PHFEM_FUSED_REFINE");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms, int64_t counts[5]) {
     return guarded([&] {
         if (!mesh) throw InvalidArgument("null mesh");
@@ -953,14 +963,25 @@ int phfem_pipeline(phfem_mesh* mesh, int problem, int flags, phfem_stage_ms* ms,
         mesh->invalidate();
         build_connectivity(*mesh->data(), *c, true, &st);
         mesh->conn = c;
+        // with both stages asked for, the assembly kernel writes the child's
+        // elements and coordinates itself (assemble.cu: refine_elem); the
+        // refinement stage is then the boundary lists alone
+        const bool fused = do_refine && do_assemble && fused_refine_enabled();
+        if (do_refine && !mesh->scratch_child) mesh->scratch_child = child_pool().take();
         if (do_assemble) {
-            assemble_system(*mesh->data(), *mesh->coef, *c, problem, *s, false, &st);
+            const MeshData& m = *mesh->data();
+            phg_refine_out ro{};
+            if (fused) {
+                prepare_child(m, *c, mesh->scratch_child);
+                ro = {m.nc, c->edge_first.p, c->edge_of_slot.p, c->edge_off.p, mesh->scratch_child->coords.p,
+                      mesh->scratch_child->tets.p};
+            }
+            assemble_system(m, *mesh->coef, *c, problem, *s, false, &st, fused ? &ro : nullptr);
             mesh->sys = s;
         }
         int64_t ne_child = 0;
         if (do_refine) {
-            if (!mesh->scratch_child) mesh->scratch_child = child_pool().take();
-            auto child = refine_mesh(*mesh->data(), *c, nullptr, &st, mesh->scratch_child);
+            auto child = refine_mesh(*mesh->data(), *c, nullptr, &st, mesh->scratch_child, fused);
             ne_child = child->ne;
         }
         const double tot = total.stop_ms();

@@ -324,15 +324,13 @@ void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* 
 
 // -------------------------------------------------------------- refinement
 
-std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st,
-                                      std::shared_ptr<MeshData> into) {
+std::shared_ptr<MeshData> prepare_child(const MeshData& m, const Connectivity& c, std::shared_ptr<MeshData> into) {
     if (!c.has_edges) throw MeshError("refine_mesh: edge table missing");
     const int64_t nc2 = m.nc + c.ned + m.ne;
     const int64_t ne2 = 12 * m.ne;
     if (nc2 >= (int64_t)INT32_MAX || 6 * ne2 >= (int64_t)INT32_MAX)
         throw MeshError("out of memory while refining to level " + std::to_string(m.level + 1) +
                         ": 32-bit node/element ids exhausted");
-    cudaEvent_t t0 = st ? st->mark() : nullptr;
     auto out = into ? into : std::make_shared<MeshData>();
     out->nc = nc2;
     out->ne = ne2;
@@ -343,16 +341,25 @@ std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, Refine
     out->tets.alloc(4 * ne2);
     out->db.alloc(3 * out->nd);
     out->nb.alloc(3 * out->nn);
+    return out;
+}
+
+std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st,
+                                      std::shared_ptr<MeshData> into, bool elements_written) {
+    if (elements_written && (map || !into)) throw InvalidArgument("refine_mesh: fused elements need the prepared child");
+    cudaEvent_t t0 = st ? st->mark() : nullptr;
+    auto out = elements_written ? into : prepare_child(m, c, into);
     if (map) {
         map->midpoint.alloc(c.ned);
         map->centroid.alloc(m.ne);
     }
     Work& w = c.w;
     reset_err(w);
-    check(phfem_gpu_refine(m.nc, m.ne, m.coords.p, m.tets.p, c.edge_first.p, c.edge_of_slot.p, c.edge_off.p,
-                           out->coords.p, out->tets.p, map ? map->midpoint.p : nullptr,
-                           map ? map->centroid.p : nullptr, SV()),
-          "refine");
+    if (!elements_written)
+        check(phfem_gpu_refine(m.nc, m.ne, m.coords.p, m.tets.p, c.edge_first.p, c.edge_of_slot.p, c.edge_off.p,
+                               out->coords.p, out->tets.p, map ? map->midpoint.p : nullptr,
+                               map ? map->centroid.p : nullptr, SV()),
+              "refine");
     if (c.has_faces) {
         // classified: each list entry's face and its owner element are known
         check(phfem_gpu_refine_boundary_owned(m.nd, m.db.p, 0, m.nc, c.entry_face.p, c.face_slots.p, m.tets.p,
@@ -411,7 +418,7 @@ void System::finish() const {
 }
 
 void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
-                     bool debug_views, Stages* st) {
+                     bool debug_views, Stages* st, const phg_refine_out* refine) {
     if (!c.has_faces) throw MeshError("assemble: face table missing");
     if (problem < 0 || problem > 5) throw InvalidArgument("unknown problem id " + std::to_string(problem));
     cudaEvent_t t0 = st ? st->mark() : nullptr;
@@ -464,8 +471,8 @@ void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, i
                                       sys.elem ? nullptr : sys.sell_val.p, sys.elem ? sys.st_val.p : nullptr,
                                       sys.elem ? sys.diag.p : nullptr, sys.rhs_neg.p, sys.bd.p, sys.rhs.p,
                                       debug_views ? sys.a_blocks.p : nullptr, debug_views ? sys.slot_coef.p : nullptr,
-                                      sys.slot_mrow.p, w.redo.p, sys.elem ? sys.halves.p : nullptr, w.err.p, ka, kb,
-                                      SV()),
+                                      sys.slot_mrow.p, w.redo.p, sys.elem ? sys.halves.p : nullptr, w.err.p, refine,
+                                      ka, kb, SV()),
           "assemble");
     sys.split = sys.elem;
     if (st) {

@@ -298,11 +298,17 @@ std::shared_ptr<MeshData> kuhn_mesh(int nx, int ny, int nz, double lx, double ly
 // the boundary classification and multiplier rows)
 void build_connectivity(const MeshData& m, Connectivity& c, bool faces, Stages* st = nullptr, bool classify = true);
 // red refinement; needs edges.  `into` (optional) is reused for the child.
+// `elements_written`: the child's elements and coordinates were written by
+// the assembly kernel (prepare_child + assemble_system's refine argument);
+// only the boundary lists are refined here.
 std::shared_ptr<MeshData> refine_mesh(const MeshData& m, Connectivity& c, RefineMap* map, Stages* st = nullptr,
-                                      std::shared_ptr<MeshData> into = nullptr);
-// fused assembly + condensation
+                                      std::shared_ptr<MeshData> into = nullptr, bool elements_written = false);
+// the child mesh of one red refinement, sized and allocated (contents unset)
+std::shared_ptr<MeshData> prepare_child(const MeshData& m, const Connectivity& c, std::shared_ptr<MeshData> into);
+// fused assembly + condensation (+ the child's elements and coordinates
+// when `refine` is given)
 void assemble_system(const MeshData& m, const Coefs& k, const Connectivity& c, int problem, System& sys,
-                     bool debug_views, Stages* st = nullptr);
+                     bool debug_views, Stages* st = nullptr, const phg_refine_out* refine = nullptr);
 phg_problem device_problem(const Coefs& k, int problem);
 
 struct SolveResult {
